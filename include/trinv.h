@@ -1,0 +1,131 @@
+/*
+ * trinv.h — C ABI of the B200-native FP64 triangular-inverse library
+ * (hot path of arXiv 2307.07611, "fast inversion" of triangular matrices).
+ *
+ * Citations are to /root/reference/PAPER.md lines (P:NNN) with the section,
+ * equation or algorithm they fall in; DESIGN.md lists the readings used where
+ * the paper is silent (C1..C21 there).
+ *
+ * Conventions for every entry point
+ *  - All matrices are IEEE fp64, ROW-MAJOR: element (i, j) of a matrix with
+ *    leading dimension ld lives at ptr[i*ld + j], 0 <= i, j < n, ld >= n.
+ *  - Matrix pointers (A, X, L, U, workspace) are DEVICE pointers; `stream`
+ *    is a cudaStream_t (0 = legacy default stream).  Every call only ENQUEUES
+ *    work on `stream` and returns; completion is observed through the stream.
+ *  - Ownership: the caller allocates and frees every buffer.  The library
+ *    never allocates device memory on the call path and keeps no pointer after
+ *    returning.  Buffers must stay alive until the enqueued work completes.
+ *  - Only the referenced triangle of an input is read (the other triangle may
+ *    hold anything, including NaN).  With diag == TRINV_UNIT the stored
+ *    diagonal is not read and is taken as 1 (CRIT*, Alg. 2).
+ *  - Outputs are FULL matrices: the triangle opposite to the inverse's is
+ *    written as +0.0 (Thm 1 "0, otherwise"; Eq. defT).
+ *  - Synchronous errors (returned before anything is enqueued): see
+ *    trinv_status_t.  n == 0 (or batch == 0) is a no-op returning TRINV_OK.
+ *  - Asynchronous numerical status: an exact zero on a referenced diagonal
+ *    ("If R_jj = 0 stop", P:713-714 / P:731-732) is reported through d_info
+ *    (device int32, may be NULL) as 1 + the smallest such row index, 0 if
+ *    none (LAPACK trtri convention).  The output of a singular input is
+ *    unspecified (Inf/NaN).  NaN/Inf inputs propagate.  No host sync occurs.
+ *  - Entry points are re-entrant and thread-safe; they may be called on any
+ *    device (the current device is used).
+ */
+#ifndef TRINV_H
+#define TRINV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TRINV_OK = 0,
+  TRINV_INVALID_ARG = 1,          /* n<0, ld<n, batch<0, stride too small, NULL with n>0, bad op/uplo */
+  TRINV_ALIASING = 2,             /* input and output ranges overlap (non-batched calls) */
+  TRINV_WORKSPACE_TOO_SMALL = 3,  /* ws_bytes < trinv_workspace_bytes(...) */
+  TRINV_CUDA_ERROR = 4,           /* a CUDA launch or API call failed; see trinv_last_cuda_error() */
+  TRINV_NOT_SUPPORTED = 5         /* request outside the implemented envelope (e.g. batched n > 32) */
+} trinv_status_t;
+
+typedef enum { TRINV_NON_UNIT = 0, TRINV_UNIT = 1 } trinv_diag_t;
+
+/* Device workspace (bytes) needed by trinv_lower ('L'), trinv_upper ('U') or
+ * inv_from_lu ('G') for order n.  A / X are the matrices that will be passed
+ * (only their addresses' 16-byte alignment is inspected; NULL means
+ * "aligned") with leading dimensions lda / ldx: an odd leading dimension or a
+ * misaligned pointer makes the call stage that matrix through the workspace.
+ * For 'G', A = L factor, X = output; the U factor is assumed laid out like L.
+ * Returns 0 for n <= 0 or an unknown op. */
+size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx);
+
+/* X = L^{-1} for a non-singular LOWER-triangular L (n x n).
+ * Method: COMBRIT with beta = 2 (Alg. 1), i.e.
+ * the recursive split inv([A 0; C B]) = [A^{-1} 0; -B^{-1} C A^{-1}  B^{-1}]
+ * (the transpose of P:1066-1069), bottom-up over levels; 32-wide diagonal
+ * leaves are inverted in shared memory by the column recurrence of the proof
+ * of Thm 1 (CRIT, Alg. 3); the off-diagonal products
+ * run on the FP64 tensor cores (DMMA) fed by TMA.
+ *   A, lda : input (device, read-only), only the lower triangle is read.
+ *   X, ldx : output (device), full n x n written; must not overlap A
+ *            (TRINV_ALIASING).
+ *   ws     : device workspace of ws_bytes >= trinv_workspace_bytes('L', ...);
+ *            may be NULL when that size is 0.
+ *   d_info : device int32 or NULL (see above). */
+trinv_status_t trinv_lower(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                           trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info,
+                           void* stream);
+
+/* X = U^{-1} for a non-singular UPPER-triangular U; the mirror image of
+ * trinv_lower: inv([A B; 0 C]) = [A^{-1}  -A^{-1} B C^{-1}; 0 C^{-1}]
+ * (P:1066-1069).  Same arguments and rules as trinv_lower (op 'U'). */
+trinv_status_t trinv_upper(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                           trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info,
+                           void* stream);
+
+/* Batched small inverses: for b in [0, batch): X_b = T_b^{-1}, T_b at
+ * A + b*strideA (leading dim lda), X_b at X + b*strideX (leading dim ldx).
+ * uplo 'L' or 'U'; 1 <= n <= 32 (TRINV_NOT_SUPPORTED above).  One warp owns
+ * one matrix; lane j computes column j by the recurrence of P:243 (CRIT for
+ * the upper case) in registers with the matrix staged in shared
+ * memory by 1-D TMA bulk copies (cp.async.bulk) when n, lda, ldx, the strides
+ * are even and the pointers 16-byte aligned, else by plain loads.
+ * X == A exactly (in-place, same ld and stride) is allowed; any other overlap
+ * is undefined.  strideA >= n*lda and strideX >= n*ldx are required.
+ * d_info: NULL or device int32[batch], one status per matrix. */
+trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* A, int64_t lda,
+                             int64_t strideA, double* X, int64_t ldx, int64_t strideX,
+                             trinv_diag_t diag, int32_t* d_info, void* stream);
+
+/* General inverse from triangular factors, X = (L U)^{-1} = U^{-1} L^{-1}
+ * (SKUL, "S K = A^{-1}" with S = U^{-1}, K = L^{-1}): L^{-1} and
+ * U^{-1} by the two calls above, then the upper x lower product
+ * X_ij = sum_{k >= max(i,j)} (U^{-1})_ik (L^{-1})_kj  (P_UL)
+ * on the DMMA engine.  Lf (lower, ldl) and Uf (upper, ldu) are read-only; X
+ * (ldx) must not overlap either (TRINV_ALIASING).  diagL / diagU select unit
+ * factors (the paper's Crout makes U unit; BASELINE config 4 makes L
+ * unit).  ws_bytes >= trinv_workspace_bytes('G', n, Lf, ldl, X, ldx).
+ * d_info reports a zero diagonal of L first (1+i), then of U (n+1+i). */
+trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu,
+                           double* X, int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU,
+                           void* ws, size_t ws_bytes, int32_t* d_info, void* stream);
+
+/* Static description of a status code. */
+const char* trinv_status_string(trinv_status_t s);
+
+/* The last CUDA error code seen by this thread's calls (0 if none). */
+int trinv_last_cuda_error(void);
+
+/* Library version string, e.g. "trinv-b200 0.1 sm_100a". */
+const char* trinv_version(void);
+
+/* Observability: number of kernel launches enqueued by this thread's calls
+ * since the last reset (used by bench.py for its "gpu_launches" count). */
+int64_t trinv_launch_count(void);
+void trinv_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRINV_H */

@@ -1,0 +1,152 @@
+"""paper_2307_07611_b200 — B200-native FP64 triangular inversion (arXiv 2307.07611 hot path).
+
+Thin Python binding over the C ABI in include/trinv.h (libtrinv.so, built in-tree
+for sm_100a).  This module only marshals arguments: shapes, leading dimensions,
+device pointers, the current CUDA stream and a workspace allocated through torch.
+Every arithmetic step runs in the library's CUDA kernels; there is no CPU or
+PyTorch fallback — if libtrinv.so is missing or no GPU is present the calls raise.
+
+    X = trinv_lower(L)            # L^{-1}, full matrix, +0.0 above the diagonal
+    X = trinv_upper(U)            # U^{-1}
+    X = trinv_batched(A, "L")     # A: [B, n, n], n <= 32
+    X = inv_from_lu(L, U)         # (L U)^{-1} = U^{-1} L^{-1}, L unit by default
+"""
+import ctypes
+import os
+
+from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMatrixError,  # noqa: F401
+                   lib, so_path, status_string, launch_count, reset_launch_count)
+
+__all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "inv_from_lu", "workspace_bytes",
+           "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ld(t):
+    """Leading dimension of a row-major 2-D (or [B, n, n]) CUDA float64 tensor."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64:
+        raise TypeError("expected a torch.float64 tensor")
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (device memory); host buffers: copy with .cuda() first")
+    if t.shape[-1] > 1 and t.stride(-1) != 1:
+        raise ValueError("row-major layout required (stride(-1) == 1)")
+    return max(t.stride(-2), t.shape[-1]) if t.shape[-2] > 1 else t.shape[-1]
+
+
+def _stream(stream):
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(st):
+    if st != TRINV_OK:
+        raise TrinvError(st)
+
+
+def workspace_bytes(op, n, A=None, lda=None, X=None, ldx=None):
+    """Device workspace bytes for op 'L' | 'U' | 'G' (see trinv_workspace_bytes)."""
+    pa = ctypes.c_void_p(A.data_ptr()) if A is not None else None
+    px = ctypes.c_void_p(X.data_ptr()) if X is not None else None
+    lda = n if lda is None else lda
+    ldx = n if ldx is None else ldx
+    return lib().trinv_workspace_bytes(op.encode(), n, pa, lda, px, ldx)
+
+
+def _alloc_ws(nbytes, device):
+    torch = _torch()
+    if nbytes == 0:
+        return None, 0
+    w = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    return w, nbytes
+
+
+def _info(check, device):
+    torch = _torch()
+    return torch.zeros(1, dtype=torch.int32, device=device) if check else None
+
+
+def _raise_info(info, what):
+    if info is not None:
+        v = int(info.item())
+        if v != 0:
+            raise SingularMatrixError(v, what)
+
+
+def _tri(uplo, A, unit, out, check, stream):
+    torch = _torch()
+    n = A.shape[-1]
+    if A.dim() != 2 or A.shape[0] != n:
+        raise ValueError("expected a square 2-D matrix")
+    lda = _ld(A)
+    X = torch.empty((n, n), dtype=torch.float64, device=A.device) if out is None else out
+    ldx = _ld(X)
+    ws, wsb = _alloc_ws(workspace_bytes(uplo, n, A, lda, X, ldx), A.device)
+    info = _info(check, A.device)
+    f = lib().trinv_lower if uplo == "L" else lib().trinv_upper
+    _check(f(n, ctypes.c_void_p(A.data_ptr()), lda, ctypes.c_void_p(X.data_ptr()), ldx,
+             TRINV_UNIT if unit else TRINV_NON_UNIT,
+             ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+             ctypes.c_void_p(info.data_ptr()) if info is not None else None, _stream(stream)))
+    _raise_info(info, "trinv_lower" if uplo == "L" else "trinv_upper")
+    return X
+
+
+def trinv_lower(A, *, unit=False, out=None, check=False, stream=None):
+    """X = A^{-1} for lower-triangular A (only the lower triangle is used)."""
+    return _tri("L", A, unit, out, check, stream)
+
+
+def trinv_upper(A, *, unit=False, out=None, check=False, stream=None):
+    """X = A^{-1} for upper-triangular A (only the upper triangle is used)."""
+    return _tri("U", A, unit, out, check, stream)
+
+
+def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None):
+    """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 32.  Returns X, or (X, info[B]) if info."""
+    torch = _torch()
+    if A.dim() != 3 or A.shape[1] != A.shape[2]:
+        raise ValueError("expected [B, n, n]")
+    B, n = A.shape[0], A.shape[1]
+    lda = _ld(A)
+    X = torch.empty_like(A, memory_format=torch.contiguous_format) if out is None else out
+    ldx = _ld(X)
+    sa = A.stride(0) if B > 1 else n * lda
+    sx = X.stride(0) if B > 1 else n * ldx
+    inf = torch.empty(B, dtype=torch.int32, device=A.device) if info else None
+    _check(lib().trinv_batched(uplo.encode(), n, B, ctypes.c_void_p(A.data_ptr()), lda, sa,
+                               ctypes.c_void_p(X.data_ptr()), ldx, sx,
+                               TRINV_UNIT if unit else TRINV_NON_UNIT,
+                               ctypes.c_void_p(inf.data_ptr()) if inf is not None else None,
+                               _stream(stream)))
+    return (X, inf) if info else X
+
+
+def inv_from_lu(L, U, *, unit_l=True, unit_u=False, out=None, check=False, stream=None):
+    """X = (L U)^{-1} = U^{-1} L^{-1} from a lower factor L and an upper factor U."""
+    torch = _torch()
+    n = L.shape[-1]
+    if L.shape != (n, n) or U.shape != (n, n):
+        raise ValueError("expected two n x n factors")
+    ldl, ldu = _ld(L), _ld(U)
+    X = torch.empty((n, n), dtype=torch.float64, device=L.device) if out is None else out
+    ldx = _ld(X)
+    nb = workspace_bytes("G", n, L, ldl, X, ldx)
+    nb = max(nb, lib().trinv_workspace_bytes(b"G", n, ctypes.c_void_p(U.data_ptr()), ldu,
+                                             ctypes.c_void_p(X.data_ptr()), ldx))
+    ws, wsb = _alloc_ws(nb, L.device)
+    info = _info(check, L.device)
+    _check(lib().inv_from_lu(n, ctypes.c_void_p(L.data_ptr()), ldl, ctypes.c_void_p(U.data_ptr()), ldu,
+                             ctypes.c_void_p(X.data_ptr()), ldx,
+                             TRINV_UNIT if unit_l else TRINV_NON_UNIT,
+                             TRINV_UNIT if unit_u else TRINV_NON_UNIT,
+                             ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+                             ctypes.c_void_p(info.data_ptr()) if info is not None else None,
+                             _stream(stream)))
+    _raise_info(info, "inv_from_lu")
+    return X

@@ -1,0 +1,80 @@
+"""ctypes loader for libtrinv.so (the C ABI of include/trinv.h).  Loading fails
+loudly when the library has not been built: there is no fallback path."""
+import ctypes
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+HEADER = os.path.join(HERE, "..", "include", "trinv.h")
+_SO = os.path.join(HERE, "libtrinv.so")
+
+TRINV_OK, TRINV_INVALID_ARG, TRINV_ALIASING, TRINV_WORKSPACE_TOO_SMALL, TRINV_CUDA_ERROR, TRINV_NOT_SUPPORTED = range(6)
+TRINV_NON_UNIT, TRINV_UNIT = 0, 1
+_lib = None
+
+_i64, _vp, _sz, _i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+
+
+class TrinvError(RuntimeError):
+    def __init__(self, status):
+        self.status = status
+        msg = status_string(status)
+        if status == TRINV_CUDA_ERROR:
+            msg += f" (cudaError {lib().trinv_last_cuda_error()})"
+        super().__init__(msg)
+
+
+class SingularMatrixError(ArithmeticError):
+    def __init__(self, info, what=""):
+        self.info = info
+        super().__init__(f"{what}: exact zero on the diagonal (info = {info})")
+
+
+def so_path():
+    return _SO
+
+
+def lib():
+    """Load libtrinv.so (build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(_SO)
+    L.trinv_workspace_bytes.argtypes = [ctypes.c_char, _i64, _vp, _i64, _vp, _i64]
+    L.trinv_workspace_bytes.restype = _sz
+    for name in ("trinv_lower", "trinv_upper"):
+        f = getattr(L, name)
+        f.argtypes = [_i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]
+        f.restype = _i32
+    L.trinv_batched.argtypes = [ctypes.c_char, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp]
+    L.trinv_batched.restype = _i32
+    L.inv_from_lu.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _vp]
+    L.inv_from_lu.restype = _i32
+    L.trinv_status_string.argtypes = [_i32]
+    L.trinv_status_string.restype = ctypes.c_char_p
+    L.trinv_last_cuda_error.restype = _i32
+    L.trinv_version.restype = ctypes.c_char_p
+    L.trinv_launch_count.restype = _i64
+    _lib = L
+    return L
+
+
+def status_string(st):
+    return lib().trinv_status_string(st).decode()
+
+
+def launch_count():
+    return lib().trinv_launch_count()
+
+
+def reset_launch_count():
+    lib().trinv_reset_launch_count()
+
+
+def declared_symbols():
+    """Function names declared in include/trinv.h."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(\w+)\s*\(", src)) - {"if", "defined", "sizeof"})

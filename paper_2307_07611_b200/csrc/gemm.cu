@@ -1,0 +1,286 @@
+// gemm.cu — the off-diagonal products of the recursive split on the FP64
+// tensor cores (DESIGN.md §Kernels "K_trmm").
+//
+// One launch covers every merge of one recursion level (COMBRIT with
+// beta = 2, Alg. 1: the n/(2b) merges of a level are independent,
+// P:499-500).  Per merge at offset s with halves b (first) and r (second):
+//   lower  inv([A 0; C B]) = [A^{-1} 0; -B^{-1} C A^{-1}  B^{-1}]
+//     MODE_LOWER_1:  W   = C . A^{-1}       tile (I,J): k in [J*BN, b)       (A^{-1} lower)
+//     MODE_LOWER_2:  X21 = -B^{-1} . W      tile (I,J): k in [0, (I+1)*BM)   (B^{-1} lower)
+//   upper  inv([A B; 0 C]) = [A^{-1}  -A^{-1} B C^{-1}; 0 C^{-1}]
+//     MODE_UPPER_1:  W   = A^{-1} . B       tile (I,J): k in [I*BM, b)
+//     MODE_UPPER_2:  X12 = -W . C^{-1}      tile (I,J): k in [0, (J+1)*BN)
+//   general from factors (SKUL S K = A^{-1}; P_UL)
+//     MODE_UL:       X = U^{-1} . L^{-1}    tile (I,J): k in [max(I*BM, J*BN), n)
+// The K-ranges skip the structurally-zero blocks of the triangular operand
+// (P_TF = m^3); diagonal tiles are multiplied densely on the
+// explicit zeros written by the previous level.  LOWER_2 / UPPER_2 also write
+// +0.0 over the mirrored tile of the opposite triangle (row a7).
+//
+// Engine: CTA tile BM x BN, K-step BK = 16, STAGES-deep smem ring filled by
+// TMA (cp.async.bulk.tensor.2d) from a producer warp through full/empty
+// mbarriers; WM x WN consumer warps issue mma.sync.m8n8k4.f64 (DMMA.8x8x4).
+// A tiles: one box (16 x BM) with 128-byte swizzle -> conflict-free fragment
+// loads; B tiles: BN/8 boxes (8 x 16), 64-byte rows -> conflict-free.
+// Out-of-range rows / columns (ragged last merge, n not a multiple of the
+// tile) are zero-filled by TMA and clipped at the store.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace trinv {
+
+constexpr int BK = 16;
+
+struct TileCoord {
+  int64_t a_row, a_col;  // A-operand: rows a_row.., columns a_col + k
+  int64_t b_row, b_col;  // B-operand: rows b_row + k, columns b_col..
+  int64_t o_row, o_col;  // output tile origin
+  int64_t m_row, m_col;  // mirror tile origin (rows BN x cols BM), if any
+  int64_t k_begin, k_end;
+  bool valid, mirror;
+};
+
+template <int BM, int BN>
+__device__ __forceinline__ TileCoord map_tile(const LevelArgs& p, int64_t t) {
+  TileCoord c{};
+  const int64_t b = p.b, n = p.n, merges = p.merges;
+  const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
+  int64_t g = 0, I = 0, J = 0;
+  c.valid = true;
+  c.mirror = false;
+  switch (p.mode) {
+    case MODE_LOWER_1: {  // longest K first: J ascending
+      J = t / (merges * TMmax);
+      const int64_t rem = t % (merges * TMmax);
+      g = rem / TMmax; I = rem % TMmax;
+    } break;
+    case MODE_LOWER_2: {  // I descending
+      I = TMmax - 1 - t / (merges * TNmax);
+      const int64_t rem = t % (merges * TNmax);
+      g = rem / TNmax; J = rem % TNmax;
+    } break;
+    case MODE_UPPER_1: {  // I ascending
+      I = t / (merges * TNmax);
+      const int64_t rem = t % (merges * TNmax);
+      g = rem / TNmax; J = rem % TNmax;
+    } break;
+    case MODE_UPPER_2: {  // J descending
+      J = TNmax - 1 - t / (merges * TMmax);
+      const int64_t rem = t % (merges * TMmax);
+      g = rem / TMmax; I = rem % TMmax;
+    } break;
+    default: {  // MODE_UL: max(I, J) ascending
+      int64_t m = (int64_t)sqrt((double)t);
+      while (m * m > t) --m;
+      while ((m + 1) * (m + 1) <= t) ++m;
+      const int64_t q = t - m * m;
+      if (q <= m) { I = m; J = q; } else { I = q - m - 1; J = m; }
+    } break;
+  }
+  const int64_t s = 2 * g * b;
+  const int64_t r = (p.mode == MODE_UL) ? n : (n - s - b < b ? n - s - b : b);  // second half
+  switch (p.mode) {
+    case MODE_LOWER_1:
+      c.valid = I * BM < r;
+      c.a_row = s + b + I * BM; c.a_col = s;
+      c.b_row = s; c.b_col = s + J * BN;
+      c.o_row = g * b + I * BM; c.o_col = J * BN;
+      c.k_begin = J * BN; c.k_end = b;
+      break;
+    case MODE_LOWER_2: {
+      c.valid = I * BM < r;
+      c.a_row = s + b + I * BM; c.a_col = s + b;
+      c.b_row = g * b; c.b_col = J * BN;
+      c.o_row = s + b + I * BM; c.o_col = s + J * BN;
+      c.mirror = true; c.m_row = s + J * BN; c.m_col = s + b + I * BM;
+      c.k_begin = 0; c.k_end = (I + 1) * BM < r ? (I + 1) * BM : r;
+    } break;
+    case MODE_UPPER_1:
+      c.valid = J * BN < r;
+      c.a_row = s + I * BM; c.a_col = s;
+      c.b_row = s; c.b_col = s + b + J * BN;
+      c.o_row = g * b + I * BM; c.o_col = J * BN;
+      c.k_begin = I * BM; c.k_end = b;
+      break;
+    case MODE_UPPER_2:
+      c.valid = J * BN < r;
+      c.a_row = g * b + I * BM; c.a_col = 0;
+      c.b_row = s + b; c.b_col = s + b + J * BN;
+      c.o_row = s + I * BM; c.o_col = s + b + J * BN;
+      c.mirror = true; c.m_row = s + b + J * BN; c.m_col = s + I * BM;
+      c.k_begin = 0; c.k_end = (J + 1) * BN < r ? (J + 1) * BN : r;
+      break;
+    default:
+      c.a_row = I * BM; c.a_col = 0;
+      c.b_row = 0; c.b_col = J * BN;
+      c.o_row = I * BM; c.o_col = J * BN;
+      c.k_begin = (I * BM > J * BN) ? I * BM : J * BN; c.k_end = n;
+      break;
+  }
+  return c;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int kConsumerWarps = WM * WN;
+  static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
+  static_assert(BM % BK == 0 && BN % BK == 0, "BK must divide BM and BN");
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+    dmma_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      const LevelArgs p) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BM][BK] swizzled
+  double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);  // [STAGES][BN/8][BK][8]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const TileCoord tc = map_tile<BM, BN>(p, blockIdx.x);
+  if (!tc.valid) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nk = (tc.k_end - tc.k_begin + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::kConsumerWarps) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&mapA);
+      tma_prefetch_desc(&mapB);
+      for (int64_t kt = 0; kt < nk; ++kt) {
+        const int s = (int)(kt % STAGES);
+        const int64_t use = kt / STAGES;
+        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const int64_t k = tc.k_begin + kt * BK;
+        tma_load_2d(sA + (size_t)s * BM * BK, &mapA, (int32_t)(tc.a_col + k), (int32_t)tc.a_row, &full[s]);
+        double* sb = sB + (size_t)s * BK * BN;
+#pragma unroll
+        for (int nb = 0; nb < BN / 8; ++nb)
+          tma_load_2d(sb + nb * BK * 8, &mapB, (int32_t)(tc.b_col + nb * 8), (int32_t)(tc.b_row + k), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  // Mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle.
+  if (tc.mirror) {
+    const int ctid = threadIdx.x;
+    constexpr int PAIRS = BM / 2;
+    for (int e = ctid; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
+      const int64_t row = tc.m_row + e / PAIRS, col = tc.m_col + 2 * (e % PAIRS);
+      if (row < p.n) {
+        double* q = p.mir + row * p.ldm + col;
+        if (col + 1 < p.n) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
+        else if (col < p.n) *q = 0.0;
+      }
+    }
+  }
+
+  const int wm = warp / WN, wn = warp % WN;
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int s = (int)(kt % STAGES);
+    mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
+    const unsigned char* a_st = reinterpret_cast<const unsigned char*>(sA + (size_t)s * BM * BK);
+    const double* b_st = sB + (size_t)s * BK * BN;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double af[C::FM], bf[C::FN];
+      const int kcol = kk * 4 + lc;  // column inside the 16-wide A box
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi) {
+        const int row = wm * C::WTM + mi * 8 + lr;
+        const int off = row * 128 + ((((kcol >> 1) ^ (row & 7)) << 4) | ((kcol & 1) << 3));
+        af[mi] = *reinterpret_cast<const double*>(a_st + off);
+      }
+#pragma unroll
+      for (int ni = 0; ni < C::FN; ++ni) {
+        const int box = (wn * C::WTN + ni * 8) >> 3;
+        bf[ni] = b_st[box * BK * 8 + kcol * 8 + lr];
+      }
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue: alpha * acc -> out (clipped) ----------------
+#pragma unroll
+  for (int mi = 0; mi < C::FM; ++mi) {
+    const int64_t row = tc.o_row + wm * C::WTM + mi * 8 + lr;
+    if (row >= p.out_rows) continue;
+    double* orow = p.out + row * p.ldo;
+#pragma unroll
+    for (int ni = 0; ni < C::FN; ++ni) {
+      const int64_t col = tc.o_col + wn * C::WTN + ni * 8 + 2 * lc;
+      const double v0 = p.alpha * acc[mi][ni][0], v1 = p.alpha * acc[mi][ni][1];
+      if (col + 1 < p.out_cols) *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
+      else if (col < p.out_cols) orow[col] = v0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES>
+static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  CUtensorMap mA, mB;
+  if (!encode_map(&mA, a.opA, BK, BM, true)) return cudaErrorInvalidValue;
+  if (!encode_map(&mB, a.opB, 8, BK, false)) return cudaErrorInvalidValue;
+  int64_t tiles;
+  if (a.mode == MODE_UL) {
+    const int64_t T = (a.n + BM - 1) / BM;
+    tiles = T * T;
+  } else {
+    tiles = a.merges * ((a.b + BM - 1) / BM) * ((a.b + BN - 1) / BN);
+  }
+  if (tiles <= 0) return cudaSuccess;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+  // Tile size follows the level: min(b, 128) (b is a power of two >= 32 for
+  // the triangular modes; UL uses 128).
+  const int64_t t = (a.mode == MODE_UL) ? 128 : (a.b < 128 ? a.b : 128);
+  if (t >= 128) return launch_cfg<128, 128, 2, 4, 5>(a, s, launches);
+  if (t >= 64) return launch_cfg<64, 64, 2, 2, 4>(a, s, launches);
+  return launch_cfg<32, 32, 2, 2, 4>(a, s, launches);
+}
+
+}  // namespace trinv

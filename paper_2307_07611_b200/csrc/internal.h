@@ -1,0 +1,60 @@
+// internal.h — launchers shared between the kernel translation units and the
+// C-ABI driver (trinv.cu).  Not part of the public ABI (include/trinv.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace trinv {
+
+// ---- leaf / batched kernels (leaf.cu) ------------------------------------------
+struct LeafArgs {
+  const double* A;
+  int64_t lda, sA;
+  double* X;
+  int64_t ldx, sX;
+  int64_t batch;    // number of matrices
+  int n;            // order of matrices 0..batch-2
+  int n_last;       // order of the last matrix (ragged leaf); == n for uniform batches
+  int unit;         // 1: unit diagonal (not read)
+  int32_t* info;    // NULL, per-matrix [batch], or a single accumulator
+  int info_mode;    // 0 none, 1 per matrix, 2 single min-nonzero of (info_off + b*info_stride + i + 1)
+  int64_t info_stride, info_off;
+};
+// Returns cudaError_t of the launch.  uplo 'L' or 'U'.  The TMA-staged path is
+// taken when every address and size it moves is 16-byte aligned.
+cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches);
+
+// ---- DMMA GEMM engine (gemm.cu) ---------------------------------------------------
+enum GemmMode : int {
+  MODE_LOWER_1 = 0,  // W   = C . A^{-1}          (C from input, A^{-1} lower from X)
+  MODE_LOWER_2 = 1,  // X21 = -B^{-1} . W         (B^{-1} lower from X), mirror X12 := 0
+  MODE_UPPER_1 = 2,  // W   = A^{-1} . B          (A^{-1} upper from X, B from input)
+  MODE_UPPER_2 = 3,  // X12 = -W . C^{-1}         (C^{-1} upper from X), mirror X21 := 0
+  MODE_UL = 4        // X   = U^{-1} . L^{-1}     (k >= max(i, j))
+};
+
+struct MatRef {
+  const double* ptr;
+  int64_t rows, cols, ld;  // bounds (elements) and leading dimension
+};
+
+struct LevelArgs {
+  int mode;
+  int64_t n;   // matrix order
+  int64_t b;   // level block size (size of the first half of every merge); == n for UL
+  int64_t merges;
+  MatRef opA, opB;  // operand matrices (TMA-read)
+  double* out;      // output matrix (row-major, ldo)
+  int64_t ldo, out_rows, out_cols;
+  double* mir;      // matrix whose mirrored tile is zero-filled (LOWER_2/UPPER_2), else NULL
+  int64_t ldm;
+  double alpha;
+};
+cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
+
+// Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
+// runtime's driver entry point).  Returns false on failure.
+bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, bool swizzle128);
+
+}  // namespace trinv

@@ -1,0 +1,126 @@
+"""Parity of trinv_batched against the CPU oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2307_07611_b200 as P  # noqa: E402
+from gpu_common import REL_TOL, RES_TOL  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _run(A, uplo="L", unit=False, **kw):
+    X, info = P.trinv_batched(torch.from_numpy(A).to(DEV), uplo, unit=unit, info=True, **kw)
+    torch.cuda.synchronize()
+    return X.cpu().numpy(), info.cpu().numpy()
+
+
+def test_config1_full_batch():
+    """BASELINE config 1: 131072 lower 32x32, matrix b seeded by b; every matrix checked."""
+    B = 131072
+    A = synth.host(32, batch=B)
+    X, info = _run(A)
+    R = oracle.crit_batched(A)
+    assert oracle.floored_rel_err(X, R) <= REL_TOL
+    assert np.all(info == 0)
+    idx = np.random.default_rng(0).choice(B, 512, replace=False)
+    assert oracle.residual_ratio(A[idx], X[idx]) <= RES_TOL
+    assert np.all(np.triu(X, 1) == 0.0)
+    # device-generated input (the bench path) equals the host generator bitwise
+    Ad = torch.empty((B, 32, 32), dtype=torch.float64, device=DEV)
+    synth.device_fill(Ad, 32)
+    assert torch.equal(Ad.cpu(), torch.from_numpy(A))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 17, 30, 31, 32])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_orders_and_uplo(n, uplo):
+    B = 6 * 148 * 2 + 5  # more than one matrix per warp, ragged tail
+    diag = "signed" if uplo == "L" else "pos"
+    A = synth.host(n, batch=B, uplo=uplo, diag=diag)
+    X, info = _run(A, uplo)
+    assert oracle.floored_rel_err(X, oracle.crit_batched(A, uplo)) <= REL_TOL
+    assert np.all(info == 0)
+    opp = np.triu(X, 1) if uplo == "L" else np.tril(X, -1)
+    assert np.all(opp == 0.0)
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_unit_ignores_diag_and_nan_other_triangle(uplo):
+    B, n = 1000, 32
+    A = synth.host(n, batch=B, uplo=uplo)
+    A1 = A.copy()
+    idx = np.arange(n)
+    A1[:, idx, idx] = 1.0
+    poisoned = A.copy()
+    poisoned[:, idx, idx] = np.nan
+    tri = np.triu_indices(n, 1) if uplo == "L" else np.tril_indices(n, -1)
+    poisoned[:, tri[0], tri[1]] = np.nan
+    X, _ = _run(poisoned, uplo, unit=True)
+    R = oracle.crit_batched(A1, uplo, unit=True)
+    assert oracle.floored_rel_err(X, R) <= REL_TOL
+    assert not np.isnan(X).any()
+
+
+def test_exact_pins():
+    # paper 4x4 inside a 32x32 identity-padded unit lower, bidiagonal s^(i-j), all-ones
+    T = np.array([[1, 2, 4, 1], [0, 1, 3, 2], [0, 0, 1, 5], [0, 0, 0, 1]], dtype=np.float64)
+    S = np.array([[1, -2, 2, -7], [0, 1, -3, 13], [0, 0, 1, -5], [0, 0, 0, 1]], dtype=np.float64)
+    A = np.zeros((3, 32, 32))
+    A[0] = np.eye(32); A[0, :4, :4] = T.T
+    A[1] = np.eye(32) - 0.5 * np.eye(32, k=-1)
+    A[2] = np.tril(np.ones((32, 32)))
+    X, _ = _run(A)
+    assert np.array_equal(X[0, :4, :4], S.T)
+    i, j = np.indices((32, 32))
+    assert np.array_equal(X[1], np.where(i >= j, 0.5 ** (i - j).astype(float), 0.0))
+    assert np.array_equal(X[2], np.eye(32) - np.eye(32, k=-1))
+    Xu, _ = _run(np.ascontiguousarray(np.transpose(A, (0, 2, 1))), "U")
+    assert np.array_equal(Xu[0, :4, :4], S)
+    # integer closure (Cor. 2): random unit +-1 lower, exact
+    rng = np.random.default_rng(5)
+    Ai = np.tril(rng.integers(-1, 2, size=(64, 32, 32)), -1).astype(np.float64) + np.eye(32)
+    Xi, _ = _run(Ai)
+    assert np.array_equal(Xi, oracle.crit_batched(Ai))
+    # diagonal: correctly rounded reciprocals, bitwise
+    d = 1.0 + rng.random((8, 32))
+    Ad = np.zeros((8, 32, 32)); Ad[:, np.arange(32), np.arange(32)] = d
+    Xd, _ = _run(Ad)
+    assert np.array_equal(Xd[:, np.arange(32), np.arange(32)], 1.0 / d)
+
+
+def test_strided_layouts_and_inplace():
+    B, n, ld = 300, 32, 40
+    A = synth.host(n, batch=B)
+    big = np.full((B, n, ld), np.nan)
+    big[:, :, :n] = A
+    At = torch.from_numpy(big).to(DEV)[:, :, :n]  # ld = 40, stride = 1280
+    X = P.trinv_batched(At)
+    assert oracle.floored_rel_err(X.cpu().numpy(), oracle.crit_batched(A)) <= REL_TOL
+    # odd leading dimension (plain-load path)
+    big2 = np.zeros((B, n, 33)); big2[:, :, :n] = A
+    X2 = P.trinv_batched(torch.from_numpy(big2).to(DEV)[:, :, :n])
+    assert oracle.floored_rel_err(X2.cpu().numpy(), oracle.crit_batched(A)) <= REL_TOL
+    # in place: X == A
+    Ai = torch.from_numpy(A.copy()).to(DEV)
+    P.trinv_batched(Ai, out=Ai)
+    assert oracle.floored_rel_err(Ai.cpu().numpy(), oracle.crit_batched(A)) <= REL_TOL
+
+
+def test_singular_info_and_determinism():
+    B = 50
+    A = synth.host(32, batch=B)
+    A[7, 5, 5] = 0.0
+    A[9, 31, 31] = 0.0
+    A[9, 3, 3] = 0.0
+    _, info = _run(A)
+    assert info[7] == 6 and info[9] == 4 and info[0] == 0
+    At = torch.from_numpy(synth.host(32, batch=4096)).to(DEV)
+    X1 = P.trinv_batched(At); X2 = P.trinv_batched(At)
+    assert torch.equal(X1, X2)
+    # sub-batch gives the same bits (sharding invariance, P-l)
+    X3 = P.trinv_batched(At[1000:1500].contiguous())
+    assert torch.equal(X3, X1[1000:1500])

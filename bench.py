@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the FP64 triangular-inverse hot path on B200.
+
+Default workload (BASELINE.json configs[1], the metric's batched case):
+131072 independent lower-triangular 32x32 fp64 matrices per GPU, matrix b
+seeded by its global index b, row-major contiguous, inverted by trinv_batched
+(one launch per step).  `value` = matrices inverted by all ranks / max-over-
+ranks device time, inverses/s.  --config 0|2|3|4 runs the single-matrix
+configurations (GFLOP/s at n^3/3 per triangular inverse, 4n^3/3 for config 4)
+as separate lines.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Multi-GPU: launched by torchrun, one rank per GPU; config 1 is partitioned by
+batch (weak scaling: every rank inverts its own 131072 matrices, global
+indices rank*131072 + b); no collective touches the data path (the barrier
+and the max-over-ranks timing reduction only).
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the
+host cores on a bounded sample of the same workload; it is the tier's
+reference arm, not the product.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 trinv GFLOP/s (n^3/3) and % FP64 TC peak; batched 32x32 inverses/s"
+FP64_PEAK_FALLBACK = 37.1  # TF/s, measured register-only DMMA peak (profiles/fp64_peaks_r01.json)
+HBM_FALLBACK = 6550.4      # GB/s, MEASURED_PEAKS.json at round start
+BATCH = 131072
+
+CONFIGS = {
+    0: dict(workload="config0: single fp64 lower n=64, seed 0", kind="L", n=64, diag="signed"),
+    1: dict(workload="config1: batch 131072 x fp64 lower 32x32, seed b per matrix", kind="B", n=32),
+    2: dict(workload="config2: single fp64 lower n=8192, 32-wide leaves", kind="L", n=8192, diag="signed"),
+    3: dict(workload="config3: single fp64 upper n=32768", kind="U", n=32768, diag="pos"),
+    4: dict(workload="config4: inv_from_lu n=16384, L unit", kind="G", n=16384),
+}
+
+
+def peaks():
+    hbm, src_h = HBM_FALLBACK, "fallback"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            hbm, src_h = float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+        except Exception:
+            pass
+    fp64, src_f = FP64_PEAK_FALLBACK, "fallback"
+    q = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    if os.path.exists(q):
+        try:
+            d = json.load(open(q))
+            fp64, src_f = float(d["dmma_tflops_sustained"]), "profiles/fp64_peaks_r01.json dmma_tflops_sustained"
+        except Exception:
+            pass
+    return hbm, src_h, fp64, src_f
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes (read+write) per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return  # the oracle arm runs on rank 0 only
+    import numpy as np
+    import oracle
+    import synth
+    cfg = CONFIGS[args.config]
+    cores = len(os.sched_getaffinity(0))
+    if cfg["kind"] == "B":
+        sample = BATCH  # the whole 131072-matrix batch per step (about 0.1-0.5 s on the host cores)
+        A = synth.host(32, batch=sample)
+        def step():
+            oracle.crit_batched(A)
+        unit, work, what = "inverses/s", sample, f"all {sample} config-1 matrices per step, OpenMP over matrices"
+    else:
+        n = cfg["n"]
+        cols = np.arange(0, n, max(1, n // 64))[:64]
+        if cfg["kind"] == "G":
+            L = synth.host(n, tag="L", diag="one")
+            U = synth.host(n, tag="U", uplo="U", diag="pos")
+            def step():
+                oracle.lu_columns(L, U, cols, unit_l=True)
+            cost = lambda j: (n - j) ** 2 + n ** 2  # noqa: E731
+            total_flops = 4 * n ** 3 / 3
+        else:
+            T = synth.host(n, uplo=cfg["kind"], diag=cfg["diag"])
+            def step():
+                oracle.columns(T, cfg["kind"], cols)
+            cost = (lambda j: (n - j) ** 2) if cfg["kind"] == "L" else (lambda j: j ** 2)  # noqa: E731
+            total_flops = n ** 3 / 3
+        frac = sum(cost(j) for j in cols) / sum(cost(j) for j in range(n))
+        work = total_flops * frac / 1e9
+        unit, what = "GFLOP/s", f"{len(cols)} columns per step (extrapolated by the column cost model)"
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = work / dt
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["workload"], "n": cfg["n"]},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": what},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- CPU baseline leg
+def cpu_baseline(cfg):
+    import numpy as np
+    import oracle
+    import synth
+    cores = len(os.sched_getaffinity(0))
+    if cfg["kind"] == "B":
+        sample = 32768
+        A = synth.host(32, batch=sample)
+        oracle.crit_batched(A[:1024])
+        t0 = time.perf_counter(); reps = 0
+        while True:
+            oracle.crit_batched(A); reps += 1
+            if time.perf_counter() - t0 > 2.0:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": sample / dt, "unit": "inverses/s", "cores": cores, "kind": "oracle",
+                "sample": f"{sample} of the 131072 config-1 matrices x {reps} reps, OpenMP over matrices"}
+    n = cfg["n"]
+    if n <= 2048:
+        T = synth.host(n, uplo="L" if cfg["kind"] != "U" else "U", diag=cfg.get("diag", "signed"))
+        t0 = time.perf_counter(); oracle.trinv(T, "L" if cfg["kind"] != "U" else "U")
+        dt = time.perf_counter() - t0
+        return {"value": n ** 3 / 3 / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                "sample": f"full inverse n={n}"}
+    cols = np.arange(0, n, n // 16)[:16]
+    if cfg["kind"] == "G":
+        L = synth.host(n, tag="L", diag="one"); U = synth.host(n, tag="U", uplo="U", diag="pos")
+        t0 = time.perf_counter(); oracle.lu_columns(L, U, cols)
+        dt = time.perf_counter() - t0
+        cost = lambda j: (n - j) ** 2 + n ** 2  # noqa: E731
+        total = 4 * n ** 3 / 3
+    else:
+        T = synth.host(n, uplo=cfg["kind"], diag=cfg["diag"])
+        t0 = time.perf_counter(); oracle.columns(T, cfg["kind"], cols)
+        dt = time.perf_counter() - t0
+        cost = (lambda j: (n - j) ** 2) if cfg["kind"] == "L" else (lambda j: j ** 2)  # noqa: E731
+        total = n ** 3 / 3
+    frac = sum(cost(j) for j in cols) / sum(cost(j) for j in range(n))
+    return {"value": total * frac / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(cols)} sampled columns, extrapolated to the full inverse by the column cost model"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2307_07611_b200 as P
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    cfg = CONFIGS[args.config]
+    hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = cfg["n"]
+    if cfg["kind"] == "B":
+        B = BATCH
+        A = torch.empty((B, n, n), dtype=torch.float64, device=dev)
+        synth.device_fill(A, n, b0=rank * B)
+        X = torch.empty_like(A)
+        def step():
+            P.trinv_batched(A, "L", out=X)
+        units_per_rank, unit = B, "inverses/s"
+        algo_bytes_per_launch = B * (n * (n + 1) / 2 + n * n) * 8  # triangle in + full matrix out
+        flops_per_step = B * n ** 3 / 3
+    else:
+        if cfg["kind"] == "G":
+            Lm = torch.empty((n, n), dtype=torch.float64, device=dev)
+            Um = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(Lm, n, tag="L", diag="one")
+            synth.device_fill(Um, n, tag="U", uplo="U", diag="pos")
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            ws = torch.empty(P.workspace_bytes("G", n, Lm, n, X, n), dtype=torch.uint8, device=dev)
+            def step():
+                import ctypes
+                st = P.lib().inv_from_lu(n, ctypes.c_void_p(Lm.data_ptr()), n, ctypes.c_void_p(Um.data_ptr()), n,
+                                         ctypes.c_void_p(X.data_ptr()), n, 1, 0, ctypes.c_void_p(ws.data_ptr()),
+                                         ws.numel(), None, ctypes.c_void_p(stream.cuda_stream))
+                assert st == 0, P.status_string(st)
+            flops_per_step = 4 * n ** 3 / 3
+        else:
+            A = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(A, n, uplo=cfg["kind"], diag=cfg["diag"])
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            f = P.trinv_lower if cfg["kind"] == "L" else P.trinv_upper
+            def step():
+                f(A, out=X)
+            flops_per_step = n ** 3 / 3
+        units_per_rank, unit = flops_per_step / 1e9, "GFLOP/s"
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # ---- timed region: K steps, per-step events on the launching stream ----
+    P.reset_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    prof = cfg["kind"] != "B"
+    if prof:
+        P._lib.profile_begin()
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        barrier()
+    launches = P.launch_count()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / args.steps
+    value = units_per_rank * world * args.steps / (total_ms / 1e3)
+
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based SplitMix64, synth/)"}
+    conf = {"workload": cfg["workload"], "n": n, "per_rank_units": units_per_rank,
+            "l2_policy": "inputs larger than L2 (126 MB)" if (cfg["kind"] == "B" or n >= 4096)
+            else "input smaller than L2, not flushed (latency config)",
+            "parallelism": f"batch partition x{world}" if cfg["kind"] == "B" else "replicas (single matrix per GPU)"}
+    if cfg["kind"] == "B":
+        conf["batch_per_rank"] = BATCH
+    line["config"] = conf
+
+    # ---- roofline of the dominant kernel ----
+    if cfg["kind"] == "B":
+        avg_ms = statistics.mean(step_ms)  # one launch per step: the leaf kernel
+        achieved = algo_bytes_per_launch / (avg_ms / 1e3) / 1e9
+        line["roofline"] = {"bound": "hbm", "kernel": "leaf_tma_kernel (trinv_batched)", "achieved": achieved,
+                            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                            "traffic": ncu_traffic("leaf_tma_kernel"), "peak_source": hbm_src,
+                            "algorithmic_bytes_per_launch": algo_bytes_per_launch,
+                            "launch_ms": avg_ms, "fp64_gflops": flops_per_step / (avg_ms / 1e3) / 1e9}
+    else:
+        ms_d, n_d, fl_d, _ = P._lib.profile_read(1)
+        ms_l, n_l, fl_l, _ = P._lib.profile_read(0)
+        P._lib.profile_end()
+        achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
+        line["roofline"] = {"bound": "tensor", "kernel": "dmma_level_kernel (all product launches)",
+                            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                            "frac": achieved / fp64_peak, "traffic": ncu_traffic("dmma_level_kernel"),
+                            "peak_source": fp64_src + " (FP64 DMMA, register-only loop)",
+                            "dmma_share_of_step": ms_d / (args.steps * ms_per_step) if ms_per_step else None,
+                            "dmma_launches_per_step": n_d / args.steps, "leaf_ms_per_step": ms_l / args.steps,
+                            "whole_step_tflops": flops_per_step / (ms_per_step / 1e3) / 1e12,
+                            "whole_step_frac_of_peak": flops_per_step / (ms_per_step / 1e3) / 1e12 / fp64_peak}
+    line["gpu_launches"] = launches
+    line["clocks"] = clk.summary()
+
+    # ---- end-to-end through the public API with host buffers ----
+    if cfg["kind"] == "B" and args.e2e_steps > 0:
+        import numpy as np
+        h_in = torch.empty((BATCH, n, n), dtype=torch.float64).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_in.copy_(A.cpu())
+        d_in = torch.empty_like(A); d_out = torch.empty_like(A)
+        def e2e_step():
+            d_in.copy_(h_in, non_blocking=True)
+            P.trinv_batched(d_in, "L", out=d_out)
+            h_out.copy_(d_out, non_blocking=True)
+        e2e_step(); barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(); e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream); barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.e2e_steps
+        nbytes = h_in.numel() * 8
+        line["e2e"] = {"value": BATCH * world / (e_ms / 1e3), "unit": unit, "h2d_bytes_per_step": nbytes,
+                       "d2h_bytes_per_step": nbytes, "ms_per_step": e_ms, "steps": args.e2e_steps,
+                       "path": "pinned host -> cudaMemcpyAsync -> trinv_batched (C-ABI) -> pinned host"}
+        del h_in, h_out, d_in, d_out
+    elif cfg["kind"] != "B":
+        # host buffers: H2D of the input factor(s), the call, D2H of the inverse
+        ins = [Lm, Um] if cfg["kind"] == "G" else [A]
+        h_ins = [t.cpu().pin_memory() for t in ins]
+        h_out = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(); e0.record(stream)
+        steps_e = max(1, min(args.e2e_steps, 3))
+        for _ in range(steps_e):
+            for d, h in zip(ins, h_ins):
+                d.copy_(h, non_blocking=True)
+            step()
+            h_out.copy_(X, non_blocking=True)
+        e1.record(stream); barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1)) / steps_e
+        line["e2e"] = {"value": units_per_rank * world / (e_ms / 1e3), "unit": unit,
+                       "h2d_bytes_per_step": sum(h.numel() * 8 for h in h_ins), "d2h_bytes_per_step": n * n * 8,
+                       "ms_per_step": e_ms, "steps": steps_e}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

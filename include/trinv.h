@@ -15,9 +15,10 @@
  *  - Ownership: the caller allocates and frees every buffer.  The library
  *    never allocates device memory on the call path and keeps no pointer after
  *    returning.  Buffers must stay alive until the enqueued work completes.
- *  - Only the referenced triangle of an input is read (the other triangle may
- *    hold anything, including NaN).  With diag == TRINV_UNIT the stored
- *    diagonal is not read and is taken as 1 (CRIT*, Alg. 2).
+ *  - Only the referenced triangle of an input is used (the other triangle may
+ *    hold anything, including NaN; it may be loaded but never enters the
+ *    arithmetic).  With diag == TRINV_UNIT the stored diagonal is not used and
+ *    is taken as 1 (CRIT*, Alg. 2).
  *  - Outputs are FULL matrices: the triangle opposite to the inverse's is
  *    written as +0.0 (Thm 1 "0, otherwise"; Eq. defT).
  *  - Synchronous errors (returned before anything is enqueued): see
@@ -67,7 +68,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
  * leaves are inverted in shared memory by the column recurrence of the proof
  * of Thm 1 (CRIT, Alg. 3); the off-diagonal products
  * run on the FP64 tensor cores (DMMA) fed by TMA.
- *   A, lda : input (device, read-only), only the lower triangle is read.
+ *   A, lda : input (device, read-only), only the lower triangle is used.
  *   X, ldx : output (device), full n x n written; must not overlap A
  *            (TRINV_ALIASING).
  *   ws     : device workspace of ws_bytes >= trinv_workspace_bytes('L', ...);
@@ -124,6 +125,19 @@ const char* trinv_version(void);
  * since the last reset (used by bench.py for its "gpu_launches" count). */
 int64_t trinv_launch_count(void);
 void trinv_reset_launch_count(void);
+
+/* Observability: per-launch device timing.  Between trinv_profile_begin() and
+ * trinv_profile_end() every kernel this thread enqueues is bracketed by CUDA
+ * events recorded on its stream (small overhead; for measurement runs only).
+ * trinv_profile_read(kind, ...) synchronises those events and returns, for
+ * kind 0 (leaf / batched kernels) or 1 (DMMA product kernels), the summed
+ * device milliseconds, the launch count and the ALGORITHMIC flops and bytes
+ * of those launches (n^3/3 per leaf; triangular-aware products, P:608-612,
+ * P:1269-1271; leaf bytes = referenced triangle in + full matrix out).
+ * Any output pointer may be NULL.  Returns a trinv_status_t value. */
+void trinv_profile_begin(void);
+void trinv_profile_end(void);
+int trinv_profile_read(int kind, double* ms, int64_t* launches, double* flops, double* bytes);
 
 #ifdef __cplusplus
 }

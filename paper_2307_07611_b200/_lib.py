@@ -57,6 +57,9 @@ def lib():
     L.trinv_last_cuda_error.restype = _i32
     L.trinv_version.restype = ctypes.c_char_p
     L.trinv_launch_count.restype = _i64
+    L.trinv_profile_read.argtypes = [_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    L.trinv_profile_read.restype = _i32
     _lib = L
     return L
 
@@ -71,6 +74,23 @@ def launch_count():
 
 def reset_launch_count():
     lib().trinv_reset_launch_count()
+
+
+def profile_begin():
+    lib().trinv_profile_begin()
+
+
+def profile_end():
+    lib().trinv_profile_end()
+
+
+def profile_read(kind):
+    """(ms, launches, flops, bytes) summed over the profiled launches of `kind` (0 leaf, 1 DMMA)."""
+    ms, n, f, b = ctypes.c_double(), _i64(), ctypes.c_double(), ctypes.c_double()
+    st = lib().trinv_profile_read(kind, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(f), ctypes.byref(b))
+    if st != TRINV_OK:
+        raise TrinvError(st)
+    return ms.value, n.value, f.value, b.value
 
 
 def declared_symbols():

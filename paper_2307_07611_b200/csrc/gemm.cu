@@ -274,7 +274,27 @@ static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launc
   return cudaGetLastError();
 }
 
+// Algorithmic flops of one level launch, exploiting the triangular operand
+// (P_TF; P_UL): 2 flops per multiply-add that touches
+// a non-zero of the triangular factor.
+static double level_flops(const LevelArgs& a) {
+  if (a.mode == MODE_UL) {
+    const double n = (double)a.n;
+    return 2.0 * (n * (n + 1) * (2 * n + 1) / 6.0) - n * n;  // sum_{i,j} 2(n - max(i,j)) ~ 2n^3/3
+  }
+  double f = 0.0;
+  for (int64_t g = 0; g < a.merges; ++g) {
+    const double b = (double)a.b;
+    const int64_t s0 = 2 * g * a.b;
+    const double r = (double)(a.n - s0 - a.b < a.b ? a.n - s0 - a.b : a.b);
+    const bool first = (a.mode == MODE_LOWER_1 || a.mode == MODE_UPPER_1);
+    f += first ? r * b * (b + 1) : b * r * (r + 1);
+  }
+  return f;
+}
+
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+  ProfileScope prof(KIND_DMMA, level_flops(a), 0.0, s);
   // Tile size follows the level: min(b, 128) (b is a power of two >= 32 for
   // the triangular modes; UL uses 128).
   const int64_t t = (a.mode == MODE_UL) ? 128 : (a.b < 128 ? a.b : 128);

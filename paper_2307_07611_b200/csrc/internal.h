@@ -57,4 +57,14 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
 // runtime's driver entry point).  Returns false on failure.
 bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, bool swizzle128);
 
+// Optional per-launch timing (trinv_profile_* in include/trinv.h): when enabled on
+// this thread, every launch is bracketed by CUDA events on its stream.
+enum LaunchKind : int { KIND_LEAF = 0, KIND_DMMA = 1, KIND_COUNT = 2 };
+struct ProfileScope {
+  ProfileScope(int kind, double flops, double bytes, cudaStream_t s);
+  ~ProfileScope();
+  void* rec;
+  cudaStream_t stream_ = nullptr;
+};
+
 }  // namespace trinv

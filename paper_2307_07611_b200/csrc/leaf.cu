@@ -209,6 +209,9 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   const bool even = (a.n % 2 == 0) && (a.n_last % 2 == 0) && (a.lda % 2 == 0) && (a.ldx % 2 == 0) &&
                     (a.sA % 2 == 0) && (a.sX % 2 == 0);
   const bool tma = even && aligned16(a.A) && aligned16(a.X);
+  // algorithmic work: n^3/3 flops and the referenced triangle in + full matrix out per matrix
+  const double nn = (double)a.n;
+  ProfileScope prof(KIND_LEAF, a.batch * nn * nn * nn / 3.0, a.batch * (nn * (nn + 1) / 2 + nn * nn) * 8.0, s);
   if (tma) {
     const int64_t ctas_needed = (a.batch + kWarps - 1) / kWarps;
     const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);

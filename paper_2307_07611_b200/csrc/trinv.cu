@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/trinv.h"
 #include "internal.h"
@@ -22,6 +23,32 @@ namespace trinv {
 
 static thread_local int g_last_cuda_error = 0;
 static thread_local int64_t g_launches = 0;
+
+// ---- optional per-launch profiling ------------------------------------------------
+struct ProfRec {
+  int kind;
+  double flops, bytes;
+  cudaEvent_t e0, e1;
+};
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfRec>* g_prof = nullptr;
+
+ProfileScope::ProfileScope(int kind, double flops, double bytes, cudaStream_t s) : rec(nullptr) {
+  if (!g_prof_on) return;
+  if (!g_prof) g_prof = new std::vector<ProfRec>();
+  ProfRec r{kind, flops, bytes, nullptr, nullptr};
+  cudaEventCreate(&r.e0);
+  cudaEventCreate(&r.e1);
+  cudaEventRecord(r.e0, s);
+  g_prof->push_back(r);
+  rec = reinterpret_cast<void*>(static_cast<uintptr_t>(g_prof->size()));
+  stream_ = s;
+}
+ProfileScope::~ProfileScope() {
+  if (!rec || !g_prof) return;
+  const size_t i = reinterpret_cast<uintptr_t>(rec) - 1;
+  cudaEventRecord((*g_prof)[i].e1, stream_);
+}
 
 // ---- tensor-map encoding through the runtime's driver entry point -----------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -287,5 +314,39 @@ int trinv_last_cuda_error(void) { return g_last_cuda_error; }
 const char* trinv_version(void) { return "trinv-b200 0.1 sm_100a"; }
 int64_t trinv_launch_count(void) { return g_launches; }
 void trinv_reset_launch_count(void) { g_launches = 0; }
+
+void trinv_profile_begin(void) {
+  trinv_profile_end();
+  g_prof_on = true;
+}
+
+void trinv_profile_end(void) {
+  g_prof_on = false;
+  if (!g_prof) return;
+  for (auto& r : *g_prof) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g_prof->clear();
+}
+
+int trinv_profile_read(int kind, double* ms, int64_t* launches, double* flops, double* bytes) {
+  double t = 0, f = 0, b = 0;
+  int64_t c = 0;
+  if (g_prof) {
+    for (auto& r : *g_prof) {
+      if (r.kind != kind) continue;
+      if (cudaEventSynchronize(r.e1) != cudaSuccess) return (int)TRINV_CUDA_ERROR;
+      float e = 0.f;
+      cudaEventElapsedTime(&e, r.e0, r.e1);
+      t += e; f += r.flops; b += r.bytes; ++c;
+    }
+  }
+  if (ms) *ms = t;
+  if (launches) *launches = c;
+  if (flops) *flops = f;
+  if (bytes) *bytes = b;
+  return (int)TRINV_OK;
+}
 
 }  // extern "C"

@@ -56,6 +56,9 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.
 bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, bool swizzle128);
+// General FP64 tiled map (no swizzle, zero OOB fill): dims[0] innermost, strides in bytes for dims 1..rank-1.
+bool encode_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                   const uint32_t* box);
 
 // Optional per-launch timing (trinv_profile_* in include/trinv.h): when enabled on
 // this thread, every launch is bracketed by CUDA events on its stream.

@@ -11,12 +11,14 @@
 // different columns are independent: the 32 lanes never
 // exchange data; T is read from shared memory as warp-wide broadcasts.
 //
-// HBM staging (a3): every warp runs its own NS-deep ring of 8 KiB slots.
-// Loads are 1-D TMA bulk copies (cp.async.bulk, one per matrix when it is
-// contiguous, one per row otherwise) completing on a per-slot mbarrier; the
-// inverse is written back into the same slot and stored with a bulk copy
-// smem->global.  The slot is reloaded only after that store has read it.
+// HBM staging (a3): every warp runs its own NS-deep ring of smem slots filled
+// by 2-D TMA (cp.async.bulk.tensor) with only the referenced triangle, each
+// slot completing on its own mbarrier (see leaf32_tma_kernel).  Orders below
+// 32 and odd layouts use the plain-load kernel (leaf_plain_kernel).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -73,16 +75,6 @@ __device__ __forceinline__ void leaf_compute(double* T, int n, int unit, int lan
   }
 }
 
-// Write X into the slot row-major; the opposite triangle as +0.0 (C12).
-template <bool UPPER>
-__device__ __forceinline__ void leaf_write_slot(double* T, int lane, const double (&x)[LEAF]) {
-#pragma unroll
-  for (int i = 0; i < LEAF; ++i) {
-    const bool zero = UPPER ? (i > lane) : (i < lane);
-    T[i * LEAF + lane] = zero ? 0.0 : x[i];
-  }
-}
-
 __device__ __forceinline__ void leaf_report(const LeafArgs& a, int64_t b, int lane, bool singular,
                                             int first_zero) {
   if (a.info_mode == 1) {
@@ -93,13 +85,85 @@ __device__ __forceinline__ void leaf_report(const LeafArgs& a, int64_t b, int la
 }
 
 // ---------------------------------------------------------------------------
-// TMA-staged persistent kernel: WARPS warps per CTA, NS slots per warp.
+// Triangle-only staging (n = 32).  Each slot holds the referenced triangle as
+// two 16-row bands loaded by 2-D TMA (cp.async.bulk.tensor over a 3-D view
+// [batch][32 rows][32 cols] of the input): lower = rows 0-15 x cols 0-15 and
+// rows 16-31 x cols 0-31; upper = rows 0-15 x cols 0-31 and rows 16-31 x cols
+// 16-31.  6 KiB per matrix instead of 8 KiB, two TMA instructions.  The inverse
+// leaves the registers through coalesced 256-byte row stores, so a slot is free
+// again as soon as the warp has read it; the next load is issued before the
+// stores.
+//
+// The upper case runs the lower recurrence on T' = J U J (J = index reversal,
+// T'_ik = U_{31-i,31-k}): X' = J U^{-1} J, lane j then holds column 31-j of
+// U^{-1}.  One straight-line code path, no per-step branches.
+constexpr int kBand = 768;  // doubles per slot (16x16 + 16x32)
+__host__ __device__ __forceinline__ int lidx(int i, int k) { return i < 16 ? i * 16 + k : 256 + (i - 16) * 32 + k; }
+__host__ __device__ __forceinline__ int uidx(int i, int k) { return i < 16 ? i * 32 + k : 512 + (i - 16) * 16 + (k - 16); }
+template <bool UPPER>
+__device__ __forceinline__ double2 tri_pair(const double* T, int i, int k) {  // (T'_ik, T'_i,k+1), k even
+  if (!UPPER) return *reinterpret_cast<const double2*>(T + lidx(i, k));
+  const double2 v = *reinterpret_cast<const double2*>(T + uidx(31 - i, 30 - k));  // U_{r,c}, U_{r,c+1}
+  return make_double2(v.y, v.x);
+}
+template <bool UPPER>
+__device__ __forceinline__ double tri_sub(const double* T, int k) {  // T'_{k+1,k}, k even
+  return UPPER ? T[uidx(30 - k, 31 - k)] : T[lidx(k + 1, k)];
+}
+template <bool UPPER>
+__device__ __forceinline__ double tri_diag(const double* T, int i) {  // T_ii, original index
+  return UPPER ? T[uidx(i, i)] : T[lidx(i, i)];
+}
+
+template <bool UPPER, int K>
+__device__ __forceinline__ void leaf32_step(const double* T, const double* rr, double (&x)[LEAF]) {
+  const double2 r = *reinterpret_cast<const double2*>(rr + K);
+  const double xk = x[K] * r.x;
+  x[K] = xk;
+  x[K + 1] = fma(-tri_sub<UPPER>(T, K), xk, x[K + 1]);
+  const double xk1 = x[K + 1] * r.y;
+  x[K + 1] = xk1;
+#pragma unroll
+  for (int i = K + 2; i < LEAF; ++i) {
+    const double2 t = tri_pair<UPPER>(T, i, K);
+    x[i] = fma(-t.x, xk, x[i]);
+    x[i] = fma(-t.y, xk1, x[i]);
+  }
+}
+template <bool UPPER, int... P>
+__device__ __forceinline__ void leaf32_steps(const double* T, const double* rr, double (&x)[LEAF],
+                                             std::integer_sequence<int, P...>) {
+  (leaf32_step<UPPER, 2 * P>(T, rr, x), ...);
+}
+
+template <bool UPPER>
+__device__ __forceinline__ void leaf32_compute(const double* T, double* rr, int unit, int lane, double (&x)[LEAF],
+                                               bool& singular, int& first_zero) {
+  const double d = tri_diag<UPPER>(T, lane);
+  const bool zero = (!unit) && d == 0.0;
+  const unsigned zmask = __ballot_sync(0xffffffffu, zero);
+  singular = zmask != 0;
+  first_zero = singular ? __ffs(zmask) - 1 : -1;
+  rr[UPPER ? LEAF - 1 - lane : lane] = unit ? 1.0 : 1.0 / d;  // r'_k = rr[k] in T' order
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < LEAF; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+  // pairs (k, k+1): x_k = r_k acc_k; acc_{k+1} -= T'_{k+1,k} x_k; x_{k+1} = r_{k+1} acc_{k+1};
+  // acc_i -= T'_ik x_k + T'_{i,k+1} x_{k+1} (i >= k+2), one 16-byte broadcast per row.
+  // Compile-time step indices (template expansion) keep x[] in registers.
+  leaf32_steps<UPPER>(T, rr, x, std::make_integer_sequence<int, LEAF / 2>{});
+}
+
 template <bool UPPER, int WARPS, int NS>
-__global__ void __launch_bounds__(WARPS * 32, 1) leaf_tma_kernel(const LeafArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    leaf32_tma_kernel(const __grid_constant__ CUtensorMap band0, const __grid_constant__ CUtensorMap band1,
+                      const LeafArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * LEAF * LEAF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WARPS * NS * LEAF * LEAF * 8) + warp * NS;
+  double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * kBand;
+  double* rr = reinterpret_cast<double*>(smem_raw) + (size_t)WARPS * NS * kBand + warp * LEAF;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem_raw + ((size_t)WARPS * NS * kBand + WARPS * LEAF) * 8) + warp * NS;
 
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t TW = (int64_t)gridDim.x * WARPS;
@@ -110,60 +174,52 @@ __global__ void __launch_bounds__(WARPS * 32, 1) leaf_tma_kernel(const LeafArgs 
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
+  if (lane == 0 && warp == 0) {
+    tma_prefetch_desc(&band0);
+    tma_prefetch_desc(&band1);
+  }
   __syncwarp();
 
-  auto order = [&](int64_t b) { return (b == a.batch - 1) ? a.n_last : a.n; };
-  auto issue_load = [&](int64_t t) {
-    const int64_t b = gw + t * TW;
-    const int nb = order(b);
-    double* slot = slots + (t % NS) * LEAF * LEAF;
+  auto issue_load = [&](int64_t t) {  // lane 0 only
+    const int b = (int)(gw + t * TW);
+    double* slot = slots + (t % NS) * kBand;
     uint64_t* bar = &bars[t % NS];
-    const double* src = a.A + b * a.sA;
-    if (nb == LEAF && a.lda == LEAF) {
-      if (lane == 0) {
-        mbar_arrive_expect_tx(bar, LEAF * LEAF * 8);
-        bulk_g2s(slot, src, LEAF * LEAF * 8, bar);
-      }
+    mbar_arrive_expect_tx(bar, kBand * 8);
+    if (!UPPER) {
+      tma_load_3d(slot, &band0, 0, 0, b, bar);         // rows 0-15, cols 0-15
+      tma_load_3d(slot + 256, &band1, 0, 16, b, bar);  // rows 16-31, cols 0-31
     } else {
-      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nb * nb * 8));
-      __syncwarp();
-      if (lane < nb) bulk_g2s(slot + lane * LEAF, src + lane * a.lda, (uint32_t)(nb * 8), bar);
+      tma_load_3d(slot, &band1, 0, 0, b, bar);         // rows 0-15, cols 0-31
+      tma_load_3d(slot + 512, &band0, 16, 16, b, bar); // rows 16-31, cols 16-31
     }
   };
 
-  for (int64_t t = 0; t < NS - 1 && t < count; ++t) issue_load(t);
+  if (lane == 0)
+    for (int64_t t = 0; t < NS && t < count; ++t) issue_load(t);
 
   for (int64_t t = 0; t < count; ++t) {
     const int64_t b = gw + t * TW;
-    const int nb = order(b);
-    double* slot = slots + (t % NS) * LEAF * LEAF;
+    double* slot = slots + (t % NS) * kBand;
     mbar_wait(&bars[t % NS], (uint32_t)((t / NS) & 1));
 
     double x[LEAF];
     bool singular;
     int first_zero;
-    leaf_compute<UPPER>(slot, nb, a.unit, lane, x, singular, first_zero);
-    __syncwarp();
-    leaf_write_slot<UPPER>(slot, lane, x);
-    fence_proxy_async_smem();
-    __syncwarp();
+    leaf32_compute<UPPER>(slot, rr, a.unit, lane, x, singular, first_zero);
+    __syncwarp();  // every lane has finished reading the slot and rr
+    if (t + NS < count && lane == 0) {
+      fence_proxy_async_smem();
+      issue_load(t + NS);
+    }
     double* dst = a.X + b * a.sX;
-    if (nb == LEAF && a.ldx == LEAF) {
-      if (lane == 0) bulk_s2g(dst, slot, LEAF * LEAF * 8);
-    } else {
-      if (lane < nb) bulk_s2g(dst + lane * a.ldx, slot + lane * LEAF, (uint32_t)(nb * 8));
+    const int col = UPPER ? LEAF - 1 - lane : lane;
+#pragma unroll
+    for (int i = 0; i < LEAF; ++i) {
+      const int row = UPPER ? LEAF - 1 - i : i;
+      dst[(int64_t)row * a.ldx + col] = (i < lane) ? 0.0 : x[i];
     }
-    bulk_commit();
     leaf_report(a, b, lane, singular, first_zero);
-
-    const int64_t tn = t + NS - 1;  // refill the slot used by iteration t-1
-    if (tn < count) {
-      bulk_wait_read<1>();  // the store issued at t-1 has finished reading its slot
-      __syncwarp();
-      issue_load(tn);
-    }
   }
-  bulk_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -196,10 +252,19 @@ __global__ void __launch_bounds__(128) leaf_plain_kernel(const LeafArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-constexpr int kWarps = 6, kSlots = 4;
-constexpr size_t kTmaSmem = (size_t)kWarps * kSlots * LEAF * LEAF * 8 + kWarps * kSlots * 8;
+constexpr int kTriWarps = 8, kTriSlots = 4;
+constexpr size_t kTriSmem =
+    ((size_t)kTriWarps * kTriSlots * kBand + kTriWarps * LEAF) * 8 + kTriWarps * kTriSlots * 8;
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// 3-D view [batch][32 rows][32 cols] of the inputs; box = 16 rows x `cols` columns x 1 matrix.
+static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols) {
+  const uint64_t dims[3] = {32, 32, (uint64_t)a.batch};
+  const uint64_t strides[2] = {(uint64_t)a.lda * 8, (uint64_t)a.sA * 8};
+  const uint32_t box[3] = {(uint32_t)cols, 16, 1};
+  return encode_map_nd(m, a.A, 3, dims, strides, box);
+}
 
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.batch <= 0) return cudaSuccess;
@@ -212,17 +277,20 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   // algorithmic work: n^3/3 flops and the referenced triangle in + full matrix out per matrix
   const double nn = (double)a.n;
   ProfileScope prof(KIND_LEAF, a.batch * nn * nn * nn / 3.0, a.batch * (nn * (nn + 1) / 2 + nn * nn) * 8.0, s);
-  if (tma) {
-    const int64_t ctas_needed = (a.batch + kWarps - 1) / kWarps;
+  const bool full32 = a.n == LEAF && a.n_last == LEAF;
+  CUtensorMap m16, m32;
+  const bool maps = full32 && a.batch < (int64_t)1 << 31 && encode_batch_map(&m16, a, 16) && encode_batch_map(&m32, a, 32);
+  if (tma && full32 && maps) {
+    const int64_t ctas_needed = (a.batch + kTriWarps - 1) / kTriWarps;
     const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
     if (uplo == 'L') {
-      auto k = leaf_tma_kernel<false, kWarps, kSlots>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-      k<<<grid, kWarps * 32, kTmaSmem, s>>>(a);
+      auto k = leaf32_tma_kernel<false, kTriWarps, kTriSlots>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+      k<<<grid, kTriWarps * 32, kTriSmem, s>>>(m16, m32, a);
     } else {
-      auto k = leaf_tma_kernel<true, kWarps, kSlots>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-      k<<<grid, kWarps * 32, kTmaSmem, s>>>(a);
+      auto k = leaf32_tma_kernel<true, kTriWarps, kTriSlots>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+      k<<<grid, kTriWarps * 32, kTriSmem, s>>>(m16, m32, a);
     }
   } else {
     const int64_t ctas_needed = (a.batch + 3) / 4;

@@ -82,6 +82,20 @@ bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, boo
   return rc == CUDA_SUCCESS;
 }
 
+bool encode_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                   const uint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc || rank < 1 || rank > 5) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
+  for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
+  CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), d, st, b, e,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS;
+}
+
 // ---- layout helpers -----------------------------------------------------------
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static bool tma_ok(const void* p, int64_t ld) { return p == nullptr ? (ld % 2 == 0) : (aligned16(p) && ld % 2 == 0); }

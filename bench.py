@@ -247,10 +247,17 @@ def main():
     import paper_2307_07611_b200 as P
 
     world, rank, local = dist_setup()
+    # BENCH_DIST_BACKEND=gloo + BENCH_ONE_GPU=1 exercise the multi-rank logic on a single GPU
+    # (test only: ranks never wait on each other inside a kernel).
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    dev_index = 0 if (world == 1 or os.environ.get("BENCH_ONE_GPU")) else local
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     cfg = CONFIGS[args.config]
@@ -264,7 +271,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -342,9 +349,9 @@ def main():
     if cfg["kind"] == "B":
         avg_ms = statistics.mean(step_ms)  # one launch per step: the leaf kernel
         achieved = algo_bytes_per_launch / (avg_ms / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": "leaf_tma_kernel (trinv_batched)", "achieved": achieved,
+        line["roofline"] = {"bound": "hbm", "kernel": "leaf32_tma_kernel (trinv_batched)", "achieved": achieved,
                             "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                            "traffic": ncu_traffic("leaf_tma_kernel"), "peak_source": hbm_src,
+                            "traffic": ncu_traffic("leaf32_tma_kernel"), "peak_source": hbm_src,
                             "algorithmic_bytes_per_launch": algo_bytes_per_launch,
                             "launch_ms": avg_ms, "fp64_gflops": flops_per_step / (avg_ms / 1e3) / 1e9}
     else:

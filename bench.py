@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-graph", action="store_true", help="never replay steps from a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -315,19 +316,36 @@ def main():
         step()
     barrier()
     # ---- timed region: K steps, per-step events on the launching stream ----
+    # Small single matrices are launch-latency bound: their steps are replayed from a
+    # CUDA graph captured from the same public call (no Python between launches).
+    use_graph = cfg["kind"] != "B" and n <= 1024 and not args.no_graph
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):  # captured on torch's side stream, replayed on `stream`
+            step()
+        graph.replay()
+        barrier()
+        launches_per_step = None
+    run = graph.replay if graph is not None else step
+    # per-launch events inside the timed region for the multi-launch configs (ms-scale kernels)
+    prof = cfg["kind"] != "B" and graph is None
     P.reset_launch_count()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    prof = cfg["kind"] != "B"
     if prof:
         P._lib.profile_begin()
     with ClockSampler(dev.index) as clk:
         barrier()
         ev[0].record(stream)
         for i in range(args.steps):
-            step()
+            run()
             ev[i + 1].record(stream)
         barrier()
     launches = P.launch_count()
+    if graph is not None:
+        # count the kernels inside one captured step, then scale to the timed steps
+        P.reset_launch_count(); step(); barrier()
+        launches = P.launch_count() * args.steps
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
     total_ms = max_over_ranks(total_ms)
@@ -355,18 +373,31 @@ def main():
                             "algorithmic_bytes_per_launch": algo_bytes_per_launch,
                             "launch_ms": avg_ms, "fp64_gflops": flops_per_step / (avg_ms / 1e3) / 1e9}
     else:
+        if not prof:  # graph-replayed latency config: a separate profiled pass of eager steps
+            P._lib.profile_begin()
+            for _ in range(args.steps):
+                step()
+            barrier()
         ms_d, n_d, fl_d, _ = P._lib.profile_read(1)
         ms_l, n_l, fl_l, _ = P._lib.profile_read(0)
         P._lib.profile_end()
         achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
-        line["roofline"] = {"bound": "tensor", "kernel": "dmma_level_kernel (all product launches)",
-                            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                            "frac": achieved / fp64_peak, "traffic": ncu_traffic("dmma_level_kernel"),
-                            "peak_source": fp64_src + " (FP64 DMMA, register-only loop)",
-                            "dmma_share_of_step": ms_d / (args.steps * ms_per_step) if ms_per_step else None,
-                            "dmma_launches_per_step": n_d / args.steps, "leaf_ms_per_step": ms_l / args.steps,
-                            "whole_step_tflops": flops_per_step / (ms_per_step / 1e3) / 1e12,
-                            "whole_step_frac_of_peak": flops_per_step / (ms_per_step / 1e3) / 1e12 / fp64_peak}
+        if n_d == 0:  # a single leaf launch (n <= 64): latency-bound, no tensor-core product
+            line["roofline"] = {"bound": "latency", "kernel": "leaf64_kernel (single launch)", "achieved": None,
+                                "peak": None, "unit": None, "frac": None, "traffic": None,
+                                "leaf_us_per_launch": 1e3 * ms_l / max(n_l, 1),
+                                "note": "one 64x64 inverse per launch; bounded by launch latency and the "
+                                        "64-step dependent recurrence, not by HBM or the tensor pipe"}
+        else:
+            line["roofline"] = {"bound": "tensor", "kernel": "dmma_level_kernel (all product launches)",
+                              "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                              "frac": achieved / fp64_peak, "traffic": ncu_traffic("dmma_level_kernel"),
+                              "peak_source": fp64_src + " (FP64 DMMA, register-only loop)",
+                              "dmma_share_of_step": ms_d / (args.steps * ms_per_step) if ms_per_step else None,
+                              "dmma_launches_per_step": n_d / args.steps, "leaf_ms_per_step": ms_l / args.steps,
+                              "whole_step_tflops": flops_per_step / (ms_per_step / 1e3) / 1e12,
+                              "whole_step_frac_of_peak": flops_per_step / (ms_per_step / 1e3) / 1e12 / fp64_peak}
+        line["config"]["cuda_graph"] = graph is not None
     line["gpu_launches"] = launches
     line["clocks"] = clk.summary()
 

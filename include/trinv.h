@@ -47,7 +47,7 @@ typedef enum {
   TRINV_ALIASING = 2,             /* input and output ranges overlap (non-batched calls) */
   TRINV_WORKSPACE_TOO_SMALL = 3,  /* ws_bytes < trinv_workspace_bytes(...) */
   TRINV_CUDA_ERROR = 4,           /* a CUDA launch or API call failed; see trinv_last_cuda_error() */
-  TRINV_NOT_SUPPORTED = 5         /* request outside the implemented envelope (e.g. batched n > 32) */
+  TRINV_NOT_SUPPORTED = 5         /* request outside the implemented envelope (e.g. batched n > 64) */
 } trinv_status_t;
 
 typedef enum { TRINV_NON_UNIT = 0, TRINV_UNIT = 1 } trinv_diag_t;
@@ -87,11 +87,12 @@ trinv_status_t trinv_upper(int64_t n, const double* A, int64_t lda, double* X, i
 
 /* Batched small inverses: for b in [0, batch): X_b = T_b^{-1}, T_b at
  * A + b*strideA (leading dim lda), X_b at X + b*strideX (leading dim ldx).
- * uplo 'L' or 'U'; 1 <= n <= 32 (TRINV_NOT_SUPPORTED above).  One warp owns
- * one matrix; lane j computes column j by the recurrence of P:243 (CRIT for
- * the upper case) in registers with the matrix staged in shared
- * memory by 1-D TMA bulk copies (cp.async.bulk) when n, lda, ldx, the strides
- * are even and the pointers 16-byte aligned, else by plain loads.
+ * uplo 'L' or 'U'; 1 <= n <= 64 (TRINV_NOT_SUPPORTED above).  Lane j computes
+ * column j by the recurrence of P:243 (CRIT for the upper case) in
+ * registers, one warp per matrix for n <= 32 (two for n <= 64).  For n = 32
+ * with even lda/ldx/strides and 16-byte aligned pointers the referenced
+ * triangle is staged in shared memory by 2-D TMA (cp.async.bulk.tensor);
+ * other layouts use plain coalesced loads.
  * X == A exactly (in-place, same ld and stride) is allowed; any other overlap
  * is undefined.  strideA >= n*lda and strideX >= n*ldx are required.
  * d_info: NULL or device int32[batch], one status per matrix. */

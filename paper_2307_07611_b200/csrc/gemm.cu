@@ -20,19 +20,25 @@
 // Engine: CTA tile BM x BN, K-step BK = 16, STAGES-deep smem ring filled by
 // TMA (cp.async.bulk.tensor.2d) from a producer warp through full/empty
 // mbarriers; WM x WN consumer warps issue mma.sync.m8n8k4.f64 (DMMA.8x8x4).
-// A tiles: one box (16 x BM) with 128-byte swizzle -> conflict-free fragment
-// loads; B tiles: BN/8 boxes (8 x 16), 64-byte rows -> conflict-free.
+// Shared-memory layouts are chosen for the m8n8k4 fragments, whose 64-bit loads
+// are served per half-warp (16 lanes = 128 B must cover the 32 banks once):
+// A tile = BK/4 boxes of [BM rows][4 k] (32-byte rows), B tile = BN/4 boxes of
+// [BK rows][4 n]; each half-warp fragment load then reads 128 contiguous bytes.
 // Out-of-range rows / columns (ragged last merge, n not a multiple of the
 // tile) are zero-filled by TMA and clipped at the store.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace trinv {
 
-constexpr int BK = 16;
-
+// Shared-memory layout variants (template parameter LAY):
+//   LAY 0: A = one 16-wide box per stage with 128-byte swizzle, B = BN/8 boxes of 8 columns
+//   LAY 1: A = BK/4 boxes of 4 columns, B = BN/4 boxes of 4 columns (half-warp conflict-free)
+//   LAY 2: A = BK/4 boxes of 4 columns, B = BN/8 boxes of 8 columns
 struct TileCoord {
   int64_t a_row, a_col;  // A-operand: rows a_row.., columns a_col + k
   int64_t b_row, b_col;  // B-operand: rows b_row + k, columns b_col..
@@ -42,7 +48,7 @@ struct TileCoord {
   bool valid, mirror;
 };
 
-template <int BM, int BN>
+template <int BM, int BN, int BK>
 __device__ __forceinline__ TileCoord map_tile(const LevelArgs& p, int64_t t) {
   TileCoord c{};
   const int64_t b = p.b, n = p.n, merges = p.merges;
@@ -122,7 +128,7 @@ __device__ __forceinline__ TileCoord map_tile(const LevelArgs& p, int64_t t) {
   return c;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int BK = 16, int LAY = 1>
 struct GemmCfg {
   static constexpr int kConsumerWarps = WM * WN;
   static constexpr int kThreads = (kConsumerWarps + 1) * 32;
@@ -135,20 +141,21 @@ struct GemmCfg {
   static_assert(BM % BK == 0 && BN % BK == 0, "BK must divide BM and BN");
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+template <int BM, int BN, int WM, int WN, int STAGES, int BK, int LAY>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThreads, 1)
     dmma_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       const LevelArgs p) {
-  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  using C = GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>;
+  constexpr int BW = (LAY == 1) ? 4 : 8;  // B box width (columns)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BM][BK] swizzled
-  double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);  // [STAGES][BN/8][BK][8]
+  double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BK/4][BM][4]
+  double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);  // [STAGES][BN/4][BK][4]
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
-  const TileCoord tc = map_tile<BM, BN>(p, blockIdx.x);
+  const TileCoord tc = map_tile<BM, BN, BK>(p, blockIdx.x);
   if (!tc.valid) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nk = (tc.k_end - tc.k_begin + BK - 1) / BK;
@@ -173,11 +180,20 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
         if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         const int64_t k = tc.k_begin + kt * BK;
-        tma_load_2d(sA + (size_t)s * BM * BK, &mapA, (int32_t)(tc.a_col + k), (int32_t)tc.a_row, &full[s]);
+        double* sa = sA + (size_t)s * BM * BK;
+        if (LAY == 0) {
+#pragma unroll
+          for (int kb = 0; kb < BK / 16; ++kb)
+            tma_load_2d(sa + kb * BM * 16, &mapA, (int32_t)(tc.a_col + k + 16 * kb), (int32_t)tc.a_row, &full[s]);
+        } else {
+#pragma unroll
+          for (int kb = 0; kb < BK / 4; ++kb)
+            tma_load_2d(sa + kb * BM * 4, &mapA, (int32_t)(tc.a_col + k + 4 * kb), (int32_t)tc.a_row, &full[s]);
+        }
         double* sb = sB + (size_t)s * BK * BN;
 #pragma unroll
-        for (int nb = 0; nb < BN / 8; ++nb)
-          tma_load_2d(sb + nb * BK * 8, &mapB, (int32_t)(tc.b_col + nb * 8), (int32_t)(tc.b_row + k), &full[s]);
+        for (int nb = 0; nb < BN / BW; ++nb)
+          tma_load_2d(sb + nb * BK * BW, &mapB, (int32_t)(tc.b_col + nb * BW), (int32_t)(tc.b_row + k), &full[s]);
       }
     }
     return;
@@ -206,26 +222,31 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
     for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int lr = lane >> 2, lc = lane & 3;
+  // per-lane fragment offsets (doubles); A[row][k], B[k][col] with k = kk*4 + lc
+  const int a_base = (wm * C::WTM + lr) * 4 + lc;                    // LAY 1/2: box k/4 of [BM][4]
+  const int b_col = wn * C::WTN + lr;                                  // + ni*8
+  const int b_base = (b_col / BW) * BK * BW + lc * BW + (b_col % BW);  // box col/BW of [BK][BW]
   for (int64_t kt = 0; kt < nk; ++kt) {
     const int s = (int)(kt % STAGES);
     mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
-    const unsigned char* a_st = reinterpret_cast<const unsigned char*>(sA + (size_t)s * BM * BK);
-    const double* b_st = sB + (size_t)s * BK * BN;
+    const double* a_st = sA + (size_t)s * BM * BK;
+    const double* b_st = sB + (size_t)s * BK * BN + b_base;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double af[C::FM], bf[C::FN];
-      const int kcol = kk * 4 + lc;  // column inside the 16-wide A box
 #pragma unroll
       for (int mi = 0; mi < C::FM; ++mi) {
-        const int row = wm * C::WTM + mi * 8 + lr;
-        const int off = row * 128 + ((((kcol >> 1) ^ (row & 7)) << 4) | ((kcol & 1) << 3));
-        af[mi] = *reinterpret_cast<const double*>(a_st + off);
+        if (LAY == 0) {  // 16-wide boxes with 128-byte swizzle: chunk (k/2) ^ (row % 8)
+          const int row = wm * C::WTM + mi * 8 + lr;
+          const int kc = (kk & 3) * 4 + lc;
+          const int off = (kk >> 2) * BM * 16 + row * 16 + ((((kc >> 1) ^ (row & 7)) << 1) | (kc & 1));
+          af[mi] = a_st[off];
+        } else {
+          af[mi] = a_st[a_base + kk * BM * 4 + mi * 32];
+        }
       }
 #pragma unroll
-      for (int ni = 0; ni < C::FN; ++ni) {
-        const int box = (wn * C::WTN + ni * 8) >> 3;
-        bf[ni] = b_st[box * BK * 8 + kcol * 8 + lr];
-      }
+      for (int ni = 0; ni < C::FN; ++ni) bf[ni] = b_st[kk * 4 * BW + (ni * 8 / BW) * BK * BW];
 #pragma unroll
       for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
@@ -252,12 +273,13 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int BK = 16, int LAY = 1>
 static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
-  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  using C = GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>;
+  constexpr int BW = (LAY == 1) ? 4 : 8;
   CUtensorMap mA, mB;
-  if (!encode_map(&mA, a.opA, BK, BM, true)) return cudaErrorInvalidValue;
-  if (!encode_map(&mB, a.opB, 8, BK, false)) return cudaErrorInvalidValue;
+  if (!encode_map(&mA, a.opA, LAY == 0 ? 16 : 4, BM, LAY == 0)) return cudaErrorInvalidValue;
+  if (!encode_map(&mB, a.opB, BW, BK, false)) return cudaErrorInvalidValue;
   int64_t tiles;
   if (a.mode == MODE_UL) {
     const int64_t T = (a.n + BM - 1) / BM;
@@ -267,8 +289,8 @@ static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launc
   }
   if (tiles <= 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES, BK, LAY>;
+  set_smem_once<k>((int)C::SMEM);
   k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -298,7 +320,19 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) 
   // Tile size follows the level: min(b, 128) (b is a power of two >= 32 for
   // the triangular modes; UL uses 128).
   const int64_t t = (a.mode == MODE_UL) ? 128 : (a.b < 128 ? a.b : 128);
-  if (t >= 128) return launch_cfg<128, 128, 2, 4, 5>(a, s, launches);
+  if (t >= 128) {
+    static const int variant = [] {
+      const char* e = getenv("TRINV_GEMM_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    // LAY 1 measured best on B200 (config 3: 93.8% vs 92.7% for the swizzled LAY 0,
+    // profiles/r01_gemm_variants.txt); the others stay selectable for tuning.
+    switch (variant) {
+      case 2: return launch_cfg<128, 128, 2, 4, 5, 16, 0>(a, s, launches);
+      case 3: return launch_cfg<128, 128, 2, 4, 5, 16, 2>(a, s, launches);
+      default: return launch_cfg<128, 128, 2, 4, 5, 16, 1>(a, s, launches);
+    }
+  }
   if (t >= 64) return launch_cfg<64, 64, 2, 2, 4>(a, s, launches);
   return launch_cfg<32, 32, 2, 2, 4>(a, s, launches);
 }

@@ -3,9 +3,37 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace trinv {
+
+// Cached per-device SM count (host).
+inline int device_sms() {
+  static std::atomic<int> cache[64];
+  int d = 0;
+  cudaGetDevice(&d);
+  d &= 63;
+  int v = cache[d].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device.
+template <auto Kernel>
+inline void set_smem_once(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
 
 // ---- leaf / batched kernels (leaf.cu) ------------------------------------------
 struct LeafArgs {

@@ -114,7 +114,7 @@ static size_t w_bytes(int64_t n) {
 static size_t mat_bytes(int64_t n) { return (size_t)n * (size_t)even_up(n) * sizeof(double); }
 
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
-  if (n <= 32) return 0;  // a single leaf: no products, any layout
+  if (n <= 64) return 0;  // a single leaf: no products, any layout
   size_t bytes = align_up(w_bytes(n));
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
@@ -144,6 +144,13 @@ static trinv_status_t cuda_fail(cudaError_t e) {
 // info: NULL or a single accumulator already initialised by the caller.
 static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
                               int unit, double* W, int32_t* info, int64_t info_off, cudaStream_t s) {
+  if (n <= 64) {  // one leaf of order n (BASELINE config 0): a single launch
+    LeafArgs l1{};
+    l1.A = A; l1.lda = lda; l1.sA = n * lda; l1.X = X; l1.ldx = ldx; l1.sX = n * ldx;
+    l1.batch = 1; l1.n = (int)n; l1.n_last = (int)n; l1.unit = unit;
+    l1.info = info; l1.info_mode = info ? 2 : 0; l1.info_stride = 0; l1.info_off = info_off;
+    return cuda_fail(launch_leaf(uplo, l1, s, &g_launches));
+  }
   // (a1, a2) leaves: the n/32 full diagonal 32-blocks, then the ragged last one.
   const int64_t full = n / 32, tail = n % 32;
   LeafArgs la{};
@@ -202,7 +209,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   const size_t need = tri_ws(n, A, lda, X, ldx);
   if (ws_bytes < need || (need > 0 && ws == nullptr)) return TRINV_WORKSPACE_TOO_SMALL;
   if (init_info && info) TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
-  if (n <= 32) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
+  if (n <= 64) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
 
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
@@ -266,7 +273,7 @@ trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* 
   if (n == 0 || batch == 0) return TRINV_OK;
   if (!A || !X || lda < n || ldx < n) return TRINV_INVALID_ARG;
   if (batch > 1 && (strideA < n * lda || strideX < n * ldx)) return TRINV_INVALID_ARG;
-  if (n > 32) return TRINV_NOT_SUPPORTED;
+  if (n > 64) return TRINV_NOT_SUPPORTED;
   LeafArgs la{};
   la.A = A; la.lda = lda; la.sA = batch > 1 ? strideA : n * lda;
   la.X = X; la.ldx = ldx; la.sX = batch > 1 ? strideX : n * ldx;

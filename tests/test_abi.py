@@ -45,7 +45,7 @@ def test_batched_argument_validation():
     assert f(b"L", 32, 0, None, 32, 1024, None, 32, 1024, 0, None, None) == _lib.TRINV_OK
     assert f(b"X", 32, 4, FAKE, 32, 1024, FAKE2, 32, 1024, 0, None, None) == _lib.TRINV_INVALID_ARG
     assert f(b"L", 32, 4, FAKE, 32, 1000, FAKE2, 32, 1024, 0, None, None) == _lib.TRINV_INVALID_ARG
-    assert f(b"L", 64, 4, FAKE, 64, 4096, FAKE2, 64, 4096, 0, None, None) == _lib.TRINV_NOT_SUPPORTED
+    assert f(b"L", 65, 4, FAKE, 65, 65 * 65, FAKE2, 65, 65 * 65, 0, None, None) == _lib.TRINV_NOT_SUPPORTED
 
 
 def test_inv_from_lu_argument_validation():
@@ -58,7 +58,7 @@ def test_inv_from_lu_argument_validation():
 
 def test_workspace_sizes():
     ws = P.lib().trinv_workspace_bytes
-    assert ws(b"L", 32, None, 32, None, 32) == 0
+    assert ws(b"L", 64, None, 64, None, 64) == 0
     n = 32768
     assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
     assert ws(b"U", 1000, None, 1000, None, 1000) > 0

@@ -35,10 +35,10 @@ def test_config1_full_batch():
     assert torch.equal(Ad.cpu(), torch.from_numpy(A))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 17, 30, 31, 32])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 17, 30, 31, 32, 33, 40, 47, 63, 64])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_orders_and_uplo(n, uplo):
-    B = 6 * 148 * 2 + 5  # more than one matrix per warp, ragged tail
+    B = 8 * 148 * 2 + 5 if n <= 32 else 6 * 148 + 3  # several matrices per warp / CTA, ragged tail
     diag = "signed" if uplo == "L" else "pos"
     A = synth.host(n, batch=B, uplo=uplo, diag=diag)
     X, info = _run(A, uplo)
@@ -50,7 +50,7 @@ def test_orders_and_uplo(n, uplo):
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_unit_ignores_diag_and_nan_other_triangle(uplo):
-    B, n = 1000, 32
+    B, n = 1000, 32 if uplo == "L" else 48
     A = synth.host(n, batch=B, uplo=uplo)
     A1 = A.copy()
     idx = np.arange(n)

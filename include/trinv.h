@@ -100,6 +100,24 @@ trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* 
                              int64_t strideA, double* X, int64_t ldx, int64_t strideX,
                              trinv_diag_t diag, int32_t* d_info, void* stream);
 
+/* Batched inverses of HOST-resident matrices (the end-to-end path): A_host and
+ * X_host are host pointers to contiguous [batch][n][n] row-major arrays
+ * (page-locked memory is required for the copies to overlap; pageable memory
+ * works but serialises).  The batch is processed in chunks of `chunk` matrices
+ * (0 = default 4096) cycling through TRINV_HOST_SLOTS device slots carved from
+ * `ws`: the host->device copy of chunk i+1, the in-place inversion of chunk i
+ * (trinv_batched) and the device->host copy of chunk i-1 run concurrently on
+ * two internal copy streams and `stream`, ordered by events.  The call only
+ * enqueues; when `stream` reaches the work enqueued by this call, every X_host
+ * row is written.  X_host may equal A_host.  ws_bytes >=
+ * trinv_batched_host_workspace_bytes(n, chunk); d_info as for trinv_batched
+ * (device int32[batch] or NULL).  n <= 64. */
+#define TRINV_HOST_SLOTS 4
+size_t trinv_batched_host_workspace_bytes(int64_t n, int64_t chunk);
+trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const double* A_host, double* X_host,
+                                  trinv_diag_t diag, int64_t chunk, void* ws, size_t ws_bytes, int32_t* d_info,
+                                  void* stream);
+
 /* General inverse from triangular factors, X = (L U)^{-1} = U^{-1} L^{-1}
  * (SKUL, "S K = A^{-1}" with S = U^{-1}, K = L^{-1}): L^{-1} and
  * U^{-1} by the two calls above, then the upper x lower product

@@ -8,7 +8,8 @@ PyTorch fallback — if libtrinv.so is missing or no GPU is present the calls ra
 
     X = trinv_lower(L)            # L^{-1}, full matrix, +0.0 above the diagonal
     X = trinv_upper(U)            # U^{-1}
-    X = trinv_batched(A, "L")     # A: [B, n, n], n <= 32
+    X = trinv_batched(A, "L")     # A: [B, n, n] on the device, n <= 64
+    X = trinv_batched_host(Ah)    # Ah: host [B, n, n]; pipelined H2D / invert / D2H
     X = inv_from_lu(L, U)         # (L U)^{-1} = U^{-1} L^{-1}, L unit by default
 """
 import ctypes
@@ -17,7 +18,7 @@ import os
 from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMatrixError,  # noqa: F401
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
-__all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "inv_from_lu", "workspace_bytes",
+__all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -108,7 +109,7 @@ def trinv_upper(A, *, unit=False, out=None, check=False, stream=None):
 
 
 def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None):
-    """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 32.  Returns X, or (X, info[B]) if info."""
+    """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 64.  Returns X, or (X, info[B]) if info."""
     torch = _torch()
     if A.dim() != 3 or A.shape[1] != A.shape[2]:
         raise ValueError("expected [B, n, n]")
@@ -124,6 +125,31 @@ def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None)
                                TRINV_UNIT if unit else TRINV_NON_UNIT,
                                ctypes.c_void_p(inf.data_ptr()) if inf is not None else None,
                                _stream(stream)))
+    return (X, inf) if info else X
+
+
+def trinv_batched_host(A_host, uplo="L", *, unit=False, out=None, chunk=0, info=False, device=None,
+                       stream=None):
+    """Invert a HOST batch [B, n, n] (contiguous, ideally pinned): chunked H2D / invert / D2H
+    pipeline on the current CUDA device.  Returns the host tensor X (or (X, info[B] on device))."""
+    torch = _torch()
+    if A_host.is_cuda or A_host.dim() != 3 or A_host.shape[1] != A_host.shape[2]:
+        raise ValueError("expected a host tensor [B, n, n]")
+    if A_host.dtype != torch.float64 or not A_host.is_contiguous():
+        raise ValueError("expected a contiguous float64 host tensor")
+    B, n = A_host.shape[0], A_host.shape[1]
+    X = torch.empty_like(A_host, pin_memory=A_host.is_pinned()) if out is None else out
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    wsb = lib().trinv_batched_host_workspace_bytes(n, chunk)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    inf = torch.empty(B, dtype=torch.int32, device=dev) if info else None
+    _check(lib().trinv_batched_host(uplo.encode(), n, B, ctypes.c_void_p(A_host.data_ptr()),
+                                    ctypes.c_void_p(X.data_ptr()), TRINV_UNIT if unit else TRINV_NON_UNIT,
+                                    chunk, ctypes.c_void_p(ws.data_ptr()), wsb,
+                                    ctypes.c_void_p(inf.data_ptr()) if inf is not None else None,
+                                    _stream(stream)))
+    # keep the workspace alive until the stream has consumed it
+    ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
     return (X, inf) if info else X
 
 

@@ -50,6 +50,10 @@ def lib():
         f.restype = _i32
     L.trinv_batched.argtypes = [ctypes.c_char, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp]
     L.trinv_batched.restype = _i32
+    L.trinv_batched_host_workspace_bytes.argtypes = [_i64, _i64]
+    L.trinv_batched_host_workspace_bytes.restype = _sz
+    L.trinv_batched_host.argtypes = [ctypes.c_char, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp]
+    L.trinv_batched_host.restype = _i32
     L.inv_from_lu.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _vp]
     L.inv_from_lu.restype = _i32
     L.trinv_status_string.argtypes = [_i32]

@@ -233,8 +233,12 @@ __global__ void __launch_bounds__(128) leaf_plain_kernel(const LeafArgs a) {
   for (int64_t b = (int64_t)blockIdx.x * 4 + warp; b < a.batch; b += (int64_t)gridDim.x * 4) {
     const int nb = (b == a.batch - 1) ? a.n_last : a.n;
     const double* src = a.A + b * a.sA;
-    for (int i = 0; i < nb; ++i)
-      if (lane < nb) T[i * LEAF + lane] = src[i * a.lda + lane];
+    double v[LEAF];
+#pragma unroll
+    for (int i = 0; i < LEAF; ++i) v[i] = (i < nb && lane < nb) ? src[(int64_t)i * a.lda + lane] : 0.0;
+#pragma unroll
+    for (int i = 0; i < LEAF; ++i)
+      if (i < nb) T[i * LEAF + lane] = v[i];
     __syncwarp();
     double x[LEAF];
     bool singular;

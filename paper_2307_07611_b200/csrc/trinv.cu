@@ -282,6 +282,71 @@ trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* 
   return cuda_fail(launch_leaf(uplo, la, (cudaStream_t)stream, &g_launches));
 }
 
+static int64_t host_chunk(int64_t chunk) { return chunk > 0 ? chunk : 4096; }
+
+size_t trinv_batched_host_workspace_bytes(int64_t n, int64_t chunk) {
+  if (n <= 0) return 0;
+  return (size_t)TRINV_HOST_SLOTS * align_up((size_t)host_chunk(chunk) * n * n * sizeof(double));
+}
+
+trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const double* A_host, double* X_host,
+                                  trinv_diag_t diag, int64_t chunk, void* ws, size_t ws_bytes, int32_t* d_info,
+                                  void* stream) {
+  if ((uplo != 'L' && uplo != 'U') || n < 0 || batch < 0 || chunk < 0) return TRINV_INVALID_ARG;
+  if (diag != TRINV_UNIT && diag != TRINV_NON_UNIT) return TRINV_INVALID_ARG;
+  if (n == 0 || batch == 0) return TRINV_OK;
+  if (!A_host || !X_host) return TRINV_INVALID_ARG;
+  if (n > 64) return TRINV_NOT_SUPPORTED;
+  chunk = host_chunk(chunk);
+  const size_t slot_bytes = align_up((size_t)chunk * n * n * sizeof(double));
+  if (!ws || ws_bytes < trinv_batched_host_workspace_bytes(n, chunk)) return TRINV_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  cudaEvent_t start, loaded[TRINV_HOST_SLOTS], done[TRINV_HOST_SLOTS], freed[TRINV_HOST_SLOTS];
+  TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (int i = 0; i < TRINV_HOST_SLOTS; ++i) {
+    TRY(cudaEventCreateWithFlags(&loaded[i], cudaEventDisableTiming));
+    TRY(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    TRY(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+  }
+  // the copies may start only after the work already enqueued on `stream`
+  TRY(cudaEventRecord(start, s));
+  TRY(cudaStreamWaitEvent(h2d, start, 0));
+  trinv_status_t st = TRINV_OK;
+  for (int64_t c = 0; c < nchunks && st == TRINV_OK; ++c) {
+    const int slot = (int)(c % TRINV_HOST_SLOTS);
+    double* buf = reinterpret_cast<double*>(static_cast<char*>(ws) + slot * slot_bytes);
+    const int64_t b0 = c * chunk, cnt = std::min(chunk, batch - b0);
+    const size_t bytes = (size_t)cnt * n * n * sizeof(double);
+    if (c >= TRINV_HOST_SLOTS) TRY(cudaStreamWaitEvent(h2d, freed[slot], 0));
+    TRY(cudaMemcpyAsync(buf, A_host + b0 * n * n, bytes, cudaMemcpyHostToDevice, h2d));
+    TRY(cudaEventRecord(loaded[slot], h2d));
+    TRY(cudaStreamWaitEvent(s, loaded[slot], 0));
+    LeafArgs la{};
+    la.A = buf; la.lda = n; la.sA = n * n; la.X = buf; la.ldx = n; la.sX = n * n;
+    la.batch = cnt; la.n = (int)n; la.n_last = (int)n; la.unit = (int)diag;
+    la.info = d_info ? d_info + b0 : nullptr; la.info_mode = d_info ? 1 : 0;
+    st = cuda_fail(launch_leaf(uplo, la, s, &g_launches));
+    if (st != TRINV_OK) break;
+    TRY(cudaEventRecord(done[slot], s));
+    TRY(cudaStreamWaitEvent(d2h, done[slot], 0));
+    TRY(cudaMemcpyAsync(X_host + b0 * n * n, buf, bytes, cudaMemcpyDeviceToHost, d2h));
+    TRY(cudaEventRecord(freed[slot], d2h));
+  }
+  // `stream` observes completion of every device->host copy
+  TRY(cudaStreamWaitEvent(s, freed[(nchunks - 1) % TRINV_HOST_SLOTS], 0));
+  cudaEventDestroy(start);
+  for (int i = 0; i < TRINV_HOST_SLOTS; ++i) {
+    cudaEventDestroy(loaded[i]); cudaEventDestroy(done[i]); cudaEventDestroy(freed[i]);
+  }
+  cudaStreamDestroy(h2d);
+  cudaStreamDestroy(d2h);
+  return st;
+}
+
 trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu, double* X,
                            int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU, void* ws, size_t ws_bytes,
                            int32_t* d_info, void* stream) {

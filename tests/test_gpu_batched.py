@@ -124,3 +124,23 @@ def test_singular_info_and_determinism():
     # sub-batch gives the same bits (sharding invariance, P-l)
     X3 = P.trinv_batched(At[1000:1500].contiguous())
     assert torch.equal(X3, X1[1000:1500])
+
+
+@pytest.mark.parametrize("uplo,n,B,chunk", [("L", 32, 20000, 0), ("U", 32, 9000, 1000), ("L", 17, 5000, 777),
+                                            ("L", 48, 3000, 512)])
+def test_host_pipeline(uplo, n, B, chunk):
+    """trinv_batched_host: host buffers, chunked H2D / invert / D2H pipeline (the e2e path)."""
+    A = synth.host(n, batch=B, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    Ah = torch.from_numpy(A).pin_memory()
+    X, info = P.trinv_batched_host(Ah, uplo, chunk=chunk, info=True)
+    torch.cuda.synchronize()
+    assert oracle.floored_rel_err(X.numpy(), oracle.crit_batched(A, uplo)) <= REL_TOL
+    assert int(info.abs().sum()) == 0
+    # the device path gives the same bits
+    Xd = P.trinv_batched(torch.from_numpy(A).to(DEV), uplo)
+    assert torch.equal(Xd.cpu(), X)
+    # pageable memory works too (serialised copies), and in place X == A
+    Ap = torch.from_numpy(A.copy())
+    P.trinv_batched_host(Ap, uplo, out=Ap, chunk=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(Ap, X)

@@ -158,12 +158,13 @@ template <bool UPPER, int WARPS, int NS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     leaf32_tma_kernel(const __grid_constant__ CUtensorMap band0, const __grid_constant__ CUtensorMap band1,
                       const LeafArgs a) {
+  constexpr int SLOT = kBand;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * kBand;
-  double* rr = reinterpret_cast<double*>(smem_raw) + (size_t)WARPS * NS * kBand + warp * LEAF;
+  double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * SLOT;
+  double* rr = reinterpret_cast<double*>(smem_raw) + (size_t)WARPS * NS * SLOT + warp * LEAF;
   uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem_raw + ((size_t)WARPS * NS * kBand + WARPS * LEAF) * 8) + warp * NS;
+      reinterpret_cast<uint64_t*>(smem_raw + ((size_t)WARPS * NS * SLOT + WARPS * LEAF) * 8) + warp * NS;
 
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t TW = (int64_t)gridDim.x * WARPS;
@@ -182,9 +183,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   auto issue_load = [&](int64_t t) {  // lane 0 only
     const int b = (int)(gw + t * TW);
-    double* slot = slots + (t % NS) * kBand;
+    double* slot = slots + (t % NS) * SLOT;
     uint64_t* bar = &bars[t % NS];
-    mbar_arrive_expect_tx(bar, kBand * 8);
+    mbar_arrive_expect_tx(bar, SLOT * 8);
     if (!UPPER) {
       tma_load_3d(slot, &band0, 0, 0, b, bar);         // rows 0-15, cols 0-15
       tma_load_3d(slot + 256, &band1, 0, 16, b, bar);  // rows 16-31, cols 0-31
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   for (int64_t t = 0; t < count; ++t) {
     const int64_t b = gw + t * TW;
-    double* slot = slots + (t % NS) * kBand;
+    double* slot = slots + (t % NS) * SLOT;
     mbar_wait(&bars[t % NS], (uint32_t)((t / NS) & 1));
 
     double x[LEAF];
@@ -361,21 +362,35 @@ __global__ void __launch_bounds__(64) leaf64_kernel(const LeafArgs a) {
   }
 }
 
+
 // ---------------------------------------------------------------------------
-constexpr int kTriWarps = 8, kTriSlots = 4;
-constexpr size_t kTriSmem =
-    ((size_t)kTriWarps * kTriSlots * kBand + kTriWarps * LEAF) * 8 + kTriWarps * kTriSlots * 8;
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// 3-D view [batch][32 rows][32 cols] of the inputs; box = 16 rows x `cols` columns x 1 matrix.
-static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols) {
+// 3-D view [batch][32 rows][32 cols] of the inputs; box = `rows` rows x `cols` columns x 1 matrix.
+static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols, int rows = 16) {
   const uint64_t dims[3] = {32, 32, (uint64_t)a.batch};
   const uint64_t strides[2] = {(uint64_t)a.lda * 8, (uint64_t)a.sA * 8};
-  const uint32_t box[3] = {(uint32_t)cols, 16, 1};
+  const uint32_t box[3] = {(uint32_t)cols, (uint32_t)rows, 1};
   return encode_map_nd(m, a.A, 3, dims, strides, box);
 }
 
+template <int W, int NS>
+static void launch_band(char uplo, const CUtensorMap& m0, const CUtensorMap& m1, const LeafArgs& a, int sms,
+                        cudaStream_t s) {
+  constexpr size_t smem = ((size_t)W * NS * kBand + W * LEAF) * 8 + W * NS * 8;
+  const int64_t ctas_needed = (a.batch + W - 1) / W;
+  const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
+  if (uplo == 'L') {
+    constexpr auto k = leaf32_tma_kernel<false, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(m0, m1, a);
+  } else {
+    constexpr auto k = leaf32_tma_kernel<true, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(m0, m1, a);
+  }
+}
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.batch <= 0) return cudaSuccess;
   const int sms = device_sms();
@@ -393,21 +408,17 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
     return cudaGetLastError();
   }
   const bool full32 = a.n == LEAF && a.n_last == LEAF;
-  CUtensorMap m16, m32;
-  const bool maps = full32 && a.batch < (int64_t)1 << 31 && encode_batch_map(&m16, a, 16) && encode_batch_map(&m32, a, 32);
-  if (tma && full32 && maps) {
-    const int64_t ctas_needed = (a.batch + kTriWarps - 1) / kTriWarps;
-    const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
-    if (uplo == 'L') {
-      constexpr auto k = leaf32_tma_kernel<false, kTriWarps, kTriSlots>;
-      set_smem_once<k>((int)kTriSmem);
-      k<<<grid, kTriWarps * 32, kTriSmem, s>>>(m16, m32, a);
-    } else {
-      constexpr auto k = leaf32_tma_kernel<true, kTriWarps, kTriSlots>;
-      set_smem_once<k>((int)kTriSmem);
-      k<<<grid, kTriWarps * 32, kTriSmem, s>>>(m16, m32, a);
+  // n = 32, TMA-compatible layout: 8 warps x 3 slots per CTA (one CTA per SM) measured best on B200
+  // (profiles/r01_leaf_variants.txt).
+  bool launched = false;
+  if (tma && full32 && a.batch < (int64_t)1 << 31) {
+    CUtensorMap m16, m32;
+    if (encode_batch_map(&m16, a, 16) && encode_batch_map(&m32, a, 32)) {
+      launch_band<8, 3>(uplo, m16, m32, a, sms, s);
+      launched = true;
     }
-  } else {
+  }
+  if (!launched) {
     const int64_t ctas_needed = (a.batch + 3) / 4;
     const int grid = (int)(ctas_needed < (int64_t)sms * 8 ? ctas_needed : (int64_t)sms * 8);
     if (uplo == 'L')

@@ -317,9 +317,20 @@ static double level_flops(const LevelArgs& a) {
 
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
   ProfileScope prof(KIND_DMMA, level_flops(a), 0.0, s);
-  // Tile size follows the level: min(b, 128) (b is a power of two >= 32 for
-  // the triangular modes; UL uses 128).
-  const int64_t t = (a.mode == MODE_UL) ? 128 : (a.b < 128 ? a.b : 128);
+  // Tile size per level: the largest of 128 / 64 / 32 (not above b) that still
+  // gives at least two CTAs per SM; mid-size levels otherwise leave SMs idle
+  // behind a few long triangular tiles (profiles/r01_sweep_n.txt).
+  const int sms = device_sms();
+  auto tiles = [&](int64_t T) {
+    if (a.mode == MODE_UL) { const int64_t m = (a.n + T - 1) / T; return m * m; }
+    const int64_t m = (a.b + T - 1) / T;
+    return a.merges * m * m;
+  };
+  int64_t t = 32;
+  for (int64_t T : {128, 64}) {
+    if ((a.mode == MODE_UL || T <= a.b) && tiles(T) >= 2 * sms) { t = T; break; }
+  }
+  if (a.mode != MODE_UL && t > a.b) t = a.b;
   if (t >= 128) {
     static const int variant = [] {
       const char* e = getenv("TRINV_GEMM_VARIANT");

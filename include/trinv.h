@@ -58,6 +58,7 @@ typedef enum { TRINV_NON_UNIT = 0, TRINV_UNIT = 1 } trinv_diag_t;
  * "aligned") with leading dimensions lda / ldx: an odd leading dimension or a
  * misaligned pointer makes the call stage that matrix through the workspace.
  * For 'G', A = L factor, X = output; the U factor is assumed laid out like L.
+ * 'F' = lu_crout (A, X ignored), 'A' = inv_general (A = input, X = output).
  * Returns 0 for n <= 0 or an unknown op. */
 size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx);
 
@@ -130,6 +131,41 @@ trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const dou
 trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu,
                            double* X, int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU,
                            void* ws, size_t ws_bytes, int32_t* d_info, void* stream);
+
+/* ---- NEXT row f2: general inverse from A ---------------------------
+ * Crout factorisation without pivoting, A = L U with L lower (diagonal kept) and
+ * U UNIT upper — the convention of the paper's SKUL (Alg. 5, "U_ii <- 1",
+ * L_ij = A_ij - L_i,1:j-1 U_1:j-1,j, U_ij = (A_ij - L_i,1:i-1 U_1:i-1,j)/L_ii).
+ * In place, packed: on return the lower triangle with the diagonal holds L and the
+ * strict upper triangle holds U.  Blocked right-looking recursion: diagonal blocks
+ * <= 64 in shared memory, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
+ * through the triangular inverses above and the DMMA engine, Schur complement on
+ * the DMMA engine.  As in the paper there is no pivoting: the leading principal
+ * minors must be non-zero; an exact zero pivot k sets d_info = 1 + k (output then
+ * unspecified).  A: device, 16-byte aligned with even lda when n > 64
+ * (TRINV_NOT_SUPPORTED otherwise).  ws_bytes >= trinv_workspace_bytes('F', n, ...). */
+trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_bytes, int32_t* d_info,
+                        void* stream);
+
+/* X = A^{-1} for a general non-singular A with non-zero leading principal minors:
+ * lu_crout on a copy of A, then inv_from_lu(L, U unit) — SKUL's S K = A^{-1}
+ * (P:799-803).  A is read-only (any layout); X must not overlap A.  2 n^3 flops.
+ * ws_bytes >= trinv_workspace_bytes('A', n, A, lda, X, ldx). */
+trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx, void* ws,
+                           size_t ws_bytes, int32_t* d_info, void* stream);
+
+/* The DMMA product engine as a batched GEMM: for g < batch,
+ *   C_g = alpha * A_g B_g + beta * C_g,
+ * A_g = A + g*strideA (M x K, lda), B_g = B + g*strideB (K x N, ldb), C_g = C +
+ * g*strideC (M x N, ldc), all row-major fp64 on the device.  structA = 'L' / 'U'
+ * declares A lower / upper triangular (M == K; the structurally zero blocks are
+ * skipped, the other triangle of its diagonal tiles must hold zeros); structB
+ * likewise for B (N == K); at most one of them may be triangular; 'N' = dense.
+ * A and B must be 16-byte aligned with even lda/ldb/strides (TRINV_NOT_SUPPORTED
+ * otherwise); C must not overlap A or B.  K >= 1 (K = 0: TRINV_NOT_SUPPORTED). */
+trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,
+                          int64_t lda, int64_t strideA, char structA, const double* B, int64_t ldb, int64_t strideB,
+                          char structB, double beta, double* C, int64_t ldc, int64_t strideC, void* stream);
 
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);

@@ -48,6 +48,8 @@ def lib():
             getattr(L, name).argtypes = [_i64, _dp, _i64, _dp, _i64, ctypes.c_int]
             getattr(L, name).restype = ctypes.c_int
         L.oracle_columns.argtypes = [ctypes.c_char, _i64, _dp, _i64, ctypes.c_int, _i64, _lp, _dp]
+        L.oracle_skul.argtypes = [_i64, _dp, _dp, _dp, _dp, _dp]
+        L.oracle_skul.restype = ctypes.c_int
         L.oracle_lu_columns.argtypes = [_i64, _dp, _i64, ctypes.c_int, _dp, _i64, ctypes.c_int,
                                         _i64, _lp, _dp]
         _lib = L
@@ -124,3 +126,19 @@ def lu_columns(L, U, cols, unit_l=True, unit_u=False):
     lib().oracle_lu_columns(n, _p(L), n, int(unit_l), _p(U), n, int(unit_u), len(cols),
                             cols.ctypes.data_as(_lp), _p(out))
     return out
+
+
+def skul(A):
+    """SKUL (Alg. 5): (L, U, S, K, info) with A = L U (U unit), S = U^{-1}, K = L^{-1}."""
+    A = _c(A); n = A.shape[0]
+    L, U, S, K = (np.empty_like(A) for _ in range(4))
+    info = lib().oracle_skul(n, _p(A), _p(L), _p(U), _p(S), _p(K))
+    return L, U, S, K, info
+
+
+def inv_general(A):
+    """A^{-1} = S K from SKUL; the product is a plain library matmul."""
+    L, U, S, K, info = skul(A)
+    if info:
+        raise ZeroDivisionError(f"zero pivot at {info}")
+    return S @ K

@@ -216,3 +216,59 @@ int oracle_pathsum_lower(int64_t n, const double* L, int64_t ldl, double* X, int
   free(Lt); free(Xt);
   return rc;
 }
+
+/* ---------------------------------------------------------------------------
+ * SKUL (Algorithm 5) written out in the paper's order and notation,
+ * 0-based: Crout factorisation A = L U (U_ii = 1) with the inverse factors
+ * S = U^{-1} (by CRIT*, row recurrence) and K = L^{-1} computed online, and
+ * finally K <- K D (D = diag(1/L_ii)).  S K = A^{-1}.  No pivoting
+ * (the paper has none); returns 1 + i at the first zero L_ii, 0 otherwise.
+ * All outputs are n x n row-major with leading dimension n.  The listing's
+ * "S_{1,2} = -U_{1,2}" line is the l = 1, i = 1 instance of the S update and is
+ * realised by running that update for i = 1 as well (reading C3 of DESIGN.md).
+ * ------------------------------------------------------------------------- */
+int oracle_skul(int64_t n, const double* A, double* L, double* U, double* S, double* K) {
+  const int64_t N = n;
+  double* D = (double*)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+  for (int64_t k = 0; k < N * N; ++k) { L[k] = 0.0; U[k] = 0.0; S[k] = 0.0; K[k] = 0.0; }
+  int info = 0;
+  for (int64_t i = 0; i < N; ++i) {                       /* for i = 1..n */
+    L[i * N + 0] = A[i * N + 0];                          /*   L_{i,1} = A_{i,1} */
+    U[i * N + i] = 1.0; S[i * N + i] = 1.0; K[i * N + i] = 1.0;
+  }
+  if (N == 0) { free(D); return 0; }
+  if (L[0] == 0.0) info = 1;
+  for (int64_t j = 1; j < N; ++j) U[0 * N + j] = A[0 * N + j] / L[0];  /* U_{1,j} = A_{1,j}/L_{1,1} */
+  D[0] = 1.0 / L[0];
+  if (N > 1) S[0 * N + 1] = -U[0 * N + 1];                 /* S_{1,2} = -U_{1,2} */
+  for (int64_t i = 1; i < N; ++i) {                        /* for i = 2..n */
+    for (int64_t j = 1; j <= i; ++j) {                     /*   L_{i,j} = A_{i,j} - L_{i,1:j-1} . U_{1:j-1,j} */
+      double dot = 0.0;
+      for (int64_t p = 0; p < j; ++p) dot += L[i * N + p] * U[p * N + j];
+      L[i * N + j] = A[i * N + j] - dot;
+    }
+    if (L[i * N + i] == 0.0 && !info) info = (int)(i + 1);
+    D[i] = 1.0 / L[i * N + i];                             /*   D_{i,i} = 1/L_{i,i} */
+    for (int64_t j = 0; j < i; ++j) {                      /*   K_{i,j} = -L_{i,1:i} . K_{1:i,j} D_{i,i} */
+      double dot = 0.0;
+      for (int64_t p = 0; p <= i; ++p) dot += L[i * N + p] * K[p * N + j];
+      K[i * N + j] = -dot * D[i];
+    }
+    for (int64_t j = i + 1; j < N; ++j) {                  /*   U_{i,j} = (A_{i,j} - L_{i,1:i-1} . U_{1:i-1,j}) / L_{i,i} */
+      double dot = 0.0;
+      for (int64_t p = 0; p < i; ++p) dot += L[i * N + p] * U[p * N + j];
+      U[i * N + j] = (A[i * N + j] - dot) / L[i * N + i];
+    }
+    if (i < N - 1) {                                       /*   S_{l,i+1} = -S_{l,l:i} . U_{l:i,i+1}, l = 1..i */
+      for (int64_t l = 0; l <= i; ++l) {
+        double dot = 0.0;
+        for (int64_t p = l; p <= i; ++p) dot += S[l * N + p] * U[p * N + i + 1];
+        S[l * N + i + 1] = -dot;
+      }
+    }
+  }
+  for (int64_t i = 0; i < N; ++i)                          /* K <- K D */
+    for (int64_t j = 0; j < N; ++j) K[i * N + j] *= D[j];
+  free(D);
+  return info;
+}

@@ -18,7 +18,8 @@ import os
 from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMatrixError,  # noqa: F401
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
-__all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "workspace_bytes",
+__all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "inv_general",
+           "lu_crout", "gemm", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -36,7 +37,9 @@ def _ld(t):
         raise ValueError("expected a CUDA tensor (device memory); host buffers: copy with .cuda() first")
     if t.shape[-1] > 1 and t.stride(-1) != 1:
         raise ValueError("row-major layout required (stride(-1) == 1)")
-    return max(t.stride(-2), t.shape[-1]) if t.shape[-2] > 1 else t.shape[-1]
+    if t.shape[-2] > 1 or t.stride(-2) >= t.shape[-1]:
+        return max(t.stride(-2), t.shape[-1])
+    return t.shape[-1]
 
 
 def _stream(stream):
@@ -151,6 +154,61 @@ def trinv_batched_host(A_host, uplo="L", *, unit=False, out=None, chunk=0, info=
     # keep the workspace alive until the stream has consumed it
     ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
     return (X, inf) if info else X
+
+
+def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", stream=None):
+    """C = alpha A B + beta C on the DMMA engine; A [.., M, K], B [.., K, N] (optionally batched
+    with a leading batch dimension); struct_a / struct_b = 'L' / 'U' declare a triangular operand."""
+    torch = _torch()
+    batched = A.dim() == 3
+    if batched != (B.dim() == 3):
+        raise ValueError("A and B must both be 2-D or both 3-D")
+    M, K = A.shape[-2], A.shape[-1]
+    N = B.shape[-1]
+    if B.shape[-2] != K:
+        raise ValueError("inner dimensions differ")
+    bs = A.shape[0] if batched else 1
+    if C is None:
+        C = torch.zeros((bs, M, N) if batched else (M, N), dtype=torch.float64, device=A.device)
+    lda, ldb, ldc = _ld(A), _ld(B), _ld(C)
+    sa = A.stride(0) if batched else M * lda
+    sb = B.stride(0) if batched else K * ldb
+    sc = C.stride(0) if batched else M * ldc
+    _check(lib().trinv_gemm(M, N, K, bs, float(alpha), ctypes.c_void_p(A.data_ptr()), lda, sa, struct_a.encode(),
+                            ctypes.c_void_p(B.data_ptr()), ldb, sb, struct_b.encode(), float(beta),
+                            ctypes.c_void_p(C.data_ptr()), ldc, sc, _stream(stream)))
+    return C
+
+
+def lu_crout(A, *, check=False, stream=None):
+    """In-place Crout factorisation without pivoting (SKUL): A <- L\\U packed,
+    L lower with its diagonal, U unit upper (strict upper part stored)."""
+    n = A.shape[-1]
+    lda = _ld(A)
+    ws, wsb = _alloc_ws(workspace_bytes("F", n), A.device)
+    info = _info(check, A.device)
+    _check(lib().lu_crout(n, ctypes.c_void_p(A.data_ptr()), lda,
+                          ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+                          ctypes.c_void_p(info.data_ptr()) if info is not None else None, _stream(stream)))
+    _raise_info(info, "lu_crout")
+    return A
+
+
+def inv_general(A, *, out=None, check=False, stream=None):
+    """X = A^{-1} for a general matrix with non-zero leading principal minors (Crout LU without
+    pivoting, then U^{-1} L^{-1})."""
+    torch = _torch()
+    n = A.shape[-1]
+    lda = _ld(A)
+    X = torch.empty((n, n), dtype=torch.float64, device=A.device) if out is None else out
+    ldx = _ld(X)
+    ws, wsb = _alloc_ws(workspace_bytes("A", n, A, lda, X, ldx), A.device)
+    info = _info(check, A.device)
+    _check(lib().inv_general(n, ctypes.c_void_p(A.data_ptr()), lda, ctypes.c_void_p(X.data_ptr()), ldx,
+                             ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+                             ctypes.c_void_p(info.data_ptr()) if info is not None else None, _stream(stream)))
+    _raise_info(info, "inv_general")
+    return X
 
 
 def inv_from_lu(L, U, *, unit_l=True, unit_u=False, out=None, check=False, stream=None):

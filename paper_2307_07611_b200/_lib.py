@@ -56,6 +56,13 @@ def lib():
     L.trinv_batched_host.restype = _i32
     L.inv_from_lu.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _vp]
     L.inv_from_lu.restype = _i32
+    L.lu_crout.argtypes = [_i64, _vp, _i64, _vp, _sz, _vp, _vp]
+    L.lu_crout.restype = _i32
+    L.inv_general.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp, _vp]
+    L.inv_general.restype = _i32
+    L.trinv_gemm.argtypes = [_i64, _i64, _i64, _i64, ctypes.c_double, _vp, _i64, _i64, ctypes.c_char, _vp, _i64,
+                             _i64, ctypes.c_char, ctypes.c_double, _vp, _i64, _i64, _vp]
+    L.trinv_gemm.restype = _i32
     L.trinv_status_string.argtypes = [_i32]
     L.trinv_status_string.restype = ctypes.c_char_p
     L.trinv_last_cuda_error.restype = _i32

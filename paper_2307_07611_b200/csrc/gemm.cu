@@ -1,9 +1,11 @@
-// gemm.cu — the off-diagonal products of the recursive split on the FP64
-// tensor cores (DESIGN.md §Kernels "K_trmm").
+// gemm.cu — FP64 tensor-core (DMMA) product engine: the off-diagonal products
+// of the recursive split and a
+// general batched GEMM with triangular-operand K-ranges used by the NEXT rows
+// (LU / general inverse, COMBRIT beta = 4, Strassen experiment).
 //
-// One launch covers every merge of one recursion level (COMBRIT with
-// beta = 2, Alg. 1: the n/(2b) merges of a level are independent,
-// P:499-500).  Per merge at offset s with halves b (first) and r (second):
+// Level launches (launch_level): one launch covers every merge of one recursion
+// level (COMBRIT with beta = 2, Alg. 1: the n/(2b) merges of a level
+// are independent).  Per merge at offset s with halves b and r:
 //   lower  inv([A 0; C B]) = [A^{-1} 0; -B^{-1} C A^{-1}  B^{-1}]
 //     MODE_LOWER_1:  W   = C . A^{-1}       tile (I,J): k in [J*BN, b)       (A^{-1} lower)
 //     MODE_LOWER_2:  X21 = -B^{-1} . W      tile (I,J): k in [0, (I+1)*BM)   (B^{-1} lower)
@@ -18,46 +20,61 @@
 // +0.0 over the mirrored tile of the opposite triangle (row a7).
 //
 // Engine: CTA tile BM x BN, K-step BK = 16, STAGES-deep smem ring filled by
-// TMA (cp.async.bulk.tensor.2d) from a producer warp through full/empty
+// TMA (cp.async.bulk.tensor) from a producer warp through full/empty
 // mbarriers; WM x WN consumer warps issue mma.sync.m8n8k4.f64 (DMMA.8x8x4).
-// Shared-memory layouts are chosen for the m8n8k4 fragments, whose 64-bit loads
-// are served per half-warp (16 lanes = 128 B must cover the 32 banks once):
-// A tile = BK/4 boxes of [BM rows][4 k] (32-byte rows), B tile = BN/4 boxes of
-// [BK rows][4 n]; each half-warp fragment load then reads 128 contiguous bytes.
-// Out-of-range rows / columns (ragged last merge, n not a multiple of the
-// tile) are zero-filled by TMA and clipped at the store.
+// Shared-memory layout for the m8n8k4 fragments, whose 64-bit loads are served
+// per half-warp (16 lanes = 128 B must cover the 32 banks once): A tile = BK/4
+// boxes of [BM rows][4 k], B tile = BN/4 boxes of [BK rows][4 n]; each
+// half-warp fragment load reads 128 contiguous bytes (measured best of three
+// layouts, profiles/r01_gemm_variants.txt).  Out-of-range rows / columns are
+// zero-filled by TMA and clipped at the store.
 #include <cuda_runtime.h>
-
-#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace trinv {
 
-// Shared-memory layout variants (template parameter LAY):
-//   LAY 0: A = one 16-wide box per stage with 128-byte swizzle, B = BN/8 boxes of 8 columns
-//   LAY 1: A = BK/4 boxes of 4 columns, B = BN/4 boxes of 4 columns (half-warp conflict-free)
-//   LAY 2: A = BK/4 boxes of 4 columns, B = BN/8 boxes of 8 columns
-struct TileCoord {
+constexpr int BK = 16;
+
+// One output tile: where its operands come from, its K-range and its epilogue.
+struct TileJob {
   int64_t a_row, a_col;  // A-operand: rows a_row.., columns a_col + k
   int64_t b_row, b_col;  // B-operand: rows b_row + k, columns b_col..
-  int64_t o_row, o_col;  // output tile origin
-  int64_t m_row, m_col;  // mirror tile origin (rows BN x cols BM), if any
+  int32_t ga, gb;        // 3rd TMA coordinate (batch) of A / B (3-D maps only)
   int64_t k_begin, k_end;
-  bool valid, mirror;
+  double* out;           // output tile origin
+  int64_t ldo, out_rows, out_cols;  // leading dimension, rows / columns left from the origin
+  double alpha, beta;
+  double* mir;           // mirror tile origin to zero-fill (BN rows x BM columns), or NULL
+  int64_t ldm, mir_rows, mir_cols;
+  bool valid;
 };
 
-template <int BM, int BN, int BK>
-__device__ __forceinline__ TileCoord map_tile(const LevelArgs& p, int64_t t) {
-  TileCoord c{};
+template <int BM, int BN, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int kConsumerWarps = WM * WN;
+  static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
+  static_assert(BM % BK == 0 && BN % BK == 0, "BK must divide BM and BN");
+};
+
+// ---------------------------------------------------------------------------
+// Level tile mapping (grid order = longest K first, so the hardware block
+// scheduler approximates a longest-processing-time schedule).
+template <int BM, int BN>
+__device__ __forceinline__ TileJob level_job(const LevelArgs& p, int64_t t) {
+  TileJob j{};
   const int64_t b = p.b, n = p.n, merges = p.merges;
   const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
   int64_t g = 0, I = 0, J = 0;
-  c.valid = true;
-  c.mirror = false;
   switch (p.mode) {
-    case MODE_LOWER_1: {  // longest K first: J ascending
+    case MODE_LOWER_1: {  // J ascending
       J = t / (merges * TMmax);
       const int64_t rem = t % (merges * TMmax);
       g = rem / TMmax; I = rem % TMmax;
@@ -87,67 +104,98 @@ __device__ __forceinline__ TileCoord map_tile(const LevelArgs& p, int64_t t) {
   }
   const int64_t s = 2 * g * b;
   const int64_t r = (p.mode == MODE_UL) ? n : (n - s - b < b ? n - s - b : b);  // second half
+  int64_t o_row = 0, o_col = 0, m_row = 0, m_col = 0;
+  bool mirror = false;
+  j.valid = true;
   switch (p.mode) {
     case MODE_LOWER_1:
-      c.valid = I * BM < r;
-      c.a_row = s + b + I * BM; c.a_col = s;
-      c.b_row = s; c.b_col = s + J * BN;
-      c.o_row = g * b + I * BM; c.o_col = J * BN;
-      c.k_begin = J * BN; c.k_end = b;
+      j.valid = I * BM < r;
+      j.a_row = s + b + I * BM; j.a_col = s;
+      j.b_row = s; j.b_col = s + J * BN;
+      o_row = g * b + I * BM; o_col = J * BN;
+      j.k_begin = J * BN; j.k_end = b;
       break;
-    case MODE_LOWER_2: {
-      c.valid = I * BM < r;
-      c.a_row = s + b + I * BM; c.a_col = s + b;
-      c.b_row = g * b; c.b_col = J * BN;
-      c.o_row = s + b + I * BM; c.o_col = s + J * BN;
-      c.mirror = true; c.m_row = s + J * BN; c.m_col = s + b + I * BM;
-      c.k_begin = 0; c.k_end = (I + 1) * BM < r ? (I + 1) * BM : r;
-    } break;
+    case MODE_LOWER_2:
+      j.valid = I * BM < r;
+      j.a_row = s + b + I * BM; j.a_col = s + b;
+      j.b_row = g * b; j.b_col = J * BN;
+      o_row = s + b + I * BM; o_col = s + J * BN;
+      mirror = true; m_row = s + J * BN; m_col = s + b + I * BM;
+      j.k_begin = 0; j.k_end = (I + 1) * BM < r ? (I + 1) * BM : r;
+      break;
     case MODE_UPPER_1:
-      c.valid = J * BN < r;
-      c.a_row = s + I * BM; c.a_col = s;
-      c.b_row = s; c.b_col = s + b + J * BN;
-      c.o_row = g * b + I * BM; c.o_col = J * BN;
-      c.k_begin = I * BM; c.k_end = b;
+      j.valid = J * BN < r;
+      j.a_row = s + I * BM; j.a_col = s;
+      j.b_row = s; j.b_col = s + b + J * BN;
+      o_row = g * b + I * BM; o_col = J * BN;
+      j.k_begin = I * BM; j.k_end = b;
       break;
     case MODE_UPPER_2:
-      c.valid = J * BN < r;
-      c.a_row = g * b + I * BM; c.a_col = 0;
-      c.b_row = s + b; c.b_col = s + b + J * BN;
-      c.o_row = s + I * BM; c.o_col = s + b + J * BN;
-      c.mirror = true; c.m_row = s + b + J * BN; c.m_col = s + I * BM;
-      c.k_begin = 0; c.k_end = (J + 1) * BN < r ? (J + 1) * BN : r;
+      j.valid = J * BN < r;
+      j.a_row = g * b + I * BM; j.a_col = 0;
+      j.b_row = s + b; j.b_col = s + b + J * BN;
+      o_row = s + I * BM; o_col = s + b + J * BN;
+      mirror = true; m_row = s + b + J * BN; m_col = s + I * BM;
+      j.k_begin = 0; j.k_end = (J + 1) * BN < r ? (J + 1) * BN : r;
       break;
     default:
-      c.a_row = I * BM; c.a_col = 0;
-      c.b_row = 0; c.b_col = J * BN;
-      c.o_row = I * BM; c.o_col = J * BN;
-      c.k_begin = (I * BM > J * BN) ? I * BM : J * BN; c.k_end = n;
+      j.a_row = I * BM; j.a_col = 0;
+      j.b_row = 0; j.b_col = J * BN;
+      o_row = I * BM; o_col = J * BN;
+      j.k_begin = (I * BM > J * BN) ? I * BM : J * BN; j.k_end = n;
       break;
   }
-  return c;
+  j.ga = j.gb = 0;
+  j.out = p.out + o_row * p.ldo + o_col;
+  j.ldo = p.ldo; j.out_rows = p.out_rows - o_row; j.out_cols = p.out_cols - o_col;
+  j.alpha = p.alpha; j.beta = 0.0;
+  if (mirror) {
+    j.mir = p.mir + m_row * p.ldm + m_col;
+    j.ldm = p.ldm; j.mir_rows = n - m_row; j.mir_cols = n - m_col;
+  } else {
+    j.mir = nullptr;
+  }
+  return j;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int BK = 16, int LAY = 1>
-struct GemmCfg {
-  static constexpr int kConsumerWarps = WM * WN;
-  static constexpr int kThreads = (kConsumerWarps + 1) * 32;
-  static constexpr int WTM = BM / WM, WTN = BN / WN;
-  static constexpr int FM = WTM / 8, FN = WTN / 8;
-  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
-  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
-  static_assert(BM % BK == 0 && BN % BK == 0, "BK must divide BM and BN");
-};
+// General batched GEMM tile mapping: g outer, then I, J (K-range classes of a
+// triangular operand ordered longest first).
+template <int BM, int BN>
+__device__ __forceinline__ TileJob gemm_job(const GemmArgs& p, int64_t t) {
+  TileJob j{};
+  const int64_t TM = (p.M + BM - 1) / BM, TN = (p.N + BN - 1) / BN;
+  const int64_t per = TM * TN;
+  const int64_t g = t / per, rem = t % per;
+  int64_t I, J;
+  if (p.triA != TRI_NONE) {  // class = I (its K-range)
+    I = rem / TN; J = rem % TN;
+    if (p.triA == TRI_LOWER) I = TM - 1 - I;  // long K (large I) first
+  } else {
+    J = rem / TM; I = rem % TM;
+    if (p.triB == TRI_UPPER) J = TN - 1 - J;  // long K (large J) first
+  }
+  int64_t kb = 0, ke = p.K;
+  if (p.triA == TRI_LOWER) ke = ke < (I + 1) * BM ? ke : (I + 1) * BM;  // A[i][k] = 0 for k > i
+  if (p.triA == TRI_UPPER) kb = kb > I * BM ? kb : I * BM;              // A[i][k] = 0 for k < i
+  if (p.triB == TRI_LOWER) kb = kb > J * BN ? kb : J * BN;              // B[k][j] = 0 for k < j
+  if (p.triB == TRI_UPPER) ke = ke < (J + 1) * BN ? ke : (J + 1) * BN;  // B[k][j] = 0 for k > j
+  j.valid = true;
+  j.a_row = I * BM; j.a_col = 0;
+  j.b_row = 0; j.b_col = J * BN;
+  j.ga = (int32_t)g; j.gb = (int32_t)g;
+  j.k_begin = kb; j.k_end = ke > kb ? ke : kb;
+  j.out = p.C + g * p.sC + (I * BM) * p.ldc + J * BN;
+  j.ldo = p.ldc; j.out_rows = p.M - I * BM; j.out_cols = p.N - J * BN;
+  j.alpha = p.alpha; j.beta = p.beta;
+  j.mir = nullptr;
+  return j;
+}
 
-template <int BM, int BN, int WM, int WN, int STAGES, int BK, int LAY>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThreads, 1)
-    dmma_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                      const LevelArgs p) {
-  using C = GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>;
-  constexpr int BW = (LAY == 1) ? 4 : 8;  // B box width (columns)
-  extern __shared__ unsigned char smem_raw[];
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES, int RANK>
+__device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensorMap* mapB, const TileJob& tj,
+                                         unsigned char* smem_raw) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BK/4][BM][4]
@@ -155,10 +203,8 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThr
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
-  const TileCoord tc = map_tile<BM, BN, BK>(p, blockIdx.x);
-  if (!tc.valid) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nk = (tc.k_end - tc.k_begin + BK - 1) / BK;
+  const int64_t nk = (tj.k_end - tj.k_begin + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -172,44 +218,46 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThr
   if (warp == C::kConsumerWarps) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      tma_prefetch_desc(&mapA);
-      tma_prefetch_desc(&mapB);
+      tma_prefetch_desc(mapA);
+      tma_prefetch_desc(mapB);
       for (int64_t kt = 0; kt < nk; ++kt) {
         const int s = (int)(kt % STAGES);
         const int64_t use = kt / STAGES;
         if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        const int64_t k = tc.k_begin + kt * BK;
+        const int64_t k = tj.k_begin + kt * BK;
         double* sa = sA + (size_t)s * BM * BK;
-        if (LAY == 0) {
 #pragma unroll
-          for (int kb = 0; kb < BK / 16; ++kb)
-            tma_load_2d(sa + kb * BM * 16, &mapA, (int32_t)(tc.a_col + k + 16 * kb), (int32_t)tc.a_row, &full[s]);
-        } else {
-#pragma unroll
-          for (int kb = 0; kb < BK / 4; ++kb)
-            tma_load_2d(sa + kb * BM * 4, &mapA, (int32_t)(tc.a_col + k + 4 * kb), (int32_t)tc.a_row, &full[s]);
+        for (int kb = 0; kb < BK / 4; ++kb) {
+          if (RANK == 2)
+            tma_load_2d(sa + kb * BM * 4, mapA, (int32_t)(tj.a_col + k + 4 * kb), (int32_t)tj.a_row, &full[s]);
+          else
+            tma_load_3d(sa + kb * BM * 4, mapA, (int32_t)(tj.a_col + k + 4 * kb), (int32_t)tj.a_row, tj.ga,
+                        &full[s]);
         }
         double* sb = sB + (size_t)s * BK * BN;
 #pragma unroll
-        for (int nb = 0; nb < BN / BW; ++nb)
-          tma_load_2d(sb + nb * BK * BW, &mapB, (int32_t)(tc.b_col + nb * BW), (int32_t)(tc.b_row + k), &full[s]);
+        for (int nb = 0; nb < BN / 4; ++nb) {
+          if (RANK == 2)
+            tma_load_2d(sb + nb * BK * 4, mapB, (int32_t)(tj.b_col + nb * 4), (int32_t)(tj.b_row + k), &full[s]);
+          else
+            tma_load_3d(sb + nb * BK * 4, mapB, (int32_t)(tj.b_col + nb * 4), (int32_t)(tj.b_row + k), tj.gb,
+                        &full[s]);
+        }
       }
     }
     return;
   }
 
   // ---------------- consumers ----------------
-  // Mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle.
-  if (tc.mirror) {
-    const int ctid = threadIdx.x;
+  if (tj.mir) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
     constexpr int PAIRS = BM / 2;
-    for (int e = ctid; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
-      const int64_t row = tc.m_row + e / PAIRS, col = tc.m_col + 2 * (e % PAIRS);
-      if (row < p.n) {
-        double* q = p.mir + row * p.ldm + col;
-        if (col + 1 < p.n) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
-        else if (col < p.n) *q = 0.0;
+    for (int e = threadIdx.x; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
+      const int64_t row = e / PAIRS, col = 2 * (e % PAIRS);
+      if (row < tj.mir_rows) {
+        double* q = tj.mir + row * tj.ldm + col;
+        if (col + 1 < tj.mir_cols) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
+        else if (col < tj.mir_cols) *q = 0.0;
       }
     }
   }
@@ -222,31 +270,21 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThr
     for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int lr = lane >> 2, lc = lane & 3;
-  // per-lane fragment offsets (doubles); A[row][k], B[k][col] with k = kk*4 + lc
-  const int a_base = (wm * C::WTM + lr) * 4 + lc;                    // LAY 1/2: box k/4 of [BM][4]
-  const int b_col = wn * C::WTN + lr;                                  // + ni*8
-  const int b_base = (b_col / BW) * BK * BW + lc * BW + (b_col % BW);  // box col/BW of [BK][BW]
+  // per-lane fragment offsets (doubles): A[row][k] in box k/4 of [BM][4]; B[k][col] in box col/4 of [BK][4]
+  const int a_base = (wm * C::WTM + lr) * 4 + lc;
+  const int b_base = ((wn * C::WTN + lr) >> 2) * BK * 4 + lc * 4 + (lr & 3);
   for (int64_t kt = 0; kt < nk; ++kt) {
     const int s = (int)(kt % STAGES);
     mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
-    const double* a_st = sA + (size_t)s * BM * BK;
+    const double* a_st = sA + (size_t)s * BM * BK + a_base;
     const double* b_st = sB + (size_t)s * BK * BN + b_base;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double af[C::FM], bf[C::FN];
 #pragma unroll
-      for (int mi = 0; mi < C::FM; ++mi) {
-        if (LAY == 0) {  // 16-wide boxes with 128-byte swizzle: chunk (k/2) ^ (row % 8)
-          const int row = wm * C::WTM + mi * 8 + lr;
-          const int kc = (kk & 3) * 4 + lc;
-          const int off = (kk >> 2) * BM * 16 + row * 16 + ((((kc >> 1) ^ (row & 7)) << 1) | (kc & 1));
-          af[mi] = a_st[off];
-        } else {
-          af[mi] = a_st[a_base + kk * BM * 4 + mi * 32];
-        }
-      }
+      for (int mi = 0; mi < C::FM; ++mi) af[mi] = a_st[kk * BM * 4 + mi * 32];
 #pragma unroll
-      for (int ni = 0; ni < C::FN; ++ni) bf[ni] = b_st[kk * 4 * BW + (ni * 8 / BW) * BK * BW];
+      for (int ni = 0; ni < C::FN; ++ni) bf[ni] = b_st[kk * 16 + ni * 2 * BK * 4];
 #pragma unroll
       for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
@@ -256,30 +294,66 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>::kThr
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---------------- epilogue: alpha * acc -> out (clipped) ----------------
+  // ---------------- epilogue: out = alpha * acc (+ beta * out), clipped ----------------
+  // 16-byte stores need an even leading dimension and an aligned tile origin
+  const bool vec = ((reinterpret_cast<uintptr_t>(tj.out) & 15u) == 0) && (tj.ldo % 2 == 0);
 #pragma unroll
   for (int mi = 0; mi < C::FM; ++mi) {
-    const int64_t row = tc.o_row + wm * C::WTM + mi * 8 + lr;
-    if (row >= p.out_rows) continue;
-    double* orow = p.out + row * p.ldo;
+    const int64_t row = wm * C::WTM + mi * 8 + lr;
+    if (row >= tj.out_rows) continue;
+    double* orow = tj.out + row * tj.ldo;
 #pragma unroll
     for (int ni = 0; ni < C::FN; ++ni) {
-      const int64_t col = tc.o_col + wn * C::WTN + ni * 8 + 2 * lc;
-      const double v0 = p.alpha * acc[mi][ni][0], v1 = p.alpha * acc[mi][ni][1];
-      if (col + 1 < p.out_cols) *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
-      else if (col < p.out_cols) orow[col] = v0;
+      const int64_t col = wn * C::WTN + ni * 8 + 2 * lc;
+      double v0 = tj.alpha * acc[mi][ni][0], v1 = tj.alpha * acc[mi][ni][1];
+      if (col + 1 < tj.out_cols && !vec) {
+        if (tj.beta != 0.0) {
+          v0 = fma(tj.beta, orow[col], v0);
+          v1 = fma(tj.beta, orow[col + 1], v1);
+        }
+        orow[col] = v0;
+        orow[col + 1] = v1;
+      } else if (col + 1 < tj.out_cols) {
+        if (tj.beta != 0.0) {
+          const double2 o = *reinterpret_cast<const double2*>(orow + col);
+          v0 = fma(tj.beta, o.x, v0);
+          v1 = fma(tj.beta, o.y, v1);
+        }
+        *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
+      } else if (col < tj.out_cols) {
+        if (tj.beta != 0.0) v0 = fma(tj.beta, orow[col], v0);
+        orow[col] = v0;
+      }
     }
   }
 }
 
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+    dmma_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      const LevelArgs p) {
+  extern __shared__ unsigned char smem_raw[];
+  const TileJob tj = level_job<BM, BN>(p, blockIdx.x);
+  if (!tj.valid) return;
+  run_tile<BM, BN, WM, WN, STAGES, 2>(&mapA, &mapB, tj, smem_raw);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+    dmma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                     const GemmArgs p) {
+  extern __shared__ unsigned char smem_raw[];
+  const TileJob tj = gemm_job<BM, BN>(p, blockIdx.x);
+  run_tile<BM, BN, WM, WN, STAGES, 3>(&mapA, &mapB, tj, smem_raw);
+}
+
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int WM, int WN, int STAGES, int BK = 16, int LAY = 1>
-static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
-  using C = GemmCfg<BM, BN, WM, WN, STAGES, BK, LAY>;
-  constexpr int BW = (LAY == 1) ? 4 : 8;
+template <int BM, int BN, int WM, int WN, int STAGES>
+static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
   CUtensorMap mA, mB;
-  if (!encode_map(&mA, a.opA, LAY == 0 ? 16 : 4, BM, LAY == 0)) return cudaErrorInvalidValue;
-  if (!encode_map(&mB, a.opB, BW, BK, false)) return cudaErrorInvalidValue;
+  if (!encode_map(&mA, a.opA, 4, BM, false)) return cudaErrorInvalidValue;
+  if (!encode_map(&mB, a.opB, 4, BK, false)) return cudaErrorInvalidValue;
   int64_t tiles;
   if (a.mode == MODE_UL) {
     const int64_t T = (a.n + BM - 1) / BM;
@@ -289,7 +363,7 @@ static cudaError_t launch_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launc
   }
   if (tiles <= 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES, BK, LAY>;
+  constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
   set_smem_once<k>((int)C::SMEM);
   k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
   if (launches) ++*launches;
@@ -315,37 +389,70 @@ static double level_flops(const LevelArgs& a) {
   return f;
 }
 
+// Tile size: the largest of 128 / 64 / 32 (not above `cap`) giving at least two
+// CTAs per SM; mid-size problems otherwise leave SMs idle behind a few long
+// tiles (profiles/r01_sweep_n.txt).
+template <typename F>
+static int64_t pick_tile(F tiles, int64_t cap) {
+  const int sms = device_sms();
+  for (int64_t T : {128, 64}) {
+    if (T <= cap && tiles(T) >= 2 * sms) return T;
+  }
+  return cap < 32 ? cap : 32;
+}
+
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
   ProfileScope prof(KIND_DMMA, level_flops(a), 0.0, s);
-  // Tile size per level: the largest of 128 / 64 / 32 (not above b) that still
-  // gives at least two CTAs per SM; mid-size levels otherwise leave SMs idle
-  // behind a few long triangular tiles (profiles/r01_sweep_n.txt).
-  const int sms = device_sms();
   auto tiles = [&](int64_t T) {
     if (a.mode == MODE_UL) { const int64_t m = (a.n + T - 1) / T; return m * m; }
     const int64_t m = (a.b + T - 1) / T;
     return a.merges * m * m;
   };
-  int64_t t = 32;
-  for (int64_t T : {128, 64}) {
-    if ((a.mode == MODE_UL || T <= a.b) && tiles(T) >= 2 * sms) { t = T; break; }
-  }
-  if (a.mode != MODE_UL && t > a.b) t = a.b;
-  if (t >= 128) {
-    static const int variant = [] {
-      const char* e = getenv("TRINV_GEMM_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
-    // LAY 1 measured best on B200 (config 3: 93.8% vs 92.7% for the swizzled LAY 0,
-    // profiles/r01_gemm_variants.txt); the others stay selectable for tuning.
-    switch (variant) {
-      case 2: return launch_cfg<128, 128, 2, 4, 5, 16, 0>(a, s, launches);
-      case 3: return launch_cfg<128, 128, 2, 4, 5, 16, 2>(a, s, launches);
-      default: return launch_cfg<128, 128, 2, 4, 5, 16, 1>(a, s, launches);
-    }
-  }
-  if (t >= 64) return launch_cfg<64, 64, 2, 2, 4>(a, s, launches);
-  return launch_cfg<32, 32, 2, 2, 4>(a, s, launches);
+  const int64_t t = pick_tile(tiles, a.mode == MODE_UL ? 128 : a.b);
+  if (t >= 128) return launch_level_cfg<128, 128, 2, 4, 5>(a, s, launches);
+  if (t >= 64) return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches);
+  return launch_level_cfg<32, 32, 2, 2, 4>(a, s, launches);
+}
+
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES>
+static cudaError_t launch_gemm_cfg(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  CUtensorMap mA, mB;
+  const uint64_t dA[3] = {(uint64_t)a.K, (uint64_t)a.M, (uint64_t)a.batch};
+  const uint64_t sAb[2] = {(uint64_t)a.lda * 8, (uint64_t)(a.batch > 1 ? a.sA : a.M * a.lda) * 8};
+  const uint32_t bA[3] = {4, (uint32_t)BM, 1};
+  const uint64_t dB[3] = {(uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.batch};
+  const uint64_t sBb[2] = {(uint64_t)a.ldb * 8, (uint64_t)(a.batch > 1 ? a.sB : a.K * a.ldb) * 8};
+  const uint32_t bB[3] = {4, (uint32_t)BK, 1};
+  if (!encode_map_nd(&mA, a.A, 3, dA, sAb, bA)) return cudaErrorInvalidValue;
+  if (!encode_map_nd(&mB, a.B, 3, dB, sBb, bB)) return cudaErrorInvalidValue;
+  const int64_t tiles = a.batch * ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  if (tiles <= 0) return cudaSuccess;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  constexpr auto k = dmma_gemm_kernel<BM, BN, WM, WN, STAGES>;
+  set_smem_once<k>((int)C::SMEM);
+  k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+double gemm_flops(const GemmArgs& a) {
+  // dense 2MNK, or the triangular-aware count when one operand is triangular
+  const double M = (double)a.M, N = (double)a.N, K = (double)a.K;
+  if (a.triA == TRI_NONE && a.triB == TRI_NONE) return 2.0 * M * N * K * a.batch;
+  if (a.triA != TRI_NONE) return a.batch * N * M * (M + 1);  // M == K
+  return a.batch * M * N * (N + 1);                          // N == K
+}
+
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.M <= 0 || a.N <= 0 || a.batch <= 0) return cudaSuccess;
+  ProfileScope prof(KIND_DMMA, gemm_flops(a), 0.0, s);
+  auto tiles = [&](int64_t T) { return a.batch * ((a.M + T - 1) / T) * ((a.N + T - 1) / T); };
+  const int64_t t = pick_tile(tiles, 128);
+  if (t >= 128) return launch_gemm_cfg<128, 128, 2, 4, 5>(a, s, launches);
+  if (t >= 64) return launch_gemm_cfg<64, 64, 2, 2, 4>(a, s, launches);
+  return launch_gemm_cfg<32, 32, 2, 2, 4>(a, s, launches);
 }
 
 }  // namespace trinv

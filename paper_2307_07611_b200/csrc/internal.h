@@ -81,6 +81,32 @@ struct LevelArgs {
 };
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
 
+// General batched GEMM on the same engine: for g < batch,
+//   C_g = alpha * A_g B_g + beta * C_g,  A_g: M x K (lda, stride sA), B_g: K x N (ldb, sB), C_g: M x N (ldc, sC),
+// row-major.  triA / triB declare a triangular operand whose structurally zero
+// blocks are skipped (A lower: A[i][k] = 0 for k > i; A upper: k < i; B lower:
+// B[k][j] = 0 for k < j; B upper: k > j); its diagonal tiles must hold explicit
+// zeros in the other triangle.  A, B 16-byte aligned with even ld / stride.
+// C must not overlap A or B.
+enum TriKind : int { TRI_NONE = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
+struct GemmArgs {
+  int64_t M, N, K, batch;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+  double alpha, beta;
+  int triA, triB;
+};
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
+
+// ---- Crout factorisation of a diagonal block of order <= 64 (lu.cu) ----------
+cudaError_t launch_lu_leaf(double* A, int64_t lda, int n, int32_t* info, int64_t info_off, cudaStream_t s,
+                           int64_t* launches);
+double gemm_flops(const GemmArgs& a);
+
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.
 bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, bool swizzle128);

@@ -236,6 +236,99 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   return TRINV_OK;
 }
 
+
+// ---- blocked Crout LU (NEXT row f2) -----------------------------------------------
+// Split point of the factor recursion: a multiple of 64 near n/2.
+static int64_t lu_split(int64_t n) { return 64 * ((n + 127) / 128); }
+
+// Scratch of lu_rec at order n: L11^{-1}, U11^{-1} (h x even(h)), their triangular
+// workspace, and one off-diagonal product buffer (h x even(n-h) or (n-h) x even(h)).
+static size_t lu_scratch(int64_t n) {
+  if (n <= 64) return 0;
+  const int64_t h = lu_split(n), r = n - h;
+  size_t b = 2 * align_up(mat_bytes(h)) + align_up(tri_ws(h, nullptr, even_up(h), nullptr, even_up(h)));
+  b += align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
+  return std::max(b, lu_scratch(r));
+}
+
+static trinv_status_t lu_rec(int64_t n, double* A, int64_t lda, char* ws, int32_t* info, int64_t info_off,
+                             cudaStream_t s) {
+  if (n <= 64) return cuda_fail(launch_lu_leaf(A, lda, (int)n, info, info_off, s, &g_launches));
+  const int64_t h = lu_split(n), r = n - h, ldh = even_up(h);
+  double* A12 = A + h;
+  double* A21 = A + h * lda;
+  double* A22 = A21 + h;
+  trinv_status_t st = lu_rec(h, A, lda, ws, info, info_off, s);  // A11 = L11 U11
+  if (st != TRINV_OK) return st;
+  char* p = ws;
+  double* Li = reinterpret_cast<double*>(p); p += align_up(mat_bytes(h));
+  double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(h));
+  double* tws = reinterpret_cast<double*>(p); p += align_up(tri_ws(h, nullptr, ldh, nullptr, ldh));
+  double* T = reinterpret_cast<double*>(p);
+  // L11^{-1} (lower, diagonal kept) and U11^{-1} (unit upper) by the recursive split
+  st = run_tri('L', h, A, lda, Li, ldh, 0, tws, nullptr, 0, s);
+  if (st != TRINV_OK) return st;
+  st = run_tri('U', h, A, lda, Ui, ldh, 1, tws, nullptr, 0, s);
+  if (st != TRINV_OK) return st;
+  // U12 = L11^{-1} A12  (h x r; L11^{-1} lower: K-range k <= row)
+  const int64_t ldr = even_up(r);
+  GemmArgs g{};
+  g.M = h; g.N = r; g.K = h; g.batch = 1;
+  g.A = Li; g.lda = ldh; g.B = A12; g.ldb = lda; g.C = T; g.ldc = ldr;
+  g.alpha = 1.0; g.beta = 0.0; g.triA = TRI_LOWER; g.triB = TRI_NONE;
+  TRY(launch_gemm(g, s, &g_launches));
+  TRY(cudaMemcpy2DAsync(A12, lda * 8, T, ldr * 8, r * 8, h, cudaMemcpyDeviceToDevice, s));
+  // L21 = A21 U11^{-1}  (r x h; U11^{-1} upper: K-range k <= column)
+  GemmArgs g2{};
+  g2.M = r; g2.N = h; g2.K = h; g2.batch = 1;
+  g2.A = A21; g2.lda = lda; g2.B = Ui; g2.ldb = ldh; g2.C = T; g2.ldc = ldh;
+  g2.alpha = 1.0; g2.beta = 0.0; g2.triA = TRI_NONE; g2.triB = TRI_UPPER;
+  TRY(launch_gemm(g2, s, &g_launches));
+  TRY(cudaMemcpy2DAsync(A21, lda * 8, T, ldh * 8, h * 8, r, cudaMemcpyDeviceToDevice, s));
+  // Schur complement A22 <- A22 - L21 U12
+  GemmArgs g3{};
+  g3.M = r; g3.N = r; g3.K = h; g3.batch = 1;
+  g3.A = A21; g3.lda = lda; g3.B = A12; g3.ldb = lda; g3.C = A22; g3.ldc = lda;
+  g3.alpha = -1.0; g3.beta = 1.0; g3.triA = TRI_NONE; g3.triB = TRI_NONE;
+  TRY(launch_gemm(g3, s, &g_launches));
+  return lu_rec(r, A22, lda, ws, info, info_off + h, s);
+}
+static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu,
+                                       double* X, int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU, void* ws,
+                                       size_t ws_bytes, int32_t* d_info, bool init_info, cudaStream_t s) {
+  if (n < 0) return TRINV_INVALID_ARG;
+  if ((diagL != TRINV_UNIT && diagL != TRINV_NON_UNIT) || (diagU != TRINV_UNIT && diagU != TRINV_NON_UNIT))
+    return TRINV_INVALID_ARG;
+  if (n == 0) return TRINV_OK;
+  if (!Lf || !Uf || !X || ldl < n || ldu < n || ldx < n) return TRINV_INVALID_ARG;
+  if (overlap(Lf, ldl, X, ldx, n) || overlap(Uf, ldu, X, ldx, n)) return TRINV_ALIASING;
+  const int64_t lde = even_up(n);
+  const size_t tws_bytes = std::max(tri_ws(n, Lf, ldl, nullptr, lde), tri_ws(n, Uf, ldu, nullptr, lde));
+  const bool stage_x = !tma_ok(X, ldx);
+  const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0);
+  if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
+  char* p = static_cast<char*>(ws);
+  double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
+  double* Li = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
+  void* tws = p; p += align_up(tws_bytes);
+  if (init_info && d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
+  // zero diagonals: L reports 1+i, U reports n+1+i (header); the min is kept
+  trinv_status_t st = tri_entry('L', n, Lf, ldl, Li, lde, (int)diagL, tws, tws_bytes, d_info, 0, false, s);
+  if (st != TRINV_OK) return st;
+  st = tri_entry('U', n, Uf, ldu, Ui, lde, (int)diagU, tws, tws_bytes, d_info, n, false, s);
+  if (st != TRINV_OK) return st;
+  double* Xuse = X;
+  int64_t ldx_use = ldx;
+  if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; }
+  LevelArgs ul{};
+  ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
+  ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
+  ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
+  TRY(launch_level(ul, s, &g_launches));
+  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  return TRINV_OK;
+}
+
 }  // namespace trinv
 
 using namespace trinv;
@@ -245,6 +338,14 @@ extern "C" {
 size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= 0) return 0;
   if (op == 'L' || op == 'U') return tri_ws(n, A, lda, X, ldx);
+  if (op == 'F') return align_up(lu_scratch(n));
+  if (op == 'A') {  // inv_general: packed LU copy + max(LU scratch, inv_from_lu workspace) + X staging
+    const size_t g = 2 * align_up(mat_bytes(n)) + align_up(tri_ws(n, nullptr, even_up(n), nullptr, even_up(n)));
+    size_t bytes = align_up(mat_bytes(n)) + std::max(align_up(lu_scratch(n)), g);
+    if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
+    (void)A; (void)lda;
+    return bytes;
+  }
   if (op == 'G') {
     // [U^{-1} | L^{-1} | triangular scratch (+ factor staging) | X staging]; the
     // U factor is assumed to be laid out like the L factor (A, lda).
@@ -350,38 +451,67 @@ trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const dou
 trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu, double* X,
                            int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU, void* ws, size_t ws_bytes,
                            int32_t* d_info, void* stream) {
+  return inv_from_lu_core(n, Lf, ldl, Uf, ldu, X, ldx, diagL, diagU, ws, ws_bytes, d_info, true,
+                          (cudaStream_t)stream);
+}
+
+trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,
+                          int64_t lda, int64_t strideA, char structA, const double* B, int64_t ldb, int64_t strideB,
+                          char structB, double beta, double* C, int64_t ldc, int64_t strideC, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || batch < 0) return TRINV_INVALID_ARG;
+  if (M == 0 || N == 0 || batch == 0) return TRINV_OK;
+  if (K == 0) return TRINV_NOT_SUPPORTED;
+  auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
+  const int ta = tri(structA), tb = tri(structB);
+  if (ta < 0 || tb < 0 || (ta != TRI_NONE && tb != TRI_NONE)) return TRINV_INVALID_ARG;
+  if ((ta != TRI_NONE && M != K) || (tb != TRI_NONE && N != K)) return TRINV_INVALID_ARG;
+  if (!C || (K > 0 && (!A || !B)) || ldc < N || (K > 0 && (lda < K || ldb < N))) return TRINV_INVALID_ARG;
+  if (batch > 1 && (strideA < M * lda || strideB < K * ldb || strideC < M * ldc)) return TRINV_INVALID_ARG;
+  // a single-row operand never uses its leading dimension: any even value is equivalent
+  if (M == 1) lda = even_up(lda);
+  if (K == 1) ldb = even_up(ldb);
+  if (!tma_ok(A, lda) || !tma_ok(B, ldb) || (batch > 1 && (strideA % 2 || strideB % 2)))
+    return TRINV_NOT_SUPPORTED;
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A = A; g.lda = lda; g.sA = strideA; g.B = B; g.ldb = ldb; g.sB = strideB;
+  g.C = C; g.ldc = ldc; g.sC = strideC; g.alpha = alpha; g.beta = beta; g.triA = ta; g.triB = tb;
+  return cuda_fail(launch_gemm(g, (cudaStream_t)stream, &g_launches));
+}
+
+trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_bytes, int32_t* d_info,
+                        void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (n < 0) return TRINV_INVALID_ARG;
-  if ((diagL != TRINV_UNIT && diagL != TRINV_NON_UNIT) || (diagU != TRINV_UNIT && diagU != TRINV_NON_UNIT))
-    return TRINV_INVALID_ARG;
   if (n == 0) return TRINV_OK;
-  if (!Lf || !Uf || !X || ldl < n || ldu < n || ldx < n) return TRINV_INVALID_ARG;
-  if (overlap(Lf, ldl, X, ldx, n) || overlap(Uf, ldu, X, ldx, n)) return TRINV_ALIASING;
-  const int64_t lde = even_up(n);
-  const size_t tws_bytes = std::max(tri_ws(n, Lf, ldl, nullptr, lde), tri_ws(n, Uf, ldu, nullptr, lde));
-  const bool stage_x = !tma_ok(X, ldx);
-  const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0);
-  if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
-  char* p = static_cast<char*>(ws);
-  double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
-  double* Li = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
-  void* tws = p; p += align_up(tws_bytes);
+  if (!A || lda < n) return TRINV_INVALID_ARG;
+  if (n > 64 && !tma_ok(A, lda)) return TRINV_NOT_SUPPORTED;
+  const size_t need = align_up(lu_scratch(n));
+  if (ws_bytes < need || (need > 0 && !ws)) return TRINV_WORKSPACE_TOO_SMALL;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
-  // zero diagonals: L reports 1+i, U reports n+1+i (header); the min is kept
-  trinv_status_t st = tri_entry('L', n, Lf, ldl, Li, lde, (int)diagL, tws, tws_bytes, d_info, 0, false, s);
+  return lu_rec(n, A, lda, static_cast<char*>(ws), d_info, 0, s);
+}
+
+trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx, void* ws,
+                           size_t ws_bytes, int32_t* d_info, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n < 0) return TRINV_INVALID_ARG;
+  if (n == 0) return TRINV_OK;
+  if (!A || !X || lda < n || ldx < n) return TRINV_INVALID_ARG;
+  if (overlap(A, lda, X, ldx, n)) return TRINV_ALIASING;
+  const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
+  if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
+  const int64_t lde = even_up(n);
+  char* p = static_cast<char*>(ws);
+  double* LU = reinterpret_cast<double*>(p);
+  p += align_up(mat_bytes(n));
+  if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
+  TRY(cudaMemcpy2DAsync(LU, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  trinv_status_t st = lu_rec(n, LU, lde, p, d_info, 0, s);  // A = L U, U unit (Crout)
   if (st != TRINV_OK) return st;
-  st = tri_entry('U', n, Uf, ldu, Ui, lde, (int)diagU, tws, tws_bytes, d_info, n, false, s);
-  if (st != TRINV_OK) return st;
-  double* Xuse = X;
-  int64_t ldx_use = ldx;
-  if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; }
-  LevelArgs ul{};
-  ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
-  ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
-  ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
-  TRY(launch_level(ul, s, &g_launches));
-  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
-  return TRINV_OK;
+  // A^{-1} = U^{-1} L^{-1} from the packed factors (the scratch is reused, stream-ordered)
+  return inv_from_lu_core(n, LU, lde, LU, lde, X, ldx, TRINV_NON_UNIT, TRINV_UNIT, p,
+                          ws_bytes - align_up(mat_bytes(n)), d_info, false, s);
 }
 
 const char* trinv_status_string(trinv_status_t st) {

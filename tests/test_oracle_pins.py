@@ -285,3 +285,52 @@ def test_metrics():
     T = np.array([[2.0, 0.0], [1.0, 4.0]])
     Xc = oracle.columns(T, "L", [1])
     assert oracle.column_residual_ratio(T, Xc, [1]) == 0.0
+
+
+# --- NEXT row f2: SKUL (Alg. 5) ------------------------------------------
+def test_skul_paper_5x5_printed(golden):
+    g = golden("paper_5x5_factors.txt")
+    L, U, S, K, info = oracle.skul(g["A"])
+    assert info == 0
+    for got, ref in ((L, g["L_skul"]), (U, g["U_skul"]), (S, g["S_skul"]), (K, g["K_skul"])):
+        assert np.max(np.abs(got - ref)) <= 1e-4  # 4 printed decimals
+    assert np.max(np.abs(oracle.inv_general(g["A"]) - np.linalg.inv(g["A"]))) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 40, 150])
+def test_skul_identities(n):
+    Lg = synth.host(n, seed=n, tag="L", diag="pos")
+    Ug = synth.host(n, seed=n, tag="U", uplo="U", diag="one")
+    A = Lg @ Ug
+    L, U, S, K, info = oracle.skul(A)
+    assert info == 0
+    assert np.allclose(L @ U, A, rtol=0, atol=1e-14)                # A = L U
+    assert oracle.floored_rel_err(L, Lg) <= 1e-12                   # unique Crout factors
+    assert oracle.floored_rel_err(np.triu(U, 1), np.triu(Ug, 1)) <= 1e-11
+    assert np.all(np.diag(U) == 1.0)
+    assert oracle.floored_rel_err(S, oracle.crit_upper(U, unit=True)) <= 1e-13  # S = U^-1
+    assert oracle.floored_rel_err(K, oracle.crit_lower(L)) <= 1e-13             # K = L^-1
+    assert oracle.residual_ratio(A, S @ K) <= 1e-15
+
+
+def test_skul_integer_exact():
+    # unit-diagonal integer L and U: every intermediate is an integer (Cor. 2), exact
+    rng = np.random.default_rng(3)
+    n = 12
+    L = np.tril(rng.integers(-2, 3, size=(n, n)), -1).astype(float) + np.eye(n)
+    U = np.triu(rng.integers(-2, 3, size=(n, n)), 1).astype(float) + np.eye(n)
+    A = L @ U
+    L2, U2, S, K, info = oracle.skul(A)
+    assert info == 0 and np.array_equal(L2, L) and np.array_equal(U2, U)
+    X = S @ K
+    assert np.array_equal(X, np.round(X))
+    Ai = [[int(v) for v in r] for r in A]
+    Xi = [[int(v) for v in r] for r in X]
+    for i in range(n):
+        for j in range(n):
+            assert sum(Ai[i][k] * Xi[k][j] for k in range(n)) == (i == j)
+
+
+def test_skul_zero_pivot():
+    A = np.array([[0.0, 1.0], [1.0, 0.0]])
+    assert oracle.skul(A)[4] == 1

@@ -42,6 +42,8 @@ CONFIGS = {
     2: dict(workload="config2: single fp64 lower n=8192, 32-wide leaves", kind="L", n=8192, diag="signed"),
     3: dict(workload="config3: single fp64 upper n=32768", kind="U", n=32768, diag="pos"),
     4: dict(workload="config4: inv_from_lu n=16384, L unit", kind="G", n=16384),
+    5: dict(workload="NEXT f2: general fp64 inverse from A, n=16384 (A = L U with U unit; Crout LU without "
+                     "pivoting + U^-1 L^-1), 2n^3 flops", kind="A", n=16384),
 }
 
 
@@ -148,6 +150,13 @@ def run_reference(args):
         def step():
             oracle.crit_batched(A)
         unit, work, what = "inverses/s", sample, f"all {sample} config-1 matrices per step, OpenMP over matrices"
+    elif cfg["kind"] == "A":
+        m = 1024
+        Lg = synth.host(m, seed=5, tag="L", diag="pos"); Ug = synth.host(m, seed=5, tag="U", uplo="U", diag="one")
+        Am = Lg @ Ug
+        def step():
+            oracle.inv_general(Am)
+        unit, work, what = "GFLOP/s", 2 * m ** 3 / 1e9, f"SKUL + S K at n={m} per step (n={cfg['n']} takes hours)"
     else:
         n = cfg["n"]
         cols = np.arange(0, n, max(1, n // 64))[:64]
@@ -202,6 +211,14 @@ def cpu_baseline(cfg):
         return {"value": sample / dt, "unit": "inverses/s", "cores": cores, "kind": "oracle",
                 "sample": f"{sample} of the 131072 config-1 matrices x {reps} reps, OpenMP over matrices"}
     n = cfg["n"]
+    if cfg["kind"] == "A":  # SKUL oracle (O(n^3)) on a smaller order, GFLOP/s at 2n^3
+        m = 1024
+        Lg = synth.host(m, seed=5, tag="L", diag="pos"); Ug = synth.host(m, seed=5, tag="U", uplo="U", diag="one")
+        A = Lg @ Ug
+        t0 = time.perf_counter(); oracle.inv_general(A)
+        dt = time.perf_counter() - t0
+        return {"value": 2 * m ** 3 / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                "sample": f"SKUL + S K at n={m} (the n={n} workload would take hours on the host)"}
     if n <= 2048:
         T = synth.host(n, uplo="L" if cfg["kind"] != "U" else "U", diag=cfg.get("diag", "signed"))
         t0 = time.perf_counter(); oracle.trinv(T, "L" if cfg["kind"] != "U" else "U")
@@ -288,7 +305,18 @@ def main():
         algo_bytes_per_launch = B * (n * (n + 1) / 2 + n * n) * 8  # triangle in + full matrix out
         flops_per_step = B * n ** 3 / 3
     else:
-        if cfg["kind"] == "G":
+        if cfg["kind"] == "A":
+            Lg = torch.empty((n, n), dtype=torch.float64, device=dev)
+            Ug = torch.empty_like(Lg)
+            synth.device_fill(Lg, n, seed=5, tag="L", diag="pos")
+            synth.device_fill(Ug, n, seed=5, tag="U", uplo="U", diag="one")
+            A = Lg @ Ug  # input construction (library DGEMM), outside the timed region
+            del Lg, Ug
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            def step():
+                P.inv_general(A, out=X)
+            flops_per_step = 2 * n ** 3
+        elif cfg["kind"] == "G":
             Lm = torch.empty((n, n), dtype=torch.float64, device=dev)
             Um = torch.empty((n, n), dtype=torch.float64, device=dev)
             synth.device_fill(Lm, n, tag="L", diag="one")
@@ -432,7 +460,7 @@ def main():
         del h_in, h_out, ws
     elif cfg["kind"] != "B":
         # host buffers: H2D of the input factor(s), the call, D2H of the inverse
-        ins = [Lm, Um] if cfg["kind"] == "G" else [A]
+        ins = [Lm, Um] if cfg["kind"] == "G" else [A]  # config 5: A
         h_ins = [t.cpu().pin_memory() for t in ins]
         h_out = torch.empty((n, n), dtype=torch.float64).pin_memory()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

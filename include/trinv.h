@@ -167,6 +167,19 @@ trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double
                           int64_t lda, int64_t strideA, char structA, const double* B, int64_t ldb, int64_t strideB,
                           char structB, double beta, double* C, int64_t ldc, int64_t strideC, void* stream);
 
+/* ---- NEXT row f4: COMBRIT block size beta ------------------------------------------
+ * trinv_lower / trinv_upper use beta = 2.  trinv_tri_ex selects the block count of
+ * the TOP level of Alg. 1: beta = 2 (same as trinv_lower/upper) or
+ * beta = 4 (n = 4m, m = 32 * 2^k; the four diagonal blocks by the beta = 2 levels,
+ * then B_ij = iD_ii A_ij, the block Thm 1 inverse of the unit block
+ * triangle (via the recurrence of its proof) and iA_ij = iB_ij iD_jj
+ * (P:452), all on the DMMA engine).  Other n with beta = 4: TRINV_NOT_SUPPORTED.
+ * ws_bytes >= trinv_tri_ex_workspace_bytes(beta, n); A, X 16-byte aligned with
+ * even leading dimensions for beta = 4. */
+size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n);
+trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                            trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info, void* stream);
+
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);
 

@@ -19,7 +19,7 @@ from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMat
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
 __all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "inv_general",
-           "lu_crout", "gemm", "workspace_bytes",
+           "lu_crout", "gemm", "trinv_beta", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -154,6 +154,23 @@ def trinv_batched_host(A_host, uplo="L", *, unit=False, out=None, chunk=0, info=
     # keep the workspace alive until the stream has consumed it
     ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
     return (X, inf) if info else X
+
+
+def trinv_beta(A, uplo="L", beta=4, *, unit=False, out=None, check=False, stream=None):
+    """Triangular inverse with a COMBRIT top level of block count beta (2 or 4; NEXT row f4)."""
+    torch = _torch()
+    n = A.shape[-1]
+    lda = _ld(A)
+    X = torch.empty((n, n), dtype=torch.float64, device=A.device) if out is None else out
+    ldx = _ld(X)
+    ws, wsb = _alloc_ws(lib().trinv_tri_ex_workspace_bytes(beta, n), A.device)
+    info = _info(check, A.device)
+    _check(lib().trinv_tri_ex(uplo.encode(), beta, n, ctypes.c_void_p(A.data_ptr()), lda,
+                              ctypes.c_void_p(X.data_ptr()), ldx, TRINV_UNIT if unit else TRINV_NON_UNIT,
+                              ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+                              ctypes.c_void_p(info.data_ptr()) if info is not None else None, _stream(stream)))
+    _raise_info(info, "trinv_beta")
+    return X
 
 
 def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", stream=None):

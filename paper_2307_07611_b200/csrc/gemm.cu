@@ -455,4 +455,23 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   return launch_gemm_cfg<32, 32, 2, 2, 4>(a, s, launches);
 }
 
+// ---------------------------------------------------------------------------
+__global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    p[i * ld + j] = 0.0;
+  }
+}
+
+cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const int64_t total = rows * cols;
+  const int64_t blocks = (total + 255) / 256;
+  const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
+  zero_2d_kernel<<<grid, 256, 0, s>>>(p, ld, rows, cols);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 }  // namespace trinv

@@ -106,6 +106,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_lu_leaf(double* A, int64_t lda, int n, int32_t* info, int64_t info_off, cudaStream_t s,
                            int64_t* launches);
 double gemm_flops(const GemmArgs& a);
+// p[i*ld + j] = +0.0 for i < rows, j < cols.
+cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches);
 
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.

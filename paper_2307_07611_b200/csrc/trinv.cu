@@ -143,8 +143,9 @@ static trinv_status_t cuda_fail(cudaError_t e) {
 // Core recursion on an aligned, even-ld problem (or n <= 32 in any layout).
 // info: NULL or a single accumulator already initialised by the caller.
 static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
-                              int unit, double* W, int32_t* info, int64_t info_off, cudaStream_t s) {
-  if (n <= 64) {  // one leaf of order n (BASELINE config 0): a single launch
+                              int unit, double* W, int32_t* info, int64_t info_off, cudaStream_t s,
+                              int64_t b_stop = 0) {
+  if (n <= 64 && b_stop == 0) {  // one leaf of order n (BASELINE config 0): a single launch
     LeafArgs l1{};
     l1.A = A; l1.lda = lda; l1.sA = n * lda; l1.X = X; l1.ldx = ldx; l1.sX = n * ldx;
     l1.batch = 1; l1.n = (int)n; l1.n_last = (int)n; l1.unit = unit;
@@ -169,7 +170,8 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
     TRY(launch_leaf(uplo, lt, s, &g_launches));
   }
   // (a4-a7) levels: two grouped DMMA launches per level.
-  for (int64_t b = 32; b < n; b *= 2) {
+  const int64_t b_end = b_stop > 0 ? b_stop : n;
+  for (int64_t b = 32; b < b_end && b < n; b *= 2) {
     const int64_t merges = merges_at(n, b);
     const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, merges * b, b, b};
     LevelArgs l1{}, l2{};
@@ -236,6 +238,86 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   return TRINV_OK;
 }
 
+
+// ---- NEXT row f4: COMBRIT with beta = 4 at the top level ------------------------------
+// Alg. 1 with beta = 4 on n = 4m (m = 32 * 2^k): the four diagonal
+// blocks are inverted by the beta = 2 levels b < m ("Recall COMBRIT ...
+// or any preferred method"), then, for the upper case (the lower one is
+// its transpose image):
+//   B'_ij = -iD_ii A_ij                      (negated; 3 launches)
+//   iB = block Thm 1 inverse of [I B; 0 I]:  iB_i,i+1 = B'_i,i+1,
+//        iB_02 = B'_02 + B'_01 B'_12,  iB_03 = B'_03 + [B'_01 iB_02][B'_13; B'_23],
+//        iB_13 = B'_13 + B'_12 B'_23     (the recurrence of the proof of Thm 1, P:243,
+//                                          = the path sums of Eq. 6 in block form)
+//   iA_ij = iB_ij iD_jj                      (3 launches), iA_ii = iD_ii.
+static bool beta4_ok(int64_t n) {
+  if (n % 4) return false;
+  const int64_t m = n / 4;
+  if (m < 32) return false;
+  for (int64_t b = 32; b <= m; b *= 2)
+    if (b == m) return true;
+  return false;
+}
+static size_t beta4_ws(int64_t n) {
+  const int64_t m = n / 4;
+  size_t wl = 0;
+  for (int64_t b = 32; b < m; b *= 2) wl = std::max(wl, (size_t)(merges_at(n, b) * b * b) * sizeof(double));
+  return align_up(wl) + align_up((size_t)9 * m * m * sizeof(double));
+}
+
+static trinv_status_t run_tri_beta4(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                                    int unit, char* ws, int32_t* info, cudaStream_t s) {
+  const int64_t m = n / 4;
+  size_t wl = 0;
+  for (int64_t b = 32; b < m; b *= 2) wl = std::max(wl, (size_t)(merges_at(n, b) * b * b) * sizeof(double));
+  double* W = reinterpret_cast<double*>(ws);
+  double* WB = reinterpret_cast<double*>(ws + align_up(wl));  // 3m x 3m, ld 3m
+  const int64_t ldb = 3 * m;
+  trinv_status_t st = run_tri(uplo, n, A, lda, X, ldx, unit, W, info, 0, s, m);  // diagonal blocks iD_ii
+  if (st != TRINV_OK) return st;
+  auto Ab = [&](int64_t i, int64_t j) { return A + i * m * lda + j * m; };
+  auto Xb = [&](int64_t i, int64_t j) { return X + i * m * ldx + j * m; };
+  auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* pa, int64_t la, int triA, const double* pb,
+                  int64_t lb, int triB, double* pc, int64_t lc, double alpha, double beta) {
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K; g.batch = 1;
+    g.A = pa; g.lda = la; g.B = pb; g.ldb = lb; g.C = pc; g.ldc = lc;
+    g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
+    return cuda_fail(launch_gemm(g, s, &g_launches));
+  };
+  if (uplo == 'U') {
+    // WB block (i, j) (i < j) at rows i*m, cols (j-1)*m
+    auto Wb = [&](int64_t i, int64_t j) { return WB + i * m * ldb + (j - 1) * m; };
+    for (int64_t i = 0; i < 3 && st == TRINV_OK; ++i)  // B'_i,(i+1..3) = -iD_ii A_i,(i+1..3)
+      st = gemm(m, (3 - i) * m, m, Xb(i, i), ldx, TRI_UPPER, Ab(i, i + 1), lda, TRI_NONE, Wb(i, i + 1), ldb, -1.0, 0.0);
+    if (st == TRINV_OK)  // iB_02 = B'_02 + B'_01 B'_12
+      st = gemm(m, m, m, Wb(0, 1), ldb, TRI_NONE, Wb(1, 2), ldb, TRI_NONE, Wb(0, 2), ldb, 1.0, 1.0);
+    if (st == TRINV_OK)  // iB_03 = B'_03 + [B'_01 iB_02] [B'_13; B'_23]
+      st = gemm(m, m, 2 * m, Wb(0, 1), ldb, TRI_NONE, Wb(1, 3), ldb, TRI_NONE, Wb(0, 3), ldb, 1.0, 1.0);
+    if (st == TRINV_OK)  // iB_13 = B'_13 + B'_12 B'_23
+      st = gemm(m, m, m, Wb(1, 2), ldb, TRI_NONE, Wb(2, 3), ldb, TRI_NONE, Wb(1, 3), ldb, 1.0, 1.0);
+    for (int64_t j = 1; j < 4 && st == TRINV_OK; ++j)  // iA_(0..j-1),j = iB_(0..j-1),j iD_jj
+      st = gemm(j * m, m, m, Wb(0, j), ldb, TRI_NONE, Xb(j, j), ldx, TRI_UPPER, Xb(0, j), ldx, 1.0, 0.0);
+    for (int64_t i = 1; i < 4 && st == TRINV_OK; ++i)  // strictly lower block triangle := 0
+      st = cuda_fail(launch_zero_2d(Xb(i, 0), ldx, m, i * m, s, &g_launches));
+  } else {
+    // WB block (i, j) (i > j) at rows (i-1)*m, cols j*m
+    auto Wb = [&](int64_t i, int64_t j) { return WB + (i - 1) * m * ldb + j * m; };
+    for (int64_t j = 0; j < 3 && st == TRINV_OK; ++j)  // B'_(j+1..3),j = -A_(j+1..3),j iD_jj
+      st = gemm((3 - j) * m, m, m, Ab(j + 1, j), lda, TRI_NONE, Xb(j, j), ldx, TRI_LOWER, Wb(j + 1, j), ldb, -1.0, 0.0);
+    if (st == TRINV_OK)  // iB_20 = B'_20 + B'_21 B'_10
+      st = gemm(m, m, m, Wb(2, 1), ldb, TRI_NONE, Wb(1, 0), ldb, TRI_NONE, Wb(2, 0), ldb, 1.0, 1.0);
+    if (st == TRINV_OK)  // iB_30 = B'_30 + [B'_31 B'_32] [B'_10; iB_20]
+      st = gemm(m, m, 2 * m, Wb(3, 1), ldb, TRI_NONE, Wb(1, 0), ldb, TRI_NONE, Wb(3, 0), ldb, 1.0, 1.0);
+    if (st == TRINV_OK)  // iB_31 = B'_31 + B'_32 B'_21
+      st = gemm(m, m, m, Wb(3, 2), ldb, TRI_NONE, Wb(2, 1), ldb, TRI_NONE, Wb(3, 1), ldb, 1.0, 1.0);
+    for (int64_t i = 1; i < 4 && st == TRINV_OK; ++i)  // iA_i,(0..i-1) = iD_ii iB_i,(0..i-1)
+      st = gemm(m, i * m, m, Xb(i, i), ldx, TRI_LOWER, Wb(i, 0), ldb, TRI_NONE, Xb(i, 0), ldx, 1.0, 0.0);
+    for (int64_t i = 0; i < 3 && st == TRINV_OK; ++i)  // strictly upper block triangle := 0
+      st = cuda_fail(launch_zero_2d(Xb(i, i + 1), ldx, m, (3 - i) * m, s, &g_launches));
+  }
+  return st;
+}
 
 // ---- blocked Crout LU (NEXT row f2) -----------------------------------------------
 // Split point of the factor recursion: a multiple of 64 near n/2.
@@ -453,6 +535,26 @@ trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const doubl
                            int32_t* d_info, void* stream) {
   return inv_from_lu_core(n, Lf, ldl, Uf, ldu, X, ldx, diagL, diagU, ws, ws_bytes, d_info, true,
                           (cudaStream_t)stream);
+}
+
+trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                            trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info, void* stream) {
+  if (uplo != 'L' && uplo != 'U') return TRINV_INVALID_ARG;
+  if (beta == 2) return tri_entry(uplo, n, A, lda, X, ldx, (int)diag, ws, ws_bytes, d_info, 0, true, (cudaStream_t)stream);
+  if (beta != 4) return TRINV_INVALID_ARG;
+  trinv_status_t st = check_tri_args(n, A, lda, X, ldx, (int)diag);
+  if (st != TRINV_OK || n == 0) return st;
+  if (!beta4_ok(n) || !tma_ok(A, lda) || !tma_ok(X, ldx)) return TRINV_NOT_SUPPORTED;
+  if (ws_bytes < beta4_ws(n) || !ws) return TRINV_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
+  return run_tri_beta4(uplo, n, A, lda, X, ldx, (int)diag, static_cast<char*>(ws), d_info, s);
+}
+
+size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n) {
+  if (n <= 0) return 0;
+  if (beta == 4 && beta4_ok(n)) return beta4_ws(n);
+  return tri_ws(n, nullptr, even_up(n), nullptr, even_up(n));
 }
 
 trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,

@@ -60,5 +60,26 @@ def main():
         torch.cuda.empty_cache()
 
 
+
+
+def sweep_beta4():
+    dev = torch.device("cuda:0")
+    print(f"{'op':8s} {'n':>6s} {'beta2 ms':>10s} {'beta4 ms':>10s} {'b4/b2':>7s}")
+    for n in (256, 512, 1024, 2048, 4096, 8192, 16384):
+        reps = 50 if n <= 1024 else (10 if n <= 8192 else 3)
+        for uplo in ("L", "U"):
+            A = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(A, n, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+            X = torch.empty_like(A)
+            t2 = bench(lambda: P.trinv_beta(A, uplo, 2, out=X), reps)
+            t4 = bench(lambda: P.trinv_beta(A, uplo, 4, out=X), reps)
+            print(f"{'trinv' + uplo:8s} {n:6d} {t2:10.4f} {t4:10.4f} {t4 / t2:7.3f}", flush=True)
+            del A, X
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "beta4":
+        sweep_beta4()
+    else:
+        main()

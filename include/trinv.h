@@ -180,6 +180,17 @@ size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n);
 trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
                             trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info, void* stream);
 
+/* ---- NEXT row f3 (measurement only) ----------------------------------------------------
+ * C = A B for dense n x n (n divisible by 4) with ONE level of Strassen's 7-product
+ * recursion (the paper's fast multiplication for block products, P:20, P:46, P:523,
+ * P:614-629) over the DMMA GEMM, with element-wise block sums.  Kept out of the
+ * inversion path: see DESIGN.md §11 and profiles/r01_strassen.txt for the timing
+ * and error measurements behind that decision.  ws_bytes >=
+ * trinv_strassen_workspace_bytes(n); A, B, C 16-byte aligned with even ld. */
+size_t trinv_strassen_workspace_bytes(int64_t n);
+trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                   int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);
 

@@ -19,7 +19,7 @@ from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMat
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
 __all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "inv_general",
-           "lu_crout", "gemm", "trinv_beta", "workspace_bytes",
+           "lu_crout", "gemm", "gemm_strassen", "trinv_beta", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -194,6 +194,19 @@ def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", strea
     _check(lib().trinv_gemm(M, N, K, bs, float(alpha), ctypes.c_void_p(A.data_ptr()), lda, sa, struct_a.encode(),
                             ctypes.c_void_p(B.data_ptr()), ldb, sb, struct_b.encode(), float(beta),
                             ctypes.c_void_p(C.data_ptr()), ldc, sc, _stream(stream)))
+    return C
+
+
+def gemm_strassen(A, B, *, C=None, stream=None):
+    """C = A B (dense n x n) with one Strassen level over the DMMA GEMM (NEXT row f3, measurement)."""
+    torch = _torch()
+    n = A.shape[-1]
+    C = torch.empty((n, n), dtype=torch.float64, device=A.device) if C is None else C
+    ws, wsb = _alloc_ws(lib().trinv_strassen_workspace_bytes(n), A.device)
+    _check(lib().trinv_gemm_strassen(n, ctypes.c_void_p(A.data_ptr()), _ld(A), ctypes.c_void_p(B.data_ptr()), _ld(B),
+                                     ctypes.c_void_p(C.data_ptr()), _ld(C),
+                                     ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb,
+                                     _stream(stream)))
     return C
 
 

@@ -67,6 +67,10 @@ def lib():
     L.trinv_tri_ex_workspace_bytes.restype = _sz
     L.trinv_tri_ex.argtypes = [ctypes.c_char, _i32, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]
     L.trinv_tri_ex.restype = _i32
+    L.trinv_strassen_workspace_bytes.argtypes = [_i64]
+    L.trinv_strassen_workspace_bytes.restype = _sz
+    L.trinv_gemm_strassen.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp]
+    L.trinv_gemm_strassen.restype = _i32
     L.trinv_status_string.argtypes = [_i32]
     L.trinv_status_string.restype = ctypes.c_char_p
     L.trinv_last_cuda_error.restype = _i32

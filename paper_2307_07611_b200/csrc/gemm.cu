@@ -464,6 +464,27 @@ __global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols
   }
 }
 
+// C = alpha A + beta B (rows x cols, row-major, any leading dimensions; C may alias A or B exactly)
+__global__ void geam_kernel(int64_t rows, int64_t cols, double alpha, const double* A, int64_t lda, double beta,
+                            const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    C[i * ldc + j] = alpha * A[i * lda + j] + beta * B[i * ldb + j];
+  }
+}
+
+cudaError_t launch_geam(int64_t rows, int64_t cols, double alpha, const double* A, int64_t lda, double beta,
+                        const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s, int64_t* launches) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const int64_t total = rows * cols;
+  const int64_t blocks = (total + 255) / 256;
+  const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
+  geam_kernel<<<grid, 256, 0, s>>>(rows, cols, alpha, A, lda, beta, B, ldb, C, ldc);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const int64_t total = rows * cols;

@@ -106,6 +106,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_lu_leaf(double* A, int64_t lda, int n, int32_t* info, int64_t info_off, cudaStream_t s,
                            int64_t* launches);
 double gemm_flops(const GemmArgs& a);
+cudaError_t launch_geam(int64_t rows, int64_t cols, double alpha, const double* A, int64_t lda, double beta,
+                        const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s, int64_t* launches);
 // p[i*ld + j] = +0.0 for i < rows, j < cols.
 cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches);
 

@@ -557,6 +557,62 @@ size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n) {
   return tri_ws(n, nullptr, even_up(n), nullptr, even_up(n));
 }
 
+size_t trinv_strassen_workspace_bytes(int64_t n) {
+  if (n <= 0 || n % 2) return 0;
+  const int64_t h = n / 2, lh = even_up(h);
+  return 9 * align_up((size_t)h * lh * sizeof(double));  // 2 operand sums + 7 products
+}
+
+// NEXT row f3 (experiment): one level of Strassen's 7-product recursion (cited by
+// the paper for its block products) over the DMMA
+// GEMM for a dense n x n product C = A B (n even).
+trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                   int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n < 0 || n % 2) return n < 0 ? TRINV_INVALID_ARG : TRINV_NOT_SUPPORTED;
+  if (n == 0) return TRINV_OK;
+  if (!A || !B || !C || lda < n || ldb < n || ldc < n) return TRINV_INVALID_ARG;
+  if (!tma_ok(A, lda) || !tma_ok(B, ldb) || !tma_ok(C, ldc) || (n / 2) % 2) return TRINV_NOT_SUPPORTED;
+  if (ws_bytes < trinv_strassen_workspace_bytes(n) || !ws) return TRINV_WORKSPACE_TOO_SMALL;
+  const int64_t h = n / 2, lh = even_up(h);
+  const size_t slot = align_up((size_t)h * lh * sizeof(double));
+  auto buf = [&](int k) { return reinterpret_cast<double*>(static_cast<char*>(ws) + k * slot); };
+  double *SA = buf(0), *SB = buf(1);
+  double* M[7];
+  for (int k = 0; k < 7; ++k) M[k] = buf(2 + k);
+  const double *A11 = A, *A12 = A + h, *A21 = A + h * lda, *A22 = A + h * lda + h;
+  const double *B11 = B, *B12 = B + h, *B21 = B + h * ldb, *B22 = B + h * ldb + h;
+  double *C11 = C, *C12 = C + h, *C21 = C + h * ldc, *C22 = C + h * ldc + h;
+  auto add = [&](const double* X, int64_t lx, double b, const double* Y, int64_t ly, double* Z, int64_t lz) {
+    return cuda_fail(launch_geam(h, h, 1.0, X, lx, b, Y, ly, Z, lz, s, &g_launches));
+  };
+  auto mul = [&](const double* X, int64_t lx, const double* Y, int64_t ly, double* Z) {
+    GemmArgs g{};
+    g.M = h; g.N = h; g.K = h; g.batch = 1;
+    g.A = X; g.lda = lx; g.B = Y; g.ldb = ly; g.C = Z; g.ldc = lh;
+    g.alpha = 1.0; g.beta = 0.0; g.triA = TRI_NONE; g.triB = TRI_NONE;
+    return cuda_fail(launch_gemm(g, s, &g_launches));
+  };
+  trinv_status_t st = TRINV_OK;
+#define STEP(x) do { if (st == TRINV_OK) st = (x); } while (0)
+  STEP(add(A11, lda, 1.0, A22, lda, SA, lh)); STEP(add(B11, ldb, 1.0, B22, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[0]));
+  STEP(add(A21, lda, 1.0, A22, lda, SA, lh)); STEP(mul(SA, lh, B11, ldb, M[1]));
+  STEP(add(B12, ldb, -1.0, B22, ldb, SB, lh)); STEP(mul(A11, lda, SB, lh, M[2]));
+  STEP(add(B21, ldb, -1.0, B11, ldb, SB, lh)); STEP(mul(A22, lda, SB, lh, M[3]));
+  STEP(add(A11, lda, 1.0, A12, lda, SA, lh)); STEP(mul(SA, lh, B22, ldb, M[4]));
+  STEP(add(A21, lda, -1.0, A11, lda, SA, lh)); STEP(add(B11, ldb, 1.0, B12, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[5]));
+  STEP(add(A12, lda, -1.0, A22, lda, SA, lh)); STEP(add(B21, ldb, 1.0, B22, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[6]));
+  // C11 = M1 + M4 - M5 + M7, C12 = M3 + M5, C21 = M2 + M4, C22 = M1 - M2 + M3 + M6
+  STEP(add(M[0], lh, 1.0, M[3], lh, C11, ldc)); STEP(add(C11, ldc, -1.0, M[4], lh, C11, ldc));
+  STEP(add(C11, ldc, 1.0, M[6], lh, C11, ldc));
+  STEP(add(M[2], lh, 1.0, M[4], lh, C12, ldc));
+  STEP(add(M[1], lh, 1.0, M[3], lh, C21, ldc));
+  STEP(add(M[0], lh, -1.0, M[1], lh, C22, ldc)); STEP(add(C22, ldc, 1.0, M[2], lh, C22, ldc));
+  STEP(add(C22, ldc, 1.0, M[5], lh, C22, ldc));
+#undef STEP
+  return st;
+}
+
 trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,
                           int64_t lda, int64_t strideA, char structA, const double* B, int64_t ldb, int64_t strideB,
                           char structB, double beta, double* C, int64_t ldc, int64_t strideC, void* stream) {

@@ -120,3 +120,10 @@ def test_inv_general_n8192_sampled():
     ref = oracle.lu_columns(Lg.cpu().numpy(), Ug.cpu().numpy(), cols, unit_l=False, unit_u=True)
     assert oracle.floored_rel_err(Xs.T.contiguous().cpu().numpy(), ref, axis_cols=0) <= REL_TOL
     assert rho <= RES_TOL
+
+
+@pytest.mark.parametrize("n", [4, 64, 132, 1000])
+def test_gemm_strassen(n):
+    A = RNG.standard_normal((n, n)); B = RNG.standard_normal((n, n))
+    C = P.gemm_strassen(gpu(A), gpu(B)).cpu().numpy()
+    assert np.max(np.abs(C - A @ B)) <= 1e-12 * n

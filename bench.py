@@ -44,6 +44,9 @@ CONFIGS = {
     4: dict(workload="config4: inv_from_lu n=16384, L unit", kind="G", n=16384),
     5: dict(workload="NEXT f2: general fp64 inverse from A, n=16384 (A = L U with U unit; Crout LU without "
                      "pivoting + U^-1 L^-1), 2n^3 flops", kind="A", n=16384),
+    6: dict(workload="NEXT f1: one fp64 lower n=32768 split across the ranks (diagonal halves on ranks 0/1, "
+                     "2G balanced column panels of the off-diagonal block, gather on rank 0)", kind="S", n=32768,
+            diag="signed"),
 }
 
 
@@ -150,7 +153,7 @@ def run_reference(args):
         def step():
             oracle.crit_batched(A)
         unit, work, what = "inverses/s", sample, f"all {sample} config-1 matrices per step, OpenMP over matrices"
-    elif cfg["kind"] == "A":
+    elif cfg["kind"] in ("A",):
         m = 1024
         Lg = synth.host(m, seed=5, tag="L", diag="pos"); Ug = synth.host(m, seed=5, tag="U", uplo="U", diag="one")
         Am = Lg @ Ug
@@ -168,10 +171,11 @@ def run_reference(args):
             cost = lambda j: (n - j) ** 2 + n ** 2  # noqa: E731
             total_flops = 4 * n ** 3 / 3
         else:
-            T = synth.host(n, uplo=cfg["kind"], diag=cfg["diag"])
+            kind = "L" if cfg["kind"] == "S" else cfg["kind"]
+            T = synth.host(n, uplo=kind, diag=cfg["diag"])
             def step():
-                oracle.columns(T, cfg["kind"], cols)
-            cost = (lambda j: (n - j) ** 2) if cfg["kind"] == "L" else (lambda j: j ** 2)  # noqa: E731
+                oracle.columns(T, kind, cols)
+            cost = (lambda j: (n - j) ** 2) if kind == "L" else (lambda j: j ** 2)  # noqa: E731
             total_flops = n ** 3 / 3
         frac = sum(cost(j) for j in cols) / sum(cost(j) for j in range(n))
         work = total_flops * frac / 1e9
@@ -233,10 +237,11 @@ def cpu_baseline(cfg):
         cost = lambda j: (n - j) ** 2 + n ** 2  # noqa: E731
         total = 4 * n ** 3 / 3
     else:
-        T = synth.host(n, uplo=cfg["kind"], diag=cfg["diag"])
-        t0 = time.perf_counter(); oracle.columns(T, cfg["kind"], cols)
+        kind = "L" if cfg["kind"] == "S" else cfg["kind"]
+        T = synth.host(n, uplo=kind, diag=cfg["diag"])
+        t0 = time.perf_counter(); oracle.columns(T, kind, cols)
         dt = time.perf_counter() - t0
-        cost = (lambda j: (n - j) ** 2) if cfg["kind"] == "L" else (lambda j: j ** 2)  # noqa: E731
+        cost = (lambda j: (n - j) ** 2) if kind == "L" else (lambda j: j ** 2)  # noqa: E731
         total = n ** 3 / 3
     frac = sum(cost(j) for j in cols) / sum(cost(j) for j in range(n))
     return {"value": total * frac / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
@@ -305,7 +310,17 @@ def main():
         algo_bytes_per_launch = B * (n * (n + 1) / 2 + n * n) * 8  # triangle in + full matrix out
         flops_per_step = B * n ** 3 / 3
     else:
-        if cfg["kind"] == "A":
+        if cfg["kind"] == "S":
+            from paper_2307_07611_b200.dist import trinv_split
+            A = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(A, n, diag=cfg["diag"])  # replicated input on every rank
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            def step():
+                Y = trinv_split(A, "L")
+                if Y is not None:
+                    X.copy_(Y)
+            flops_per_step = n ** 3 / 3
+        elif cfg["kind"] == "A":
             Lg = torch.empty((n, n), dtype=torch.float64, device=dev)
             Ug = torch.empty_like(Lg)
             synth.device_fill(Lg, n, seed=5, tag="L", diag="pos")
@@ -339,6 +354,8 @@ def main():
                 f(A, out=X)
             flops_per_step = n ** 3 / 3
         units_per_rank, unit = flops_per_step / 1e9, "GFLOP/s"
+        if cfg["kind"] == "S":  # one matrix for the whole job (strong scaling): count it once
+            units_per_rank /= world
 
     for _ in range(args.warmup):
         step()
@@ -381,7 +398,8 @@ def main():
     value = units_per_rank * world * args.steps / (total_ms / 1e3)
 
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if cfg["kind"] == "S" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based SplitMix64, synth/)"}
     conf = {"workload": cfg["workload"], "n": n, "per_rank_units": units_per_rank,
             "l2_policy": "inputs larger than L2 (126 MB)" if (cfg["kind"] == "B" or n >= 4096)
@@ -458,7 +476,7 @@ def main():
                                "D2H overlapped on 3 streams) -> pinned host",
                        "pcie_gbs_each_way": nbytes / (e_ms / 1e3) / 1e9}
         del h_in, h_out, ws
-    elif cfg["kind"] != "B":
+    elif cfg["kind"] not in ("B", "S"):
         # host buffers: H2D of the input factor(s), the call, D2H of the inverse
         ins = [Lm, Um] if cfg["kind"] == "G" else [A]  # config 5: A
         h_ins = [t.cpu().pin_memory() for t in ins]

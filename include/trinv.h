@@ -158,9 +158,10 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
  *   C_g = alpha * A_g B_g + beta * C_g,
  * A_g = A + g*strideA (M x K, lda), B_g = B + g*strideB (K x N, ldb), C_g = C +
  * g*strideC (M x N, ldc), all row-major fp64 on the device.  structA = 'L' / 'U'
- * declares A lower / upper triangular (M == K; the structurally zero blocks are
- * skipped, the other triangle of its diagonal tiles must hold zeros); structB
- * likewise for B (N == K); at most one of them may be triangular; 'N' = dense.
+ * declares A[i][k] = 0 for k > i / k < i (triangular structure anchored at its
+ * top-left corner; the structurally zero blocks are skipped and the zeros inside
+ * the diagonal tiles must be stored); structB = 'L' / 'U' declares B[k][j] = 0
+ * for k < j / k > j; at most one operand may be structured; 'N' = dense.
  * A and B must be 16-byte aligned with even lda/ldb/strides (TRINV_NOT_SUPPORTED
  * otherwise); C must not overlap A or B.  K >= 1 (K = 0: TRINV_NOT_SUPPORTED). */
 trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,

@@ -438,11 +438,19 @@ static cudaError_t launch_gemm_cfg(const GemmArgs& a, cudaStream_t s, int64_t* l
 }
 
 double gemm_flops(const GemmArgs& a) {
-  // dense 2MNK, or the triangular-aware count when one operand is triangular
+  // 2 flops per multiply-add with a structurally non-zero element of the triangular operand
   const double M = (double)a.M, N = (double)a.N, K = (double)a.K;
-  if (a.triA == TRI_NONE && a.triB == TRI_NONE) return 2.0 * M * N * K * a.batch;
-  if (a.triA != TRI_NONE) return a.batch * N * M * (M + 1);  // M == K
-  return a.batch * M * N * (N + 1);                          // N == K
+  auto tri_sum = [](double rows, double K) {  // sum_{i < rows} min(i + 1, K)
+    const double full = rows < K ? rows : K;
+    return full * (full + 1) / 2 + (rows - full) * K;
+  };
+  double f;
+  if (a.triA == TRI_LOWER) f = 2 * N * tri_sum(M, K);
+  else if (a.triA == TRI_UPPER) f = 2 * N * (M * K - tri_sum(M, K) + (M < K ? M : K));
+  else if (a.triB == TRI_LOWER) f = 2 * M * (N * K - tri_sum(N, K) + (N < K ? N : K));
+  else if (a.triB == TRI_UPPER) f = 2 * M * tri_sum(N, K);
+  else f = 2 * M * N * K;
+  return f * a.batch;
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {

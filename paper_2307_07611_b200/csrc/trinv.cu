@@ -622,7 +622,6 @@ trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double
   auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
   const int ta = tri(structA), tb = tri(structB);
   if (ta < 0 || tb < 0 || (ta != TRI_NONE && tb != TRI_NONE)) return TRINV_INVALID_ARG;
-  if ((ta != TRI_NONE && M != K) || (tb != TRI_NONE && N != K)) return TRINV_INVALID_ARG;
   if (!C || (K > 0 && (!A || !B)) || ldc < N || (K > 0 && (lda < K || ldb < N))) return TRINV_INVALID_ARG;
   if (batch > 1 && (strideA < M * lda || strideB < K * ldb || strideC < M * ldc)) return TRINV_INVALID_ARG;
   // a single-row operand never uses its leading dimension: any even value is equivalent

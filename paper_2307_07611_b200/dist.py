@@ -50,3 +50,127 @@ def gather_batched(X_local, batch, group=None, dst=0):
         return None
     parts = [recv[r * cmax: r * cmax + counts[r]] for r in range(world)]
     return torch.cat(parts, dim=0)
+
+
+# ---------------------------------------------------------------------------
+# NEXT row f1: one large triangular matrix across G GPUs.
+#
+# Top-level split of COMBRIT beta = 2: for lower T = [A 0; C B],
+#   X = [A^-1 0; X21 B^-1],  X21 = -B^-1 (C A^-1).
+# Phase 1: rank 0 inverts A and rank min(1, G-1) inverts B (single-GPU path).
+# Phase 2: A^-1 and B^-1 are broadcast.
+# Phase 3: X21 is cut into 2G column panels; rank r owns panels r and 2G-1-r,
+#          which balances the triangular K-ranges of C A^-1 (panel p needs
+#          k >= its first column); per panel W_p = C[:, c0:] A^-1[c0:, p] and
+#          X21_p = -B^-1 W_p on the DMMA engine.
+# Phase 4: the panels are gathered on `dst`, which assembles X.
+# Upper T = [A B12; 0 C] mirrors this with row panels of X12 = -(A^-1 B12) C^-1.
+# Inputs are replicated on every rank (each rank generates / holds T).  The
+# collectives are torch.distributed calls (NCCL on GPU; with gloo the tensors
+# are staged through host memory, used by the CPU / single-GPU tests).
+def _split_point(n):
+    return 64 * ((n + 127) // 128)
+
+
+def _backend_is_nccl(group):
+    try:
+        return dist.get_backend(group) == "nccl"
+    except Exception:
+        return False
+
+
+def _bcast(t, src, group):
+    if _backend_is_nccl(group) or not t.is_cuda:
+        dist.broadcast(t, src, group=group)
+        return t
+    h = t.cpu()
+    dist.broadcast(h, src, group=group)
+    t.copy_(h)
+    return t
+
+
+def _gather(t, dst, group):
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    nccl = _backend_is_nccl(group)
+    send = t if (nccl or not t.is_cuda) else t.cpu()
+    out = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
+    dist.gather(send, out, dst=dst, group=group)
+    return out
+
+
+def panel_owner_map(world):
+    """Panels (2G of them) owned by each rank: r -> (r, 2G-1-r)."""
+    return {r: (r, 2 * world - 1 - r) for r in range(world)}
+
+
+def trinv_split(T, uplo="L", group=None, dst=0, inv=None, gemm=None):
+    """Invert one n x n triangular matrix across the ranks of `group` (see above).
+
+    T: the full matrix on every rank (device tensor for the GPU path).  Returns X
+    on `dst` and None elsewhere.  `inv(T_block, uplo)` and `gemm(A, B, alpha,
+    struct_a, struct_b)` default to this package's kernels; tests may pass CPU
+    stand-ins to exercise the partition and communication logic without a GPU.
+    """
+    from . import gemm as _gemm, trinv_lower, trinv_upper
+    if inv is None:
+        def inv(M, u):
+            M = M.contiguous()
+            return trinv_lower(M) if u == "L" else trinv_upper(M)
+    if gemm is None:
+        def gemm(A, B, alpha, sa, sb):
+            return _gemm(A, B, alpha=alpha, struct_a=sa, struct_b=sb)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = T.shape[0]
+    h = _split_point(n)
+    if h >= n:  # too small to split
+        X = inv(T, uplo)
+        return X if rank == dst else None
+    r = n - h
+    src_b = min(1, world - 1)
+    # phase 1
+    Ainv = inv(T[:h, :h], uplo) if rank == 0 else torch.empty((h, h), dtype=T.dtype, device=T.device)
+    Binv = inv(T[h:, h:], uplo) if rank == src_b else torch.empty((r, r), dtype=T.dtype, device=T.device)
+    # phase 2
+    if world > 1:
+        _bcast(Ainv, 0, group)
+        _bcast(Binv, src_b, group)
+    # phase 3: 2G panels of the off-diagonal block
+    P = 2 * world
+    w = (h + P - 1) // P
+    w += w % 2  # keep 16-byte aligned column offsets
+    mine = panel_owner_map(world)[rank]
+    panels = []
+    for p in mine:
+        c0, c1 = p * w, min(h, (p + 1) * w)
+        if uplo == "L":
+            buf = torch.zeros((r, w), dtype=T.dtype, device=T.device)
+            if c0 < c1:
+                Wp = gemm(T[h:, c0:h], Ainv[c0:, c0:c1], 1.0, "N", "L")   # C A^-1, k >= c0
+                buf[:, : c1 - c0] = gemm(Binv, Wp, -1.0, "L", "N")        # -B^-1 W
+        else:
+            buf = torch.zeros((w, r), dtype=T.dtype, device=T.device)
+            if c0 < c1:
+                Wp = gemm(Ainv[c0:c1, c0:], T[c0:h, h:], 1.0, "U", "N")   # A^-1 B12, k >= c0
+                buf[: c1 - c0, :] = gemm(Wp, Binv, -1.0, "N", "U")        # -W C^-1
+        panels.append(buf)
+    # phase 4
+    stack = torch.stack(panels)
+    got = _gather(stack, dst, group) if world > 1 else [stack]
+    if rank != dst:
+        return None
+    X = torch.zeros((n, n), dtype=T.dtype, device=T.device)
+    X[:h, :h] = Ainv
+    X[h:, h:] = Binv
+    for rk, part in enumerate(got):
+        part = part.to(T.device)
+        for k, p in enumerate(panel_owner_map(world)[rk]):
+            c0, c1 = p * w, min(h, (p + 1) * w)
+            if c0 >= c1:
+                continue
+            if uplo == "L":
+                X[h:, c0:c1] = part[k][:, : c1 - c0]
+            else:
+                X[c0:c1, h:] = part[k][: c1 - c0, :]
+    return X

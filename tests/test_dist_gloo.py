@@ -67,3 +67,45 @@ def test_gloo_world2_partition_and_gather(B):
     results = [q.get(timeout=5) for _ in range(world)]
     assert all(results), results
     assert all(p.exitcode == 0 for p in procs)
+
+
+# --- NEXT row f1: one matrix split across ranks (partition + collectives, CPU stand-ins) ---
+def _split_worker(rank, world, port, n, uplo, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        from paper_2307_07611_b200.dist import trinv_split
+        T = torch.from_numpy(synth.host(n, seed=3, uplo=uplo, diag="signed" if uplo == "L" else "pos"))
+
+        def inv(M, u):
+            return torch.from_numpy(oracle.trinv(M.contiguous().numpy(), u))
+
+        def gemm(A, B, alpha, sa, sb):
+            return alpha * (A @ B)
+
+        X = trinv_split(T, uplo, inv=inv, gemm=gemm)
+        if rank == 0:
+            R = oracle.trinv(T.numpy(), uplo)
+            q.put(oracle.floored_rel_err(X.numpy(), R) <= 1e-12 and oracle.residual_ratio(T.numpy(), X.numpy()) < 1e-15)
+        else:
+            q.put(X is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,uplo", [(2, 300, "L"), (3, 257, "U"), (2, 128, "U")])
+def test_gloo_split_single_matrix(world, n, uplo):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, n, uplo, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    results = [q.get(timeout=5) for _ in range(world)]
+    assert all(results), results
+    assert all(p.exitcode == 0 for p in procs)

@@ -6,7 +6,8 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 HEADER = os.path.join(HERE, "..", "include", "trinv.h")
-_SO = os.path.join(HERE, "libtrinv.so")
+# TRINV_LIB may point at another build of the same ABI (A/B measurements only)
+_SO = os.environ.get("TRINV_LIB") or os.path.join(HERE, "libtrinv.so")
 
 TRINV_OK, TRINV_INVALID_ARG, TRINV_ALIASING, TRINV_WORKSPACE_TOO_SMALL, TRINV_CUDA_ERROR, TRINV_NOT_SUPPORTED = range(6)
 TRINV_NON_UNIT, TRINV_UNIT = 0, 1
@@ -42,43 +43,39 @@ def lib():
     if not os.path.exists(_SO):
         raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = ctypes.CDLL(_SO)
-    L.trinv_workspace_bytes.argtypes = [ctypes.c_char, _i64, _vp, _i64, _vp, _i64]
-    L.trinv_workspace_bytes.restype = _sz
+    def sig(name, args, res=None):
+        try:
+            f = getattr(L, name)
+        except AttributeError:
+            if os.environ.get("TRINV_LIB"):  # an older build under A/B test: skip newer entry points
+                return
+            raise
+        if args is not None:
+            f.argtypes = args
+        if res is not None:
+            f.restype = res
+
+    sig("trinv_workspace_bytes", [ctypes.c_char, _i64, _vp, _i64, _vp, _i64], _sz)
     for name in ("trinv_lower", "trinv_upper"):
-        f = getattr(L, name)
-        f.argtypes = [_i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]
-        f.restype = _i32
-    L.trinv_batched.argtypes = [ctypes.c_char, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp]
-    L.trinv_batched.restype = _i32
-    L.trinv_batched_host_workspace_bytes.argtypes = [_i64, _i64]
-    L.trinv_batched_host_workspace_bytes.restype = _sz
-    L.trinv_batched_host.argtypes = [ctypes.c_char, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp]
-    L.trinv_batched_host.restype = _i32
-    L.inv_from_lu.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _vp]
-    L.inv_from_lu.restype = _i32
-    L.lu_crout.argtypes = [_i64, _vp, _i64, _vp, _sz, _vp, _vp]
-    L.lu_crout.restype = _i32
-    L.inv_general.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp, _vp]
-    L.inv_general.restype = _i32
-    L.trinv_gemm.argtypes = [_i64, _i64, _i64, _i64, ctypes.c_double, _vp, _i64, _i64, ctypes.c_char, _vp, _i64,
-                             _i64, ctypes.c_char, ctypes.c_double, _vp, _i64, _i64, _vp]
-    L.trinv_gemm.restype = _i32
-    L.trinv_tri_ex_workspace_bytes.argtypes = [_i32, _i64]
-    L.trinv_tri_ex_workspace_bytes.restype = _sz
-    L.trinv_tri_ex.argtypes = [ctypes.c_char, _i32, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]
-    L.trinv_tri_ex.restype = _i32
-    L.trinv_strassen_workspace_bytes.argtypes = [_i64]
-    L.trinv_strassen_workspace_bytes.restype = _sz
-    L.trinv_gemm_strassen.argtypes = [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp]
-    L.trinv_gemm_strassen.restype = _i32
-    L.trinv_status_string.argtypes = [_i32]
-    L.trinv_status_string.restype = ctypes.c_char_p
-    L.trinv_last_cuda_error.restype = _i32
-    L.trinv_version.restype = ctypes.c_char_p
-    L.trinv_launch_count.restype = _i64
-    L.trinv_profile_read.argtypes = [_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
-                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
-    L.trinv_profile_read.restype = _i32
+        sig(name, [_i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp], _i32)
+    sig("trinv_batched", [ctypes.c_char, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp], _i32)
+    sig("trinv_batched_host_workspace_bytes", [_i64, _i64], _sz)
+    sig("trinv_batched_host", [ctypes.c_char, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp], _i32)
+    sig("inv_from_lu", [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _vp], _i32)
+    sig("lu_crout", [_i64, _vp, _i64, _vp, _sz, _vp, _vp], _i32)
+    sig("inv_general", [_i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp, _vp], _i32)
+    sig("trinv_gemm", [_i64, _i64, _i64, _i64, ctypes.c_double, _vp, _i64, _i64, ctypes.c_char, _vp, _i64,
+                             _i64, ctypes.c_char, ctypes.c_double, _vp, _i64, _i64, _vp], _i32)
+    sig("trinv_tri_ex_workspace_bytes", [_i32, _i64], _sz)
+    sig("trinv_tri_ex", [ctypes.c_char, _i32, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp], _i32)
+    sig("trinv_strassen_workspace_bytes", [_i64], _sz)
+    sig("trinv_gemm_strassen", [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp], _i32)
+    sig("trinv_status_string", [_i32], ctypes.c_char_p)
+    sig("trinv_last_cuda_error", None, _i32)
+    sig("trinv_version", None, ctypes.c_char_p)
+    sig("trinv_launch_count", None, _i64)
+    sig("trinv_profile_read", [_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _i32)
     _lib = L
     return L
 

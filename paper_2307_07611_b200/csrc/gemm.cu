@@ -37,17 +37,17 @@ namespace trinv {
 
 constexpr int BK = 16;
 
-// One output tile: where its operands come from, its K-range and its epilogue.
+// One output tile: where its operands come from and its K-range.  Only o_row /
+// o_col / g stay live across the main loop; everything else of the epilogue is
+// read from the kernel parameters (constant bank), which keeps the 128x128 tile
+// within the 168-register cap of a 9-warp CTA without spills.
 struct TileJob {
-  int64_t a_row, a_col;  // A-operand: rows a_row.., columns a_col + k
-  int64_t b_row, b_col;  // B-operand: rows b_row + k, columns b_col..
+  int32_t a_row, a_col;  // A-operand: rows a_row.., columns a_col + k
+  int32_t b_row, b_col;  // B-operand: rows b_row + k, columns b_col..
   int32_t ga, gb;        // 3rd TMA coordinate (batch) of A / B (3-D maps only)
-  int64_t k_begin, k_end;
-  double* out;           // output tile origin
-  int64_t ldo, out_rows, out_cols;  // leading dimension, rows / columns left from the origin
-  double alpha, beta;
-  double* mir;           // mirror tile origin to zero-fill (BN rows x BM columns), or NULL
-  int64_t ldm, mir_rows, mir_cols;
+  int32_t k_begin, k_end;
+  int32_t o_row, o_col, g;  // output tile origin (and batch index)
+  int32_t m_row, m_col;     // mirror tile origin (zero fill, level modes 2), or -1
   bool valid;
 };
 
@@ -65,146 +65,165 @@ struct GemmCfg {
 };
 
 // ---------------------------------------------------------------------------
-// Level tile mapping (grid order = longest K first, so the hardware block
-// scheduler approximates a longest-processing-time schedule).
-template <int BM, int BN>
-__device__ __forceinline__ TileJob level_job(const LevelArgs& p, int64_t t) {
-  TileJob j{};
-  const int64_t b = p.b, n = p.n, merges = p.merges;
-  const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
-  int64_t g = 0, I = 0, J = 0;
-  switch (p.mode) {
-    case MODE_LOWER_1: {  // J ascending
-      J = t / (merges * TMmax);
-      const int64_t rem = t % (merges * TMmax);
-      g = rem / TMmax; I = rem % TMmax;
-    } break;
-    case MODE_LOWER_2: {  // I descending
-      I = TMmax - 1 - t / (merges * TNmax);
-      const int64_t rem = t % (merges * TNmax);
-      g = rem / TNmax; J = rem % TNmax;
-    } break;
-    case MODE_UPPER_1: {  // I ascending
-      I = t / (merges * TNmax);
-      const int64_t rem = t % (merges * TNmax);
-      g = rem / TNmax; J = rem % TNmax;
-    } break;
-    case MODE_UPPER_2: {  // J descending
-      J = TNmax - 1 - t / (merges * TMmax);
-      const int64_t rem = t % (merges * TMmax);
-      g = rem / TMmax; I = rem % TMmax;
-    } break;
-    default: {  // MODE_UL: max(I, J) ascending
-      int64_t m = (int64_t)sqrt((double)t);
-      while (m * m > t) --m;
-      while ((m + 1) * (m + 1) <= t) ++m;
-      const int64_t q = t - m * m;
-      if (q <= m) { I = m; J = q; } else { I = q - m - 1; J = m; }
-    } break;
+// Level launches: tile mapping (grid order = longest K first, so the hardware
+// block scheduler approximates a longest-processing-time schedule) + epilogue.
+struct LevelTraits {
+  using Params = LevelArgs;
+  template <int BM, int BN>
+  static __device__ __forceinline__ TileJob job(const LevelArgs& p, int64_t t) {
+    TileJob j{};
+    const int64_t b = p.b, n = p.n, merges = p.merges;
+    const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
+    int64_t g = 0, I = 0, J = 0;
+    switch (p.mode) {
+      case MODE_LOWER_1: {  // J ascending
+        J = t / (merges * TMmax);
+        const int64_t rem = t % (merges * TMmax);
+        g = rem / TMmax; I = rem % TMmax;
+      } break;
+      case MODE_LOWER_2: {  // I descending
+        I = TMmax - 1 - t / (merges * TNmax);
+        const int64_t rem = t % (merges * TNmax);
+        g = rem / TNmax; J = rem % TNmax;
+      } break;
+      case MODE_UPPER_1: {  // I ascending
+        I = t / (merges * TNmax);
+        const int64_t rem = t % (merges * TNmax);
+        g = rem / TNmax; J = rem % TNmax;
+      } break;
+      case MODE_UPPER_2: {  // J descending
+        J = TNmax - 1 - t / (merges * TMmax);
+        const int64_t rem = t % (merges * TMmax);
+        g = rem / TMmax; I = rem % TMmax;
+      } break;
+      default: {  // MODE_UL: max(I, J) ascending
+        int64_t m = (int64_t)sqrt((double)t);
+        while (m * m > t) --m;
+        while ((m + 1) * (m + 1) <= t) ++m;
+        const int64_t q = t - m * m;
+        if (q <= m) { I = m; J = q; } else { I = q - m - 1; J = m; }
+      } break;
+    }
+    const int64_t s = 2 * g * b;
+    const int64_t r = (p.mode == MODE_UL) ? n : (n - s - b < b ? n - s - b : b);  // second half
+    j.valid = true;
+    j.m_row = j.m_col = -1;
+    j.g = 0; j.ga = j.gb = 0;
+    switch (p.mode) {
+      case MODE_LOWER_1:
+        j.valid = I * BM < r;
+        j.a_row = (int32_t)(s + b + I * BM); j.a_col = (int32_t)s;
+        j.b_row = (int32_t)s; j.b_col = (int32_t)(s + J * BN);
+        j.o_row = (int32_t)(g * b + I * BM); j.o_col = (int32_t)(J * BN);
+        j.k_begin = (int32_t)(J * BN); j.k_end = (int32_t)b;
+        break;
+      case MODE_LOWER_2:
+        j.valid = I * BM < r;
+        j.a_row = (int32_t)(s + b + I * BM); j.a_col = (int32_t)(s + b);
+        j.b_row = (int32_t)(g * b); j.b_col = (int32_t)(J * BN);
+        j.o_row = (int32_t)(s + b + I * BM); j.o_col = (int32_t)(s + J * BN);
+        j.m_row = (int32_t)(s + J * BN); j.m_col = (int32_t)(s + b + I * BM);
+        j.k_begin = 0; j.k_end = (int32_t)((I + 1) * BM < r ? (I + 1) * BM : r);
+        break;
+      case MODE_UPPER_1:
+        j.valid = J * BN < r;
+        j.a_row = (int32_t)(s + I * BM); j.a_col = (int32_t)s;
+        j.b_row = (int32_t)s; j.b_col = (int32_t)(s + b + J * BN);
+        j.o_row = (int32_t)(g * b + I * BM); j.o_col = (int32_t)(J * BN);
+        j.k_begin = (int32_t)(I * BM); j.k_end = (int32_t)b;
+        break;
+      case MODE_UPPER_2:
+        j.valid = J * BN < r;
+        j.a_row = (int32_t)(g * b + I * BM); j.a_col = 0;
+        j.b_row = (int32_t)(s + b); j.b_col = (int32_t)(s + b + J * BN);
+        j.o_row = (int32_t)(s + I * BM); j.o_col = (int32_t)(s + b + J * BN);
+        j.m_row = (int32_t)(s + b + J * BN); j.m_col = (int32_t)(s + I * BM);
+        j.k_begin = 0; j.k_end = (int32_t)((J + 1) * BN < r ? (J + 1) * BN : r);
+        break;
+      default:
+        j.a_row = (int32_t)(I * BM); j.a_col = 0;
+        j.b_row = 0; j.b_col = (int32_t)(J * BN);
+        j.o_row = (int32_t)(I * BM); j.o_col = (int32_t)(J * BN);
+        j.k_begin = (int32_t)((I * BM > J * BN) ? I * BM : J * BN); j.k_end = (int32_t)n;
+        break;
+    }
+    return j;
   }
-  const int64_t s = 2 * g * b;
-  const int64_t r = (p.mode == MODE_UL) ? n : (n - s - b < b ? n - s - b : b);  // second half
-  int64_t o_row = 0, o_col = 0, m_row = 0, m_col = 0;
-  bool mirror = false;
-  j.valid = true;
-  switch (p.mode) {
-    case MODE_LOWER_1:
-      j.valid = I * BM < r;
-      j.a_row = s + b + I * BM; j.a_col = s;
-      j.b_row = s; j.b_col = s + J * BN;
-      o_row = g * b + I * BM; o_col = J * BN;
-      j.k_begin = J * BN; j.k_end = b;
-      break;
-    case MODE_LOWER_2:
-      j.valid = I * BM < r;
-      j.a_row = s + b + I * BM; j.a_col = s + b;
-      j.b_row = g * b; j.b_col = J * BN;
-      o_row = s + b + I * BM; o_col = s + J * BN;
-      mirror = true; m_row = s + J * BN; m_col = s + b + I * BM;
-      j.k_begin = 0; j.k_end = (I + 1) * BM < r ? (I + 1) * BM : r;
-      break;
-    case MODE_UPPER_1:
-      j.valid = J * BN < r;
-      j.a_row = s + I * BM; j.a_col = s;
-      j.b_row = s; j.b_col = s + b + J * BN;
-      o_row = g * b + I * BM; o_col = J * BN;
-      j.k_begin = I * BM; j.k_end = b;
-      break;
-    case MODE_UPPER_2:
-      j.valid = J * BN < r;
-      j.a_row = g * b + I * BM; j.a_col = 0;
-      j.b_row = s + b; j.b_col = s + b + J * BN;
-      o_row = s + I * BM; o_col = s + b + J * BN;
-      mirror = true; m_row = s + b + J * BN; m_col = s + I * BM;
-      j.k_begin = 0; j.k_end = (J + 1) * BN < r ? (J + 1) * BN : r;
-      break;
-    default:
-      j.a_row = I * BM; j.a_col = 0;
-      j.b_row = 0; j.b_col = J * BN;
-      o_row = I * BM; o_col = J * BN;
-      j.k_begin = (I * BM > J * BN) ? I * BM : J * BN; j.k_end = n;
-      break;
+  static __device__ __forceinline__ double* out(const LevelArgs& p, const TileJob& j) {
+    return p.out + (int64_t)j.o_row * p.ldo + j.o_col;
   }
-  j.ga = j.gb = 0;
-  j.out = p.out + o_row * p.ldo + o_col;
-  j.ldo = p.ldo; j.out_rows = p.out_rows - o_row; j.out_cols = p.out_cols - o_col;
-  j.alpha = p.alpha; j.beta = 0.0;
-  if (mirror) {
-    j.mir = p.mir + m_row * p.ldm + m_col;
-    j.ldm = p.ldm; j.mir_rows = n - m_row; j.mir_cols = n - m_col;
-  } else {
-    j.mir = nullptr;
-  }
-  return j;
-}
+  static __device__ __forceinline__ int64_t ldo(const LevelArgs& p) { return p.ldo; }
+  static __device__ __forceinline__ int64_t rows_left(const LevelArgs& p, const TileJob& j) { return p.out_rows - j.o_row; }
+  static __device__ __forceinline__ int64_t cols_left(const LevelArgs& p, const TileJob& j) { return p.out_cols - j.o_col; }
+  static __device__ __forceinline__ double alpha(const LevelArgs& p) { return p.alpha; }
+  static __device__ __forceinline__ double beta(const LevelArgs&) { return 0.0; }
+  static __device__ __forceinline__ double* mir(const LevelArgs& p) { return p.mir; }
+  static __device__ __forceinline__ int64_t ldm(const LevelArgs& p) { return p.ldm; }
+  static __device__ __forceinline__ int64_t n(const LevelArgs& p) { return p.n; }
+};
 
-// General batched GEMM tile mapping: g outer, then I, J (K-range classes of a
+// General batched GEMM: tiles g outer, then I, J (K-range classes of a
 // triangular operand ordered longest first).
-template <int BM, int BN>
-__device__ __forceinline__ TileJob gemm_job(const GemmArgs& p, int64_t t) {
-  TileJob j{};
-  const int64_t TM = (p.M + BM - 1) / BM, TN = (p.N + BN - 1) / BN;
-  const int64_t per = TM * TN;
-  const int64_t g = t / per, rem = t % per;
-  int64_t I, J;
-  if (p.triA != TRI_NONE) {  // class = I (its K-range)
-    I = rem / TN; J = rem % TN;
-    if (p.triA == TRI_LOWER) I = TM - 1 - I;  // long K (large I) first
-  } else {
-    J = rem / TM; I = rem % TM;
-    if (p.triB == TRI_UPPER) J = TN - 1 - J;  // long K (large J) first
+struct GemmTraits {
+  using Params = GemmArgs;
+  template <int BM, int BN>
+  static __device__ __forceinline__ TileJob job(const GemmArgs& p, int64_t t) {
+    TileJob j{};
+    const int64_t TM = (p.M + BM - 1) / BM, TN = (p.N + BN - 1) / BN;
+    const int64_t per = TM * TN;
+    const int64_t g = t / per, rem = t % per;
+    int64_t I, J;
+    if (p.triA != TRI_NONE) {  // class = I (its K-range)
+      I = rem / TN; J = rem % TN;
+      if (p.triA == TRI_LOWER) I = TM - 1 - I;  // long K (large I) first
+    } else {
+      J = rem / TM; I = rem % TM;
+      if (p.triB == TRI_UPPER) J = TN - 1 - J;  // long K (large J) first
+    }
+    int64_t kb = 0, ke = p.K;
+    if (p.triA == TRI_LOWER) ke = ke < (I + 1) * BM ? ke : (I + 1) * BM;  // A[i][k] = 0 for k > i
+    if (p.triA == TRI_UPPER) kb = kb > I * BM ? kb : I * BM;              // A[i][k] = 0 for k < i
+    if (p.triB == TRI_LOWER) kb = kb > J * BN ? kb : J * BN;              // B[k][j] = 0 for k < j
+    if (p.triB == TRI_UPPER) ke = ke < (J + 1) * BN ? ke : (J + 1) * BN;  // B[k][j] = 0 for k > j
+    j.valid = true;
+    j.a_row = (int32_t)(I * BM); j.a_col = 0;
+    j.b_row = 0; j.b_col = (int32_t)(J * BN);
+    j.ga = j.gb = j.g = (int32_t)g;
+    j.k_begin = (int32_t)kb; j.k_end = (int32_t)(ke > kb ? ke : kb);
+    j.o_row = (int32_t)(I * BM); j.o_col = (int32_t)(J * BN);
+    j.m_row = j.m_col = -1;
+    return j;
   }
-  int64_t kb = 0, ke = p.K;
-  if (p.triA == TRI_LOWER) ke = ke < (I + 1) * BM ? ke : (I + 1) * BM;  // A[i][k] = 0 for k > i
-  if (p.triA == TRI_UPPER) kb = kb > I * BM ? kb : I * BM;              // A[i][k] = 0 for k < i
-  if (p.triB == TRI_LOWER) kb = kb > J * BN ? kb : J * BN;              // B[k][j] = 0 for k < j
-  if (p.triB == TRI_UPPER) ke = ke < (J + 1) * BN ? ke : (J + 1) * BN;  // B[k][j] = 0 for k > j
-  j.valid = true;
-  j.a_row = I * BM; j.a_col = 0;
-  j.b_row = 0; j.b_col = J * BN;
-  j.ga = (int32_t)g; j.gb = (int32_t)g;
-  j.k_begin = kb; j.k_end = ke > kb ? ke : kb;
-  j.out = p.C + g * p.sC + (I * BM) * p.ldc + J * BN;
-  j.ldo = p.ldc; j.out_rows = p.M - I * BM; j.out_cols = p.N - J * BN;
-  j.alpha = p.alpha; j.beta = p.beta;
-  j.mir = nullptr;
-  return j;
-}
+  static __device__ __forceinline__ double* out(const GemmArgs& p, const TileJob& j) {
+    return p.C + (int64_t)j.g * p.sC + (int64_t)j.o_row * p.ldc + j.o_col;
+  }
+  static __device__ __forceinline__ int64_t ldo(const GemmArgs& p) { return p.ldc; }
+  static __device__ __forceinline__ int64_t rows_left(const GemmArgs& p, const TileJob& j) { return p.M - j.o_row; }
+  static __device__ __forceinline__ int64_t cols_left(const GemmArgs& p, const TileJob& j) { return p.N - j.o_col; }
+  static __device__ __forceinline__ double alpha(const GemmArgs& p) { return p.alpha; }
+  static __device__ __forceinline__ double beta(const GemmArgs& p) { return p.beta; }
+  static __device__ __forceinline__ double* mir(const GemmArgs&) { return nullptr; }
+  static __device__ __forceinline__ int64_t ldm(const GemmArgs&) { return 0; }
+  static __device__ __forceinline__ int64_t n(const GemmArgs&) { return 0; }
+};
 
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int WM, int WN, int STAGES, int RANK>
-__device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensorMap* mapB, const TileJob& tj,
-                                         unsigned char* smem_raw) {
+template <int BM, int BN, int WM, int WN, int STAGES, int RANK, typename TR>
+__device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensorMap* mapB,
+                                         const typename TR::Params& p, unsigned char* smem_raw) {
   using C = GemmCfg<BM, BN, WM, WN, STAGES>;
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const TileJob tj = TR::template job<BM, BN>(p, blockIdx.x);
+  if (!tj.valid) return;
+  // align by offsetting the __shared__ pointer itself (an integer round trip would turn
+  // the fragment loads into generic LD instead of LDS)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BK/4][BM][4]
   double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);  // [STAGES][BN/4][BK][4]
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nk = (tj.k_end - tj.k_begin + BK - 1) / BK;
+  const int nk = (tj.k_end - tj.k_begin + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -220,29 +239,27 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
     if (lane == 0) {
       tma_prefetch_desc(mapA);
       tma_prefetch_desc(mapB);
-      for (int64_t kt = 0; kt < nk; ++kt) {
-        const int s = (int)(kt % STAGES);
-        const int64_t use = kt / STAGES;
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        const int use = kt / STAGES;
         if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        const int64_t k = tj.k_begin + kt * BK;
+        const int32_t k = tj.k_begin + kt * BK;
         double* sa = sA + (size_t)s * BM * BK;
 #pragma unroll
         for (int kb = 0; kb < BK / 4; ++kb) {
           if (RANK == 2)
-            tma_load_2d(sa + kb * BM * 4, mapA, (int32_t)(tj.a_col + k + 4 * kb), (int32_t)tj.a_row, &full[s]);
+            tma_load_2d(sa + kb * BM * 4, mapA, tj.a_col + k + 4 * kb, tj.a_row, &full[s]);
           else
-            tma_load_3d(sa + kb * BM * 4, mapA, (int32_t)(tj.a_col + k + 4 * kb), (int32_t)tj.a_row, tj.ga,
-                        &full[s]);
+            tma_load_3d(sa + kb * BM * 4, mapA, tj.a_col + k + 4 * kb, tj.a_row, tj.ga, &full[s]);
         }
         double* sb = sB + (size_t)s * BK * BN;
 #pragma unroll
         for (int nb = 0; nb < BN / 4; ++nb) {
           if (RANK == 2)
-            tma_load_2d(sb + nb * BK * 4, mapB, (int32_t)(tj.b_col + nb * 4), (int32_t)(tj.b_row + k), &full[s]);
+            tma_load_2d(sb + nb * BK * 4, mapB, tj.b_col + nb * 4, tj.b_row + k, &full[s]);
           else
-            tma_load_3d(sb + nb * BK * 4, mapB, (int32_t)(tj.b_col + nb * 4), (int32_t)(tj.b_row + k), tj.gb,
-                        &full[s]);
+            tma_load_3d(sb + nb * BK * 4, mapB, tj.b_col + nb * 4, tj.b_row + k, tj.gb, &full[s]);
         }
       }
     }
@@ -250,14 +267,16 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   }
 
   // ---------------- consumers ----------------
-  if (tj.mir) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
+  if (tj.m_row >= 0) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
+    const int64_t nn = TR::n(p), ldm = TR::ldm(p);
+    double* mir = TR::mir(p) + (int64_t)tj.m_row * ldm + tj.m_col;
     constexpr int PAIRS = BM / 2;
     for (int e = threadIdx.x; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
       const int64_t row = e / PAIRS, col = 2 * (e % PAIRS);
-      if (row < tj.mir_rows) {
-        double* q = tj.mir + row * tj.ldm + col;
-        if (col + 1 < tj.mir_cols) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
-        else if (col < tj.mir_cols) *q = 0.0;
+      if (tj.m_row + row < nn) {
+        double* q = mir + row * ldm + col;
+        if (tj.m_col + col + 1 < nn) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
+        else if (tj.m_col + col < nn) *q = 0.0;
       }
     }
   }
@@ -273,8 +292,8 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   // per-lane fragment offsets (doubles): A[row][k] in box k/4 of [BM][4]; B[k][col] in box col/4 of [BK][4]
   const int a_base = (wm * C::WTM + lr) * 4 + lc;
   const int b_base = ((wn * C::WTN + lr) >> 2) * BK * 4 + lc * 4 + (lr & 3);
-  for (int64_t kt = 0; kt < nk; ++kt) {
-    const int s = (int)(kt % STAGES);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % STAGES;
     mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
     const double* a_st = sA + (size_t)s * BM * BK + a_base;
     const double* b_st = sB + (size_t)s * BK * BN + b_base;
@@ -295,34 +314,30 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   }
 
   // ---------------- epilogue: out = alpha * acc (+ beta * out), clipped ----------------
+  double* out = TR::out(p, tj);
+  const int64_t ldo = TR::ldo(p), rows = TR::rows_left(p, tj), cols = TR::cols_left(p, tj);
+  const double alpha = TR::alpha(p), beta = TR::beta(p);
   // 16-byte stores need an even leading dimension and an aligned tile origin
-  const bool vec = ((reinterpret_cast<uintptr_t>(tj.out) & 15u) == 0) && (tj.ldo % 2 == 0);
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (ldo % 2 == 0);
 #pragma unroll
   for (int mi = 0; mi < C::FM; ++mi) {
     const int64_t row = wm * C::WTM + mi * 8 + lr;
-    if (row >= tj.out_rows) continue;
-    double* orow = tj.out + row * tj.ldo;
+    if (row >= rows) continue;
+    double* orow = out + row * ldo;
 #pragma unroll
     for (int ni = 0; ni < C::FN; ++ni) {
       const int64_t col = wn * C::WTN + ni * 8 + 2 * lc;
-      double v0 = tj.alpha * acc[mi][ni][0], v1 = tj.alpha * acc[mi][ni][1];
-      if (col + 1 < tj.out_cols && !vec) {
-        if (tj.beta != 0.0) {
-          v0 = fma(tj.beta, orow[col], v0);
-          v1 = fma(tj.beta, orow[col + 1], v1);
-        }
-        orow[col] = v0;
-        orow[col + 1] = v1;
-      } else if (col + 1 < tj.out_cols) {
-        if (tj.beta != 0.0) {
+      double v0 = alpha * acc[mi][ni][0], v1 = alpha * acc[mi][ni][1];
+      if (col + 1 < cols && vec) {
+        if (beta != 0.0) {
           const double2 o = *reinterpret_cast<const double2*>(orow + col);
-          v0 = fma(tj.beta, o.x, v0);
-          v1 = fma(tj.beta, o.y, v1);
+          v0 = fma(beta, o.x, v0);
+          v1 = fma(beta, o.y, v1);
         }
         *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
-      } else if (col < tj.out_cols) {
-        if (tj.beta != 0.0) v0 = fma(tj.beta, orow[col], v0);
-        orow[col] = v0;
+      } else {
+        if (col < cols) orow[col] = (beta != 0.0) ? fma(beta, orow[col], v0) : v0;
+        if (col + 1 < cols) orow[col + 1] = (beta != 0.0) ? fma(beta, orow[col + 1], v1) : v1;
       }
     }
   }
@@ -333,9 +348,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
     dmma_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       const LevelArgs p) {
   extern __shared__ unsigned char smem_raw[];
-  const TileJob tj = level_job<BM, BN>(p, blockIdx.x);
-  if (!tj.valid) return;
-  run_tile<BM, BN, WM, WN, STAGES, 2>(&mapA, &mapB, tj, smem_raw);
+  run_tile<BM, BN, WM, WN, STAGES, 2, LevelTraits>(&mapA, &mapB, p, smem_raw);
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES>
@@ -343,8 +356,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
     dmma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const GemmArgs p) {
   extern __shared__ unsigned char smem_raw[];
-  const TileJob tj = gemm_job<BM, BN>(p, blockIdx.x);
-  run_tile<BM, BN, WM, WN, STAGES, 3>(&mapA, &mapB, tj, smem_raw);
+  run_tile<BM, BN, WM, WN, STAGES, 3, GemmTraits>(&mapA, &mapB, p, smem_raw);
 }
 
 // ---------------------------------------------------------------------------

@@ -47,7 +47,7 @@ typedef enum {
   TRINV_ALIASING = 2,             /* input and output ranges overlap (non-batched calls) */
   TRINV_WORKSPACE_TOO_SMALL = 3,  /* ws_bytes < trinv_workspace_bytes(...) */
   TRINV_CUDA_ERROR = 4,           /* a CUDA launch or API call failed; see trinv_last_cuda_error() */
-  TRINV_NOT_SUPPORTED = 5         /* request outside the implemented envelope (e.g. batched n > 64) */
+  TRINV_NOT_SUPPORTED = 5         /* request outside the implemented envelope (e.g. batched n > 128) */
 } trinv_status_t;
 
 typedef enum { TRINV_NON_UNIT = 0, TRINV_UNIT = 1 } trinv_diag_t;
@@ -88,9 +88,11 @@ trinv_status_t trinv_upper(int64_t n, const double* A, int64_t lda, double* X, i
 
 /* Batched small inverses: for b in [0, batch): X_b = T_b^{-1}, T_b at
  * A + b*strideA (leading dim lda), X_b at X + b*strideX (leading dim ldx).
- * uplo 'L' or 'U'; 1 <= n <= 64 (TRINV_NOT_SUPPORTED above).  Lane j computes
+ * uplo 'L' or 'U'; 1 <= n <= 128 (TRINV_NOT_SUPPORTED above).  Lane j computes
  * column j by the recurrence of P:243 (CRIT for the upper case) in
- * registers, one warp per matrix for n <= 32 (two for n <= 64).  For n = 32
+ * registers, one warp per matrix for n <= 32.  Orders 33..128 run one CTA per
+ * matrix: 32-wide leaves by that recurrence, then the beta = 2 merges of
+ * Alg. 1 on the FP64 tensor cores from shared memory.  For n = 32
  * with even lda/ldx/strides and 16-byte aligned pointers the referenced
  * triangle is staged in shared memory by 2-D TMA (cp.async.bulk.tensor);
  * other layouts use plain coalesced loads.
@@ -112,7 +114,7 @@ trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* 
  * enqueues; when `stream` reaches the work enqueued by this call, every X_host
  * row is written.  X_host may equal A_host.  ws_bytes >=
  * trinv_batched_host_workspace_bytes(n, chunk); d_info as for trinv_batched
- * (device int32[batch] or NULL).  n <= 64. */
+ * (device int32[batch] or NULL).  n <= 128. */
 #define TRINV_HOST_SLOTS 4
 size_t trinv_batched_host_workspace_bytes(int64_t n, int64_t chunk);
 trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const double* A_host, double* X_host,

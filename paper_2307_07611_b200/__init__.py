@@ -8,7 +8,7 @@ PyTorch fallback — if libtrinv.so is missing or no GPU is present the calls ra
 
     X = trinv_lower(L)            # L^{-1}, full matrix, +0.0 above the diagonal
     X = trinv_upper(U)            # U^{-1}
-    X = trinv_batched(A, "L")     # A: [B, n, n] on the device, n <= 64
+    X = trinv_batched(A, "L")     # A: [B, n, n] on the device, n <= 128
     X = trinv_batched_host(Ah)    # Ah: host [B, n, n]; pipelined H2D / invert / D2H
     X = inv_from_lu(L, U)         # (L U)^{-1} = U^{-1} L^{-1}, L unit by default
 """
@@ -112,7 +112,7 @@ def trinv_upper(A, *, unit=False, out=None, check=False, stream=None):
 
 
 def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None):
-    """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 64.  Returns X, or (X, info[B]) if info."""
+    """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 128.  Returns X, or (X, info[B]) if info."""
     torch = _torch()
     if A.dim() != 3 or A.shape[1] != A.shape[2]:
         raise ValueError("expected [B, n, n]")

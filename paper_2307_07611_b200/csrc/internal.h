@@ -53,6 +53,11 @@ struct LeafArgs {
 // taken when every address and size it moves is 16-byte aligned.
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches);
 
+// ---- whole-block inverses of order <= BLK_MAX, one CTA per block (blk.cu) --------
+// Same LeafArgs contract (any ld / alignment; X == A allowed); a.n, a.n_last <= BLK_MAX.
+constexpr int BLK_MAX = 128;
+cudaError_t launch_blk(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches);
+
 // ---- DMMA GEMM engine (gemm.cu) ---------------------------------------------------
 enum GemmMode : int {
   MODE_LOWER_1 = 0,  // W   = C . A^{-1}          (C from input, A^{-1} lower from X)

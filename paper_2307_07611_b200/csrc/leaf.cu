@@ -257,113 +257,6 @@ __global__ void __launch_bounds__(128) leaf_plain_kernel(const LeafArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// 64-wide leaves (n <= 64): two warps per matrix, lane = column.  For the lower
-// case warp 0 owns columns 0-31 over all 64 rows (64 registers of x) and warp 1
-// owns columns 32-63, whose entries above row 32 are structurally zero, so it
-// only runs the 32 steps of the bottom-right block; the upper case mirrors this.
-// Used for single matrices of order <= 64 (one launch, BASELINE config 0) and
-// batched orders 33..64.
-constexpr int L64 = 64;
-
-// x holds rows R0 .. R0+R-1 of column j; steps k over the same rows.
-template <bool UPPER, int R, int R0>
-__device__ __forceinline__ void solve_cols64(const double* T, const double* rr, int n, int j, double (&x)[R]) {
-#pragma unroll
-  for (int i = 0; i < R; ++i) x[i] = (R0 + i == j) ? 1.0 : 0.0;
-  if (!UPPER) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      if (R0 + k < n) {
-        const double xk = x[k] * rr[R0 + k];
-        x[k] = xk;
-#pragma unroll
-        for (int i = k + 1; i < R; ++i) x[i] = fma(-T[(R0 + i) * L64 + R0 + k], xk, x[i]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int k = R - 1; k >= 0; --k) {
-      if (R0 + k < n) {
-        const double xk = x[k] * rr[R0 + k];
-        x[k] = xk;
-#pragma unroll
-        for (int i = 0; i < k; ++i) x[i] = fma(-T[(R0 + i) * L64 + R0 + k], xk, x[i]);
-      }
-    }
-  }
-}
-
-template <bool UPPER, int R, int R0>
-__device__ __forceinline__ void store_cols64(double* dst, int64_t ldx, int n, int j, const double (&x)[R]) {
-  if (j >= n) return;
-#pragma unroll
-  for (int i = 0; i < L64; ++i) {
-    if (i < n) {
-      const bool held = i >= R0 && i < R0 + R;
-      const bool zero = UPPER ? (i > j) : (i < j);
-      double v = 0.0;
-      if (held && !zero) v = x[held ? i - R0 : 0];
-      dst[(int64_t)i * ldx + j] = v;
-    }
-  }
-}
-
-template <bool UPPER>
-__global__ void __launch_bounds__(64) leaf64_kernel(const LeafArgs a) {
-  __shared__ double T[L64 * L64];
-  __shared__ double rr[L64];
-  __shared__ int zmin[1];
-  const int half = 0;
-  const int t = threadIdx.x;                // thread within the matrix
-  const int w = t >> 5, lane = t & 31;      // warp within the matrix
-  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
-    const bool live = true;
-    const int nb = (b == a.batch - 1) ? a.n_last : a.n;
-    if (t == 0) zmin[half] = 1 << 30;
-    const double* src = a.A + b * a.sA;
-    for (int e = t; e < nb * nb; e += 64) {
-      const int i = e / nb, c = e - i * nb;
-      T[i * L64 + c] = src[(int64_t)i * a.lda + c];
-    }
-    __syncthreads();
-    if (t < nb) {
-      const double d = T[t * L64 + t];
-      if (!a.unit && d == 0.0) atomicMin(&zmin[half], t);
-      rr[t] = a.unit ? 1.0 : 1.0 / d;
-    }
-    __syncthreads();
-    if (live) {
-      const int j = w * 32 + lane;
-      double* dst = a.X + b * a.sX;
-      const bool big = UPPER ? (w == 1) : (w == 0);  // the warp that needs all 64 rows
-      if (big) {
-        double x[64];
-        solve_cols64<UPPER, 64, 0>(T, rr, nb, j, x);
-        store_cols64<UPPER, 64, 0>(dst, a.ldx, nb, j, x);
-      } else {
-        double x[32];
-        if (!UPPER) {
-          solve_cols64<false, 32, 32>(T, rr, nb, j, x);
-          store_cols64<false, 32, 32>(dst, a.ldx, nb, j, x);
-        } else {
-          solve_cols64<true, 32, 0>(T, rr, nb, j, x);
-          store_cols64<true, 32, 0>(dst, a.ldx, nb, j, x);
-        }
-      }
-      if (t == 0) {
-        const int z = zmin[half];
-        const bool singular = z < nb;
-        if (a.info_mode == 1) a.info[b] = singular ? z + 1 : 0;
-        else if (a.info_mode == 2 && singular)
-          info_min_nonzero(a.info, static_cast<int32_t>(a.info_off + b * a.info_stride + z + 1));
-      }
-    }
-    __syncthreads();
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -398,15 +291,9 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
                     (a.sA % 2 == 0) && (a.sX % 2 == 0);
   const bool tma = even && aligned16(a.A) && aligned16(a.X);
   // algorithmic work: n^3/3 flops and the referenced triangle in + full matrix out per matrix
+  if (a.n > LEAF || a.n_last > LEAF) return launch_blk(uplo, a, s, launches);  // 33..128: one CTA per matrix
   const double nn = (double)a.n;
   ProfileScope prof(KIND_LEAF, a.batch * nn * nn * nn / 3.0, a.batch * (nn * (nn + 1) / 2 + nn * nn) * 8.0, s);
-  if (a.n > LEAF || a.n_last > LEAF) {  // 33..64: two warps per matrix
-    const int grid = (int)(a.batch < (int64_t)sms * 6 ? a.batch : (int64_t)sms * 6);
-    if (uplo == 'L') leaf64_kernel<false><<<grid, 64, 0, s>>>(a);
-    else leaf64_kernel<true><<<grid, 64, 0, s>>>(a);
-    if (launches) ++*launches;
-    return cudaGetLastError();
-  }
   const bool full32 = a.n == LEAF && a.n_last == LEAF;
   // n = 32, TMA-compatible layout: 8 warps x 3 slots per CTA (one CTA per SM) measured best on B200
   // (profiles/r01_leaf_variants.txt).

@@ -2,8 +2,9 @@
 // planner (§Boundary).
 //
 // trinv_lower / trinv_upper run COMBRIT with beta = 2 (Alg. 1)
-// bottom-up: all 32-wide diagonal leaves in one launch ("any
-// preferred method"), then for b = 32, 64, ... < n one level of
+// bottom-up: all 128-wide diagonal blocks in one launch (blk.cu: 32-wide
+// leaves, "any preferred method", and the levels b = 32,
+// 64 inside each CTA), then for b = 128, 256, ... < n one level of
 // merges [s, s+b) + [s+b, s+2b) (the last one ragged, C13) with two grouped
 // DMMA launches per level (launch_level, gemm.cu).  inv_from_lu adds the
 // U^{-1} L^{-1} product.  Nothing here allocates device memory or
@@ -114,7 +115,7 @@ static size_t w_bytes(int64_t n) {
 static size_t mat_bytes(int64_t n) { return (size_t)n * (size_t)even_up(n) * sizeof(double); }
 
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
-  if (n <= 64) return 0;  // a single leaf: no products, any layout
+  if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
   size_t bytes = align_up(w_bytes(n));
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
@@ -145,33 +146,41 @@ static trinv_status_t cuda_fail(cudaError_t e) {
 static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
                               int unit, double* W, int32_t* info, int64_t info_off, cudaStream_t s,
                               int64_t b_stop = 0) {
-  if (n <= 64 && b_stop == 0) {  // one leaf of order n (BASELINE config 0): a single launch
+  if (n <= BLK_MAX && b_stop == 0) {  // one block of order n (BASELINE config 0): a single launch
     LeafArgs l1{};
     l1.A = A; l1.lda = lda; l1.sA = n * lda; l1.X = X; l1.ldx = ldx; l1.sX = n * ldx;
     l1.batch = 1; l1.n = (int)n; l1.n_last = (int)n; l1.unit = unit;
     l1.info = info; l1.info_mode = info ? 2 : 0; l1.info_stride = 0; l1.info_off = info_off;
     return cuda_fail(launch_leaf(uplo, l1, s, &g_launches));
   }
-  // (a1, a2) leaves: the n/32 full diagonal 32-blocks, then the ragged last one.
-  const int64_t full = n / 32, tail = n % 32;
+  // (a1, a2) diagonal blocks: 128-wide blocks inverted whole in one CTA each (blk.cu:
+  // leaves + the levels b = 32, 64 in shared memory), the last one ragged; or, when
+  // the caller stops the recursion below 128 (beta = 4 top level), 32-wide leaves.
+  const int64_t bw = (b_stop == 0 || b_stop >= BLK_MAX) ? BLK_MAX : 32;
+  const int64_t full = n / bw, tail = n % bw;
   LeafArgs la{};
-  la.A = A; la.lda = lda; la.sA = 32 * lda + 32;
-  la.X = X; la.ldx = ldx; la.sX = 32 * ldx + 32;
-  la.unit = unit; la.info = info; la.info_mode = info ? 2 : 0; la.info_stride = 32; la.info_off = info_off;
-  if (full > 0) {
-    la.batch = full; la.n = 32; la.n_last = 32;
-    TRY(launch_leaf(uplo, la, s, &g_launches));
-  }
-  if (tail > 0) {
-    LeafArgs lt = la;
-    lt.A = A + full * 32 * (lda + 1); lt.X = X + full * 32 * (ldx + 1);
-    lt.batch = 1; lt.n = (int)tail; lt.n_last = (int)tail;
-    lt.info_off = info_off + full * 32;
-    TRY(launch_leaf(uplo, lt, s, &g_launches));
+  la.A = A; la.lda = lda; la.sA = bw * lda + bw;
+  la.X = X; la.ldx = ldx; la.sX = bw * ldx + bw;
+  la.unit = unit; la.info = info; la.info_mode = info ? 2 : 0; la.info_stride = bw; la.info_off = info_off;
+  if (bw == BLK_MAX) {
+    la.batch = full + (tail > 0); la.n = (int)bw; la.n_last = (int)(tail > 0 ? tail : bw);
+    TRY(launch_blk(uplo, la, s, &g_launches));
+  } else {
+    if (full > 0) {
+      la.batch = full; la.n = 32; la.n_last = 32;
+      TRY(launch_leaf(uplo, la, s, &g_launches));
+    }
+    if (tail > 0) {
+      LeafArgs lt = la;
+      lt.A = A + full * 32 * (lda + 1); lt.X = X + full * 32 * (ldx + 1);
+      lt.batch = 1; lt.n = (int)tail; lt.n_last = (int)tail;
+      lt.info_off = info_off + full * 32;
+      TRY(launch_leaf(uplo, lt, s, &g_launches));
+    }
   }
   // (a4-a7) levels: two grouped DMMA launches per level.
   const int64_t b_end = b_stop > 0 ? b_stop : n;
-  for (int64_t b = 32; b < b_end && b < n; b *= 2) {
+  for (int64_t b = bw; b < b_end && b < n; b *= 2) {
     const int64_t merges = merges_at(n, b);
     const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, merges * b, b, b};
     LevelArgs l1{}, l2{};
@@ -211,7 +220,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   const size_t need = tri_ws(n, A, lda, X, ldx);
   if (ws_bytes < need || (need > 0 && ws == nullptr)) return TRINV_WORKSPACE_TOO_SMALL;
   if (init_info && info) TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
-  if (n <= 64) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
+  if (n <= BLK_MAX) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
 
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
@@ -456,7 +465,7 @@ trinv_status_t trinv_batched(char uplo, int64_t n, int64_t batch, const double* 
   if (n == 0 || batch == 0) return TRINV_OK;
   if (!A || !X || lda < n || ldx < n) return TRINV_INVALID_ARG;
   if (batch > 1 && (strideA < n * lda || strideX < n * ldx)) return TRINV_INVALID_ARG;
-  if (n > 64) return TRINV_NOT_SUPPORTED;
+  if (n > BLK_MAX) return TRINV_NOT_SUPPORTED;
   LeafArgs la{};
   la.A = A; la.lda = lda; la.sA = batch > 1 ? strideA : n * lda;
   la.X = X; la.ldx = ldx; la.sX = batch > 1 ? strideX : n * ldx;
@@ -479,7 +488,7 @@ trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const dou
   if (diag != TRINV_UNIT && diag != TRINV_NON_UNIT) return TRINV_INVALID_ARG;
   if (n == 0 || batch == 0) return TRINV_OK;
   if (!A_host || !X_host) return TRINV_INVALID_ARG;
-  if (n > 64) return TRINV_NOT_SUPPORTED;
+  if (n > BLK_MAX) return TRINV_NOT_SUPPORTED;
   chunk = host_chunk(chunk);
   const size_t slot_bytes = align_up((size_t)chunk * n * n * sizeof(double));
   if (!ws || ws_bytes < trinv_batched_host_workspace_bytes(n, chunk)) return TRINV_WORKSPACE_TOO_SMALL;

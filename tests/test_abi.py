@@ -37,7 +37,7 @@ def test_tri_argument_validation(fn):
     assert f(4, FAKE, 4, FAKE, 4, 0, None, 0, None, None) == _lib.TRINV_ALIASING
     over = ctypes.c_void_p((1 << 20) + 8 * 5)
     assert f(4, FAKE, 4, over, 4, 0, None, 0, None, None) == _lib.TRINV_ALIASING
-    assert f(100, FAKE, 100, FAKE2, 100, 0, None, 0, None, None) == _lib.TRINV_WORKSPACE_TOO_SMALL
+    assert f(200, FAKE, 200, FAKE2, 200, 0, None, 0, None, None) == _lib.TRINV_WORKSPACE_TOO_SMALL
 
 
 def test_batched_argument_validation():
@@ -45,7 +45,7 @@ def test_batched_argument_validation():
     assert f(b"L", 32, 0, None, 32, 1024, None, 32, 1024, 0, None, None) == _lib.TRINV_OK
     assert f(b"X", 32, 4, FAKE, 32, 1024, FAKE2, 32, 1024, 0, None, None) == _lib.TRINV_INVALID_ARG
     assert f(b"L", 32, 4, FAKE, 32, 1000, FAKE2, 32, 1024, 0, None, None) == _lib.TRINV_INVALID_ARG
-    assert f(b"L", 65, 4, FAKE, 65, 65 * 65, FAKE2, 65, 65 * 65, 0, None, None) == _lib.TRINV_NOT_SUPPORTED
+    assert f(b"L", 129, 4, FAKE, 129, 129 * 129, FAKE2, 129, 129 * 129, 0, None, None) == _lib.TRINV_NOT_SUPPORTED
 
 
 def test_inv_from_lu_argument_validation():

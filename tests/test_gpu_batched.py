@@ -35,7 +35,7 @@ def test_config1_full_batch():
     assert torch.equal(Ad.cpu(), torch.from_numpy(A))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 17, 30, 31, 32, 33, 40, 47, 63, 64])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 17, 30, 31, 32, 33, 40, 47, 63, 64, 65, 80, 96, 113, 127, 128])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_orders_and_uplo(n, uplo):
     B = 8 * 148 * 2 + 5 if n <= 32 else 6 * 148 + 3  # several matrices per warp / CTA, ragged tail
@@ -127,7 +127,7 @@ def test_singular_info_and_determinism():
 
 
 @pytest.mark.parametrize("uplo,n,B,chunk", [("L", 32, 20000, 0), ("U", 32, 9000, 1000), ("L", 17, 5000, 777),
-                                            ("L", 48, 3000, 512)])
+                                            ("L", 48, 3000, 512), ("U", 100, 700, 128)])
 def test_host_pipeline(uplo, n, B, chunk):
     """trinv_batched_host: host buffers, chunked H2D / invert / D2H pipeline (the e2e path)."""
     A = synth.host(n, batch=B, uplo=uplo, diag="signed" if uplo == "L" else "pos")
@@ -144,3 +144,44 @@ def test_host_pipeline(uplo, n, B, chunk):
     P.trinv_batched_host(Ap, uplo, out=Ap, chunk=chunk)
     torch.cuda.synchronize()
     assert torch.equal(Ap, X)
+
+
+@pytest.mark.parametrize("n", [33, 64, 65, 100, 128])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_block_kernel_exact_pins_and_info(n, uplo):
+    """Orders 33..128 (one CTA per matrix: 32-wide leaves + DMMA merges in shared memory):
+    bidiagonal closed form s^(i-j) (P-d), diagonal reciprocals bitwise (C4), integer
+    closure (Cor. 2, n <= 64), power-of-two scaling (P-g) and the zero-diagonal report."""
+    i, j = np.indices((n, n))
+    mats, want = [], []
+    for s in (0.5, -0.5, 1.0, -1.0, 2.0):
+        L = np.eye(n) - s * np.eye(n, k=-1)
+        mats.append(L)
+        want.append(np.where(i >= j, s ** (i - j).astype(float), 0.0))
+    rng = np.random.default_rng(n)
+    d = (1.0 + rng.random(n)) * rng.choice([-1.0, 1.0], n)
+    mats.append(np.diag(d))
+    want.append(np.diag(1.0 / d))
+    A = np.stack(mats)
+    if uplo == "U":
+        A = np.ascontiguousarray(np.transpose(A, (0, 2, 1)))
+        want = [w.T for w in want]
+    X, info = _run(A, uplo)
+    for b, w in enumerate(want):
+        assert np.array_equal(X[b], w), b
+    assert np.all(info == 0)
+    if n <= 64:  # every intermediate an integer below 2^53: exact in any summation order
+        Ai = np.tril(rng.integers(-1, 2, size=(16, n, n)), -1).astype(np.float64) + np.eye(n)
+        if uplo == "U":
+            Ai = np.ascontiguousarray(np.transpose(Ai, (0, 2, 1)))
+        Xi, _ = _run(Ai, uplo)
+        assert np.array_equal(Xi, oracle.crit_batched(Ai, uplo))
+    G = synth.host(n, batch=40, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    X1, _ = _run(G, uplo)
+    X8, _ = _run(G * 8.0, uplo)
+    assert np.array_equal(X8 * 8.0, X1)
+    G[3, n - 1, n - 1] = 0.0
+    G[5, 7, 7] = 0.0
+    G[5, n // 2, n // 2] = 0.0
+    _, info = _run(G, uplo)
+    assert info[3] == n and info[5] == 8 and info[0] == 0

@@ -140,11 +140,11 @@ trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const doubl
  * L_ij = A_ij - L_i,1:j-1 U_1:j-1,j, U_ij = (A_ij - L_i,1:i-1 U_1:i-1,j)/L_ii).
  * In place, packed: on return the lower triangle with the diagonal holds L and the
  * strict upper triangle holds U.  Blocked right-looking recursion: diagonal blocks
- * <= 64 in shared memory, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
+ * <= 128 in registers of one CTA, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
  * through the triangular inverses above and the DMMA engine, Schur complement on
  * the DMMA engine.  As in the paper there is no pivoting: the leading principal
  * minors must be non-zero; an exact zero pivot k sets d_info = 1 + k (output then
- * unspecified).  A: device, 16-byte aligned with even lda when n > 64
+ * unspecified).  A: device, 16-byte aligned with even lda when n > 128
  * (TRINV_NOT_SUPPORTED otherwise).  ws_bytes >= trinv_workspace_bytes('F', n, ...). */
 trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_bytes, int32_t* d_info,
                         void* stream);

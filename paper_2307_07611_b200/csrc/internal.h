@@ -107,7 +107,8 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 
-// ---- Crout factorisation of a diagonal block of order <= 64 (lu.cu) ----------
+// ---- Crout factorisation of a diagonal block of order <= LU_MAX (lu.cu) -------
+constexpr int LU_MAX = 128;
 cudaError_t launch_lu_leaf(double* A, int64_t lda, int n, int32_t* info, int64_t info_off, cudaStream_t s,
                            int64_t* launches);
 double gemm_flops(const GemmArgs& a);

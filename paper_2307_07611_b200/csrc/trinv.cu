@@ -335,7 +335,7 @@ static int64_t lu_split(int64_t n) { return 64 * ((n + 127) / 128); }
 // Scratch of lu_rec at order n: L11^{-1}, U11^{-1} (h x even(h)), their triangular
 // workspace, and one off-diagonal product buffer (h x even(n-h) or (n-h) x even(h)).
 static size_t lu_scratch(int64_t n) {
-  if (n <= 64) return 0;
+  if (n <= LU_MAX) return 0;
   const int64_t h = lu_split(n), r = n - h;
   size_t b = 2 * align_up(mat_bytes(h)) + align_up(tri_ws(h, nullptr, even_up(h), nullptr, even_up(h)));
   b += align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
@@ -344,7 +344,7 @@ static size_t lu_scratch(int64_t n) {
 
 static trinv_status_t lu_rec(int64_t n, double* A, int64_t lda, char* ws, int32_t* info, int64_t info_off,
                              cudaStream_t s) {
-  if (n <= 64) return cuda_fail(launch_lu_leaf(A, lda, (int)n, info, info_off, s, &g_launches));
+  if (n <= LU_MAX) return cuda_fail(launch_lu_leaf(A, lda, (int)n, info, info_off, s, &g_launches));
   const int64_t h = lu_split(n), r = n - h, ldh = even_up(h);
   double* A12 = A + h;
   double* A21 = A + h * lda;
@@ -651,7 +651,7 @@ trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_b
   if (n < 0) return TRINV_INVALID_ARG;
   if (n == 0) return TRINV_OK;
   if (!A || lda < n) return TRINV_INVALID_ARG;
-  if (n > 64 && !tma_ok(A, lda)) return TRINV_NOT_SUPPORTED;
+  if (n > LU_MAX && !tma_ok(A, lda)) return TRINV_NOT_SUPPORTED;
   const size_t need = align_up(lu_scratch(n));
   if (ws_bytes < need || (need > 0 && !ws)) return TRINV_WORKSPACE_TOO_SMALL;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));

@@ -60,7 +60,7 @@ def test_gemm_batched():
     assert np.max(np.abs(C - A @ B)) <= 1e-12 * K
 
 
-@pytest.mark.parametrize("n", [1, 3, 40, 64, 65, 100, 200, 513, 1000])
+@pytest.mark.parametrize("n", [1, 3, 40, 64, 65, 100, 128, 129, 200, 513, 1000])
 def test_lu_crout_vs_skul(n):
     Lg = synth.host(n, seed=n, tag="L", diag="pos")
     Ug = synth.host(n, seed=n, tag="U", uplo="U", diag="one")
@@ -72,7 +72,7 @@ def test_lu_crout_vs_skul(n):
     assert oracle.floored_rel_err(np.triu(LU, 1) + np.eye(n), U) <= REL_TOL
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 64, 65, 127, 300, 1000, 1500])
+@pytest.mark.parametrize("n", [1, 2, 5, 64, 65, 127, 128, 129, 300, 1000, 1500])
 def test_inv_general_full(n):
     Lg = synth.host(n, seed=2 * n, tag="L", diag="pos")
     Ug = synth.host(n, seed=2 * n, tag="U", uplo="U", diag="one")

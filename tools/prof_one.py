@@ -28,6 +28,14 @@ def main():
         synth.device_fill(U, n, uplo="U", diag="pos", tag="U")
         X = torch.empty_like(L)
         fn = lambda: P.inv_from_lu(L, U, unit_l=True, out=X)  # noqa: E731
+    elif op == "A":
+        L = torch.empty((n, n), dtype=torch.float64, device=dev)
+        U = torch.empty_like(L)
+        synth.device_fill(L, n, uplo="L", diag="one", tag="L")
+        synth.device_fill(U, n, uplo="U", diag="pos", tag="U")
+        A = L @ U
+        X = torch.empty_like(A)
+        fn = lambda: P.inv_general(A, out=X)  # noqa: E731
     else:
         raise SystemExit(f"unknown op {op}")
     for _ in range(reps):

@@ -53,6 +53,11 @@ struct LeafArgs {
 // taken when every address and size it moves is 16-byte aligned.
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches);
 
+// ---- batched 64 x 64, one warp per matrix, TMA-staged triangle (leaf64.cu) -------
+// Taken for n == n_last == 64 with even ld / strides and 16-byte aligned pointers.
+bool leaf64_tma_ok(const LeafArgs& a);
+cudaError_t launch_leaf64_tma(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches);
+
 // ---- whole-block inverses of order <= BLK_MAX, one CTA per block (blk.cu) --------
 // Same LeafArgs contract (any ld / alignment; X == A allowed); a.n, a.n_last <= BLK_MAX.
 constexpr int BLK_MAX = 128;

@@ -291,7 +291,10 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
                     (a.sA % 2 == 0) && (a.sX % 2 == 0);
   const bool tma = even && aligned16(a.A) && aligned16(a.X);
   // algorithmic work: n^3/3 flops and the referenced triangle in + full matrix out per matrix
-  if (a.n > LEAF || a.n_last > LEAF) return launch_blk(uplo, a, s, launches);  // 33..128: one CTA per matrix
+  if (a.n > LEAF || a.n_last > LEAF) {
+    if (leaf64_tma_ok(a)) return launch_leaf64_tma(uplo, a, s, launches);  // 64: one warp per matrix
+    return launch_blk(uplo, a, s, launches);                                // 33..128: one CTA per matrix
+  }
   const double nn = (double)a.n;
   ProfileScope prof(KIND_LEAF, a.batch * nn * nn * nn / 3.0, a.batch * (nn * (nn + 1) / 2 + nn * nn) * 8.0, s);
   const bool full32 = a.n == LEAF && a.n_last == LEAF;

@@ -39,7 +39,8 @@ BATCH = 131072
 CONFIGS = {
     0: dict(workload="config0: single fp64 lower n=64, seed 0", kind="L", n=64, diag="signed"),
     1: dict(workload="config1: batch 131072 x fp64 lower 32x32, seed b per matrix", kind="B", n=32),
-    2: dict(workload="config2: single fp64 lower n=8192, 32-wide leaves", kind="L", n=8192, diag="signed"),
+    2: dict(workload="config2: single fp64 lower n=8192 (128-wide diagonal blocks: 16-wide leaves + in-CTA "
+                     "DMMA merges, then beta=2 levels b=128..4096)", kind="L", n=8192, diag="signed"),
     3: dict(workload="config3: single fp64 upper n=32768", kind="U", n=32768, diag="pos"),
     4: dict(workload="config4: inv_from_lu n=16384, L unit", kind="G", n=16384),
     5: dict(workload="NEXT f2: general fp64 inverse from A, n=16384 (A = L U with U unit; Crout LU without "

@@ -114,8 +114,9 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 
 // ---- Crout factorisation of a diagonal block of order <= LU_MAX (lu.cu) -------
 constexpr int LU_MAX = 128;
-cudaError_t launch_lu_leaf(double* A, int64_t lda, int n, int32_t* info, int64_t info_off, cudaStream_t s,
-                           int64_t* launches);
+// Reads the block from W (ldw), writes the packed factors to F (ldf); F may equal W.
+cudaError_t launch_lu_leaf(const double* W, int64_t ldw, double* F, int64_t ldf, int n, int32_t* info,
+                           int64_t info_off, cudaStream_t s, int64_t* launches);
 double gemm_flops(const GemmArgs& a);
 cudaError_t launch_geam(int64_t rows, int64_t cols, double alpha, const double* A, int64_t lda, double beta,
                         const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s, int64_t* launches);

@@ -342,14 +342,18 @@ static size_t lu_scratch(int64_t n) {
   return std::max(b, lu_scratch(r));
 }
 
-static trinv_status_t lu_rec(int64_t n, double* A, int64_t lda, char* ws, int32_t* info, int64_t info_off,
-                             cudaStream_t s) {
-  if (n <= LU_MAX) return cuda_fail(launch_lu_leaf(A, lda, (int)n, info, info_off, s, &g_launches));
+// Factors the working matrix W (destroyed: it carries the Schur complements) into the
+// packed factors F (lower triangle with diagonal = L, strict upper = U).  F may be W
+// itself (lu_crout, in place): the off-diagonal blocks then go through the scratch T
+// and a copy; with F != W (inv_general) the products are written straight into F.
+static trinv_status_t lu_rec(int64_t n, double* W, int64_t ldw, double* F, int64_t ldf, char* ws, int32_t* info,
+                             int64_t info_off, cudaStream_t s) {
+  if (n <= LU_MAX) return cuda_fail(launch_lu_leaf(W, ldw, F, ldf, (int)n, info, info_off, s, &g_launches));
   const int64_t h = lu_split(n), r = n - h, ldh = even_up(h);
-  double* A12 = A + h;
-  double* A21 = A + h * lda;
-  double* A22 = A21 + h;
-  trinv_status_t st = lu_rec(h, A, lda, ws, info, info_off, s);  // A11 = L11 U11
+  const bool inplace = (F == W);
+  double *W12 = W + h, *W21 = W + h * ldw, *W22 = W21 + h;
+  double *F12 = F + h, *F21 = F + h * ldf, *F22 = F21 + h;
+  trinv_status_t st = lu_rec(h, W, ldw, F, ldf, ws, info, info_off, s);  // A11 = L11 U11
   if (st != TRINV_OK) return st;
   char* p = ws;
   double* Li = reinterpret_cast<double*>(p); p += align_up(mat_bytes(h));
@@ -357,32 +361,34 @@ static trinv_status_t lu_rec(int64_t n, double* A, int64_t lda, char* ws, int32_
   double* tws = reinterpret_cast<double*>(p); p += align_up(tri_ws(h, nullptr, ldh, nullptr, ldh));
   double* T = reinterpret_cast<double*>(p);
   // L11^{-1} (lower, diagonal kept) and U11^{-1} (unit upper) by the recursive split
-  st = run_tri('L', h, A, lda, Li, ldh, 0, tws, nullptr, 0, s);
+  st = run_tri('L', h, F, ldf, Li, ldh, 0, tws, nullptr, 0, s);
   if (st != TRINV_OK) return st;
-  st = run_tri('U', h, A, lda, Ui, ldh, 1, tws, nullptr, 0, s);
+  st = run_tri('U', h, F, ldf, Ui, ldh, 1, tws, nullptr, 0, s);
   if (st != TRINV_OK) return st;
   // U12 = L11^{-1} A12  (h x r; L11^{-1} lower: K-range k <= row)
   const int64_t ldr = even_up(r);
   GemmArgs g{};
   g.M = h; g.N = r; g.K = h; g.batch = 1;
-  g.A = Li; g.lda = ldh; g.B = A12; g.ldb = lda; g.C = T; g.ldc = ldr;
+  g.A = Li; g.lda = ldh; g.B = W12; g.ldb = ldw;
+  g.C = inplace ? T : F12; g.ldc = inplace ? ldr : ldf;
   g.alpha = 1.0; g.beta = 0.0; g.triA = TRI_LOWER; g.triB = TRI_NONE;
   TRY(launch_gemm(g, s, &g_launches));
-  TRY(cudaMemcpy2DAsync(A12, lda * 8, T, ldr * 8, r * 8, h, cudaMemcpyDeviceToDevice, s));
+  if (inplace) TRY(cudaMemcpy2DAsync(F12, ldf * 8, T, ldr * 8, r * 8, h, cudaMemcpyDeviceToDevice, s));
   // L21 = A21 U11^{-1}  (r x h; U11^{-1} upper: K-range k <= column)
   GemmArgs g2{};
   g2.M = r; g2.N = h; g2.K = h; g2.batch = 1;
-  g2.A = A21; g2.lda = lda; g2.B = Ui; g2.ldb = ldh; g2.C = T; g2.ldc = ldh;
+  g2.A = W21; g2.lda = ldw; g2.B = Ui; g2.ldb = ldh;
+  g2.C = inplace ? T : F21; g2.ldc = inplace ? ldh : ldf;
   g2.alpha = 1.0; g2.beta = 0.0; g2.triA = TRI_NONE; g2.triB = TRI_UPPER;
   TRY(launch_gemm(g2, s, &g_launches));
-  TRY(cudaMemcpy2DAsync(A21, lda * 8, T, ldh * 8, h * 8, r, cudaMemcpyDeviceToDevice, s));
-  // Schur complement A22 <- A22 - L21 U12
+  if (inplace) TRY(cudaMemcpy2DAsync(F21, ldf * 8, T, ldh * 8, h * 8, r, cudaMemcpyDeviceToDevice, s));
+  // Schur complement W22 <- A22 - L21 U12
   GemmArgs g3{};
   g3.M = r; g3.N = r; g3.K = h; g3.batch = 1;
-  g3.A = A21; g3.lda = lda; g3.B = A12; g3.ldb = lda; g3.C = A22; g3.ldc = lda;
+  g3.A = F21; g3.lda = ldf; g3.B = F12; g3.ldb = ldf; g3.C = W22; g3.ldc = ldw;
   g3.alpha = -1.0; g3.beta = 1.0; g3.triA = TRI_NONE; g3.triB = TRI_NONE;
   TRY(launch_gemm(g3, s, &g_launches));
-  return lu_rec(r, A22, lda, ws, info, info_off + h, s);
+  return lu_rec(r, W22, ldw, F22, ldf, ws, info, info_off + h, s);
 }
 static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu,
                                        double* X, int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU, void* ws,
@@ -430,9 +436,9 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
   if (n <= 0) return 0;
   if (op == 'L' || op == 'U') return tri_ws(n, A, lda, X, ldx);
   if (op == 'F') return align_up(lu_scratch(n));
-  if (op == 'A') {  // inv_general: packed LU copy + max(LU scratch, inv_from_lu workspace) + X staging
+  if (op == 'A') {  // inv_general: packed factors + max(working copy + LU scratch, inv_from_lu workspace) + X staging
     const size_t g = 2 * align_up(mat_bytes(n)) + align_up(tri_ws(n, nullptr, even_up(n), nullptr, even_up(n)));
-    size_t bytes = align_up(mat_bytes(n)) + std::max(align_up(lu_scratch(n)), g);
+    size_t bytes = align_up(mat_bytes(n)) + std::max(align_up(mat_bytes(n)) + align_up(lu_scratch(n)), g);
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
     (void)A; (void)lda;
     return bytes;
@@ -655,7 +661,7 @@ trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_b
   const size_t need = align_up(lu_scratch(n));
   if (ws_bytes < need || (need > 0 && !ws)) return TRINV_WORKSPACE_TOO_SMALL;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
-  return lu_rec(n, A, lda, static_cast<char*>(ws), d_info, 0, s);
+  return lu_rec(n, A, lda, A, lda, static_cast<char*>(ws), d_info, 0, s);
 }
 
 trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx, void* ws,
@@ -668,15 +674,18 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
   if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
   const int64_t lde = even_up(n);
+  // workspace: [F: packed factors | W: working copy of A + LU scratch], the second part
+  // reused as the inv_from_lu workspace once the factorisation is done (stream order)
   char* p = static_cast<char*>(ws);
-  double* LU = reinterpret_cast<double*>(p);
+  double* F = reinterpret_cast<double*>(p);
   p += align_up(mat_bytes(n));
+  double* Wk = reinterpret_cast<double*>(p);
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
-  TRY(cudaMemcpy2DAsync(LU, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
-  trinv_status_t st = lu_rec(n, LU, lde, p, d_info, 0, s);  // A = L U, U unit (Crout)
+  TRY(cudaMemcpy2DAsync(Wk, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  trinv_status_t st = lu_rec(n, Wk, lde, F, lde, p + align_up(mat_bytes(n)), d_info, 0, s);  // A = L U
   if (st != TRINV_OK) return st;
-  // A^{-1} = U^{-1} L^{-1} from the packed factors (the scratch is reused, stream-ordered)
-  return inv_from_lu_core(n, LU, lde, LU, lde, X, ldx, TRINV_NON_UNIT, TRINV_UNIT, p,
+  // A^{-1} = U^{-1} L^{-1} from the packed factors
+  return inv_from_lu_core(n, F, lde, F, lde, X, ldx, TRINV_NON_UNIT, TRINV_UNIT, p,
                           ws_bytes - align_up(mat_bytes(n)), d_info, false, s);
 }
 

@@ -185,3 +185,34 @@ def test_block_kernel_exact_pins_and_info(n, uplo):
     G[5, n // 2, n // 2] = 0.0
     _, info = _run(G, uplo)
     assert info[3] == n and info[5] == 8 and info[0] == 0
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_batched64_tma_path(uplo):
+    """n = 64 with a batch that fills the machine (>= 4096): the one-warp-per-matrix kernel
+    with TMA-staged row bands (leaf64_tma_kernel); ragged count, zero-diagonal report,
+    unit diagonal with a poisoned unreferenced triangle, and the same bits as the
+    one-CTA-per-matrix path on a sub-batch below the threshold (P-l)."""
+    n, B = 64, 5003
+    A = synth.host(n, batch=B, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    A[17, 40, 40] = 0.0
+    A[4000, 3, 3] = 0.0
+    A[4000, 60, 60] = 0.0
+    X, info = _run(A, uplo)
+    ok = np.ones(B, bool); ok[[17, 4000]] = False
+    R = oracle.crit_batched(A[ok], uplo)
+    assert oracle.floored_rel_err(X[ok], R) <= REL_TOL
+    assert oracle.residual_ratio(A[ok][:256], X[ok][:256]) <= RES_TOL
+    assert info[17] == 41 and info[4000] == 4 and np.count_nonzero(info) == 2
+    opp = np.triu(X[ok], 1) if uplo == "L" else np.tril(X[ok], -1)
+    assert np.all(opp == 0.0)
+    # unit diagonal: neither the diagonal nor the other triangle is read
+    Au = A.copy()
+    idx = np.arange(n)
+    Au[:, idx, idx] = np.nan
+    tri = np.triu_indices(n, 1) if uplo == "L" else np.tril_indices(n, -1)
+    Au[:, tri[0], tri[1]] = np.nan
+    Xu, _ = _run(Au, uplo, unit=True)
+    A1 = A.copy(); A1[:, idx, idx] = 1.0
+    assert oracle.floored_rel_err(Xu[:300], oracle.crit_batched(A1[:300], uplo, unit=True)) <= REL_TOL
+    assert not np.isnan(Xu).any()

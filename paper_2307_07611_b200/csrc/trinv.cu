@@ -390,6 +390,60 @@ static trinv_status_t lu_rec(int64_t n, double* W, int64_t ldw, double* F, int64
   TRY(launch_gemm(g3, s, &g_launches));
   return lu_rec(r, W22, ldw, F22, ldf, ws, info, info_off + h, s);
 }
+// SKUL-style blocked recursion (the inverse factors computed alongside the factors, as
+// SKUL does element-wise, "S K = A^{-1}"): W (working copy, destroyed) is
+// factored into the packed F, and K = L^{-1} (Li, lower, diagonal kept) and S = U^{-1}
+// (Ui, unit upper) are assembled from the children's inverse factors by the merge of
+// the recursive split (COMBRIT beta = 2):
+//   K = [K11 0; -K22 (L21 K11)  K22],   S = [S11  -(S11 U12) S22; 0 S22].
+// The diagonal-block inverses computed for the factorisation are thus reused, and no
+// separate triangular inversion of the full factors is needed.  All matrices share
+// the even leading dimension ld; T is the (h x r | r x h) product scratch.
+static size_t lu_inv_scratch(int64_t n) {
+  if (n <= LU_MAX) return 0;
+  const int64_t h = lu_split(n), r = n - h;
+  return align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
+}
+static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
+                                 int32_t* info, int64_t info_off, cudaStream_t s) {
+  if (n <= LU_MAX) {
+    TRY(launch_lu_leaf(W, ld, F, ld, (int)n, info, info_off, s, &g_launches));
+    trinv_status_t st = run_tri('L', n, F, ld, Li, ld, 0, nullptr, nullptr, 0, s);
+    if (st != TRINV_OK) return st;
+    return run_tri('U', n, F, ld, Ui, ld, 1, nullptr, nullptr, 0, s);
+  }
+  const int64_t h = lu_split(n), r = n - h;
+  auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
+  auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                  int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta) {
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K; g.batch = 1;
+    g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+    g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
+    return cuda_fail(launch_gemm(g, s, &g_launches));
+  };
+  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s);  // A11 = L11 U11, K11, S11
+  if (st != TRINV_OK) return st;
+  // U12 = K11 A12 (K11 lower), L21 = A21 S11 (S11 upper), Schur W22 <- A22 - L21 U12
+  if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0))) return st;
+  if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0))) return st;
+  if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0)))
+    return st;
+  st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s);
+  if (st != TRINV_OK) return st;
+  // K21 = -K22 (L21 K11)
+  const int64_t lth = even_up(h), ltr = even_up(r);
+  if ((st = gemm(r, h, h, blk(F, h, 0), ld, TRI_NONE, Li, ld, TRI_LOWER, T, lth, 1.0, 0.0))) return st;
+  if ((st = gemm(r, h, r, blk(Li, h, h), ld, TRI_LOWER, T, lth, TRI_NONE, blk(Li, h, 0), ld, -1.0, 0.0))) return st;
+  // S12 = -(S11 U12) S22
+  if ((st = gemm(h, r, h, Ui, ld, TRI_UPPER, blk(F, 0, h), ld, TRI_NONE, T, ltr, 1.0, 0.0))) return st;
+  if ((st = gemm(h, r, r, T, ltr, TRI_NONE, blk(Ui, h, h), ld, TRI_UPPER, blk(Ui, 0, h), ld, -1.0, 0.0))) return st;
+  // structural zeros of the opposite triangles (read densely by the diagonal tiles of S K)
+  TRY(launch_zero_2d(blk(Li, 0, h), ld, h, r, s, &g_launches));
+  TRY(launch_zero_2d(blk(Ui, h, 0), ld, r, h, s, &g_launches));
+  return TRINV_OK;
+}
+
 static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl, const double* Uf, int64_t ldu,
                                        double* X, int64_t ldx, trinv_diag_t diagL, trinv_diag_t diagU, void* ws,
                                        size_t ws_bytes, int32_t* d_info, bool init_info, cudaStream_t s) {
@@ -436,9 +490,8 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
   if (n <= 0) return 0;
   if (op == 'L' || op == 'U') return tri_ws(n, A, lda, X, ldx);
   if (op == 'F') return align_up(lu_scratch(n));
-  if (op == 'A') {  // inv_general: packed factors + max(working copy + LU scratch, inv_from_lu workspace) + X staging
-    const size_t g = 2 * align_up(mat_bytes(n)) + align_up(tri_ws(n, nullptr, even_up(n), nullptr, even_up(n)));
-    size_t bytes = align_up(mat_bytes(n)) + std::max(align_up(mat_bytes(n)) + align_up(lu_scratch(n)), g);
+  if (op == 'A') {  // inv_general: F, W, K, S (n x even(n) each), the product scratch, X staging
+    size_t bytes = 4 * align_up(mat_bytes(n)) + align_up(lu_inv_scratch(n));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
     (void)A; (void)lda;
     return bytes;
@@ -674,19 +727,30 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
   if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
   const int64_t lde = even_up(n);
-  // workspace: [F: packed factors | W: working copy of A + LU scratch], the second part
-  // reused as the inv_from_lu workspace once the factorisation is done (stream order)
+  // workspace: [F packed factors | W working copy of A | K = L^{-1} | S = U^{-1} | T | X staging]
   char* p = static_cast<char*>(ws);
-  double* F = reinterpret_cast<double*>(p);
-  p += align_up(mat_bytes(n));
-  double* Wk = reinterpret_cast<double*>(p);
+  auto take = [&](size_t bytes) { double* q = reinterpret_cast<double*>(p); p += align_up(bytes); return q; };
+  double* F = take(mat_bytes(n));
+  double* Wk = take(mat_bytes(n));
+  double* Li = take(mat_bytes(n));
+  double* Ui = take(mat_bytes(n));
+  double* T = take(lu_inv_scratch(n));
+  const bool stage_x = !tma_ok(X, ldx);
+  double* Xuse = stage_x ? take(mat_bytes(n)) : X;
+  const int64_t ldx_use = stage_x ? lde : ldx;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   TRY(cudaMemcpy2DAsync(Wk, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
-  trinv_status_t st = lu_rec(n, Wk, lde, F, lde, p + align_up(mat_bytes(n)), d_info, 0, s);  // A = L U
+  // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
+  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s);
   if (st != TRINV_OK) return st;
-  // A^{-1} = U^{-1} L^{-1} from the packed factors
-  return inv_from_lu_core(n, F, lde, F, lde, X, ldx, TRINV_NON_UNIT, TRINV_UNIT, p,
-                          ws_bytes - align_up(mat_bytes(n)), d_info, false, s);
+  // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
+  LevelArgs ul{};
+  ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
+  ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
+  ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
+  TRY(launch_level(ul, s, &g_launches));
+  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  return TRINV_OK;
 }
 
 const char* trinv_status_string(trinv_status_t st) {

@@ -25,9 +25,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 # full captures of the dominant kernels
 ncu --set full --clock-control none --import-source on -k regex:leaf32_tma -s 3 -c 1 -o gpurun_out/full_leaf32 $CMD1 > gpurun_out/ncu_f1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:blk_kernel -s 3 -c 1 -o gpurun_out/full_blk $CMD0 > gpurun_out/ncu_f0.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:dmma_level -s 12 -c 1 -o gpurun_out/full_dmma_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:dmma_level -s 10 -c 2 -o gpurun_out/full_dmma_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:leaf64_tma -c 1 -o gpurun_out/full_leaf64 python tools/sweep_batched.py 64 > gpurun_out/ncu_f64.log 2>&1
 for f in full_leaf32 full_blk full_dmma_c2 full_leaf64; do
   [ -f gpurun_out/$f.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$f.ncu-rep > gpurun_out/$f.txt 2>&1
 done
 ls -la gpurun_out >> gpurun_out/steps.log
+python tools/kprof.py A 16384 > gpurun_out/kprof_A16384.txt 2>&1
+python tools/kprof.py L 8192 > gpurun_out/kprof_L8192.txt 2>&1

@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(BlkCfg<NB>::THREADS) blk_kernel(const LeafArgs
     for (int e = tid; e < NB * NB / 2; e += T) {
       const int i = e / (NB / 2), k = 2 * (e % (NB / 2));
       if (i < nb && k < nb) {
-        const double v0 = X[i * S + k], v1 = X[i * S + k + 1];
+        const double2 v = *reinterpret_cast<const double2*>(X + i * S + k);
+        const double v0 = v.x, v1 = v.y;
         if (!UPPER) {
           double* q = dst + (int64_t)i * a.ldx + k;
           if (k + 1 < nb && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {

@@ -312,12 +312,16 @@ def main():
         flops_per_step = B * n ** 3 / 3
     else:
         if cfg["kind"] == "S":
-            from paper_2307_07611_b200.dist import trinv_split
+            from paper_2307_07611_b200.dist import trinv_split, trinv_split_p2p
+            # BENCH_SPLIT=p2p: the broadcast / gather fused into the kernels over peer memory
+            split = trinv_split_p2p if os.environ.get("BENCH_SPLIT") == "p2p" else trinv_split
+            cfg = dict(cfg, workload=cfg["workload"] + (" [peer-memory transport]" if split is trinv_split_p2p
+                                                        else " [process-group transport]"))
             A = torch.empty((n, n), dtype=torch.float64, device=dev)
             synth.device_fill(A, n, diag=cfg["diag"])  # replicated input on every rank
             X = torch.empty((n, n), dtype=torch.float64, device=dev)
             def step():
-                Y = trinv_split(A, "L")
+                Y = split(A, "L")
                 if Y is not None:
                     X.copy_(Y)
             flops_per_step = n ** 3 / 3

@@ -174,3 +174,65 @@ def trinv_split(T, uplo="L", group=None, dst=0, inv=None, gemm=None):
             else:
                 X[c0:c1, h:] = part[k][: c1 - c0, :]
     return X
+
+
+# ---------------------------------------------------------------------------
+# f1 with peer-memory transport: the broadcast and the gather of trinv_split
+# fused into the kernels.  `dst` owns X; every rank maps it through CUDA IPC
+# (NVLink peer memory on a multi-GPU node).  Phase 1 writes A^-1 and B^-1 straight
+# into X on `dst`; phase 3 reads them from there as TMA operands of the panel
+# products (P2P loads replace the broadcast) and the epilogue of the second product
+# stores each X21 panel straight into X on `dst` (P2P stores replace the gather).
+# The only collectives left are two barriers (phase ordering); no data moves
+# through NCCL.  Requires an even n and a device tensor T (TMA operand layout).
+def _share_from(t, src, group):
+    """A view of rank `src`'s CUDA tensor `t` on every rank (CUDA IPC handle via the process group)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    rank = dist.get_rank(group)
+    obj = [reduce_tensor(t) if rank == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    if rank == src:
+        return t
+    fn, args = obj[0]
+    return fn(*args)
+
+
+def trinv_split_p2p(T, uplo="L", group=None, dst=0):
+    """trinv_split with the data exchange done by the kernels over peer memory (see above)."""
+    from . import gemm as _gemm, trinv_lower, trinv_upper
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = T.shape[0]
+    h = _split_point(n)
+    if world == 1 or h >= n or n % 2:
+        return trinv_split(T, uplo, group=group, dst=dst)
+    r = n - h
+    inv = trinv_lower if uplo == "L" else trinv_upper
+    Xown = torch.zeros((n, n), dtype=T.dtype, device=T.device) if rank == dst else None
+    X = _share_from(Xown, dst, group)
+    src_b = min(1, world - 1)
+    # phase 1: diagonal-block inverses written straight into X on dst
+    if rank == 0:
+        inv(T[:h, :h], out=X[:h, :h])
+    if rank == src_b:
+        inv(T[h:, h:], out=X[h:, h:])
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+    # phase 3: 2G balanced panels; operands read from X on dst, results stored there
+    P = 2 * world
+    w = (h + P - 1) // P
+    w += w % 2
+    for p in panel_owner_map(world)[rank]:
+        c0, c1 = p * w, min(h, (p + 1) * w)
+        if c0 >= c1:
+            continue
+        if uplo == "L":
+            Wp = _gemm(T[h:, c0:h], X[c0:h, c0:c1], struct_b="L")             # C A^-1, k >= c0
+            _gemm(X[h:, h:], Wp, C=X[h:, c0:c1], alpha=-1.0, struct_a="L")    # -B^-1 W -> X on dst
+        else:
+            Wp = _gemm(X[c0:c1, c0:h], T[c0:h, h:], struct_a="U")             # A^-1 B12, k >= c0
+            _gemm(Wp, X[h:, h:], C=X[c0:c1, h:], alpha=-1.0, struct_b="U")    # -W C^-1 -> X on dst
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+    return Xown if rank == dst else None
+

@@ -22,17 +22,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, uplo, q):
+def _worker(rank, world, port, n, uplo, q, transport="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle
         import synth
-        from paper_2307_07611_b200.dist import trinv_split
+        from paper_2307_07611_b200.dist import trinv_split, trinv_split_p2p
         T = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
         synth.device_fill(T, n, seed=4, uplo=uplo, diag="signed" if uplo == "L" else "pos")
-        X = trinv_split(T, uplo)
+        X = trinv_split(T, uplo) if transport == "nccl" else trinv_split_p2p(T, uplo)
         torch.cuda.synchronize()
         if rank == 0:
             Th = T.cpu().numpy()
@@ -47,12 +47,16 @@ def _worker(rank, world, port, n, uplo, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,uplo", [(2, 1024, "L"), (2, 1500, "U"), (3, 2048, "L")])
-def test_split_two_ranks_one_gpu(world, n, uplo):
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("world,n,uplo", [(2, 1024, "L"), (2, 1500, "U"), (3, 2048, "L"), (3, 1000, "U")])
+def test_split_two_ranks_one_gpu(world, n, uplo, transport):
+    """transport "nccl": process-group broadcast + gather (gloo here); "p2p": the kernels
+    read A^-1 / B^-1 from and store the X21 panels into rank 0's X through CUDA IPC
+    (peer memory), with barriers only."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, uplo, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, uplo, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

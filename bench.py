@@ -70,6 +70,17 @@ def peaks():
     return hbm, src_h, fp64, src_f
 
 
+def _bf16_sustained():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["bf16_tflops_sustained"])
+    except Exception:
+        return 1363.9
+
+
+I8_PER_BF16_SUSTAINED = _bf16_sustained()  # TF/s; x 2 = int8 TOPS (nominal 4.5 POPS / 2.25 PF dense ratio)
+
+
 def ncu_traffic(kernel_key):
     """dram bytes (read+write) per launch from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -260,6 +271,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true", help="never replay steps from a CUDA graph")
+    ap.add_argument("--products", default="dmma", choices=["dmma", "int8"],
+                    help="engine for the level products: FP64 DMMA (default) or the INT8 tensor-core "
+                         "splitting engine (8 digits, levels with block size >= 8192)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -286,6 +300,9 @@ def main():
     stream = torch.cuda.current_stream()
     cfg = CONFIGS[args.config]
     hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
+    if args.products == "int8":
+        P.set_product_engine("int8")
+        cfg = dict(cfg, workload=cfg["workload"] + " [INT8 tensor-core products, 8 digits, blocks >= 8192]")
 
     def barrier():
         if world > 1:
@@ -431,14 +448,30 @@ def main():
             barrier()
         ms_d, n_d, fl_d, _ = P._lib.profile_read(1)
         ms_l, n_l, fl_l, _ = P._lib.profile_read(0)
+        ms_o, n_o, fl_o, ops_o = P._lib.profile_read(2)  # INT8 engine: FP64-equivalent flops, int8 ops
         P._lib.profile_end()
         achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
-        if n_d == 0:  # a single leaf launch (n <= 64): latency-bound, no tensor-core product
-            line["roofline"] = {"bound": "latency", "kernel": "leaf64_kernel (single launch)", "achieved": None,
+        if n_o > 0 and ms_o >= ms_d:  # the INT8 engine carries the dominant products
+            i8_peak = 2.0 * I8_PER_BF16_SUSTAINED
+            ach = ops_o / (ms_o / 1e3) / 1e12
+            line["roofline"] = {"bound": "tensor", "kernel": "oz_gemm_kernel (INT8 tcgen05, exact 8-digit splitting)",
+                                "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
+                                "traffic": None,
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8 / bf16)",
+                                "int8_share_of_step": ms_o / (args.steps * ms_per_step),
+                                "int8_fp64_equivalent_tflops": fl_o / (ms_o / 1e3) / 1e12,
+                                "dmma_part": {"achieved_tflops": achieved, "peak": fp64_peak,
+                                              "frac": achieved / fp64_peak,
+                                              "share_of_step": ms_d / (args.steps * ms_per_step)},
+                                "whole_step_tflops": flops_per_step / (ms_per_step / 1e3) / 1e12,
+                                "whole_step_frac_of_fp64_peak": flops_per_step / (ms_per_step / 1e3) / 1e12 / fp64_peak}
+        elif n_d == 0:  # a single block launch (n <= 128): latency-bound, no level products
+            line["roofline"] = {"bound": "latency", "kernel": "blk_kernel (single launch)", "achieved": None,
                                 "peak": None, "unit": None, "frac": None, "traffic": None,
                                 "leaf_us_per_launch": 1e3 * ms_l / max(n_l, 1),
-                                "note": "one 64x64 inverse per launch; bounded by launch latency and the "
-                                        "64-step dependent recurrence, not by HBM or the tensor pipe"}
+                                "note": "one 64x64 inverse per launch in one CTA; bounded by launch latency and "
+                                        "the dependent phases (load, leaves, two merge levels, store), not by HBM "
+                                        "or the tensor pipe"}
         else:
             line["roofline"] = {"bound": "tensor", "kernel": "dmma_level_kernel (all product launches)",
                               "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",

@@ -194,6 +194,30 @@ size_t trinv_strassen_workspace_bytes(int64_t n);
 trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                    int64_t ldc, void* ws, size_t ws_bytes, void* stream);
 
+/* Opt-in product engine (experiment): C = alpha A B + beta C in FP64
+ * with the products on the INT8 tensor cores (tcgen05 kind::i8) by exact operand
+ * splitting: rows of A / columns of B scaled by powers of two and cut into `digits`
+ * signed 7-bit digits; the digit pairs with t + u <= digits + 1 are multiplied exactly
+ * (int32) and summed in FP64 (error ~ K 2^(-7 digits) |row max| |column max|).
+ * Row-major device matrices; structA / structB as in trinv_gemm (one triangular
+ * operand at most).  Envelope: M % 128 == 0, N % 256 == 0, K % 128 == 0,
+ * digits * K * 127^2 < 2^31 (K <= 16384 at 8 digits), else TRINV_NOT_SUPPORTED.
+ * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, digits) bytes. */
+size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits);
+trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                             char structA, const double* B, int64_t ldb, char structB, double beta, double* C,
+                             int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream);
+
+/* Product engine for the level products of trinv_lower / trinv_upper (and the
+ * triangular inverses inside inv_from_lu / lu_crout): engine 0 = FP64 DMMA (default),
+ * 1 = the INT8 tensor-core engine above with `digits` digits, used for every level
+ * whose block size is >= min_block (>= 256) and whose shapes fit its envelope (other
+ * levels stay on DMMA).  Process-wide; also settable before the first call with the
+ * environment variable TRINV_PRODUCTS=int8.  Changing it changes
+ * trinv_workspace_bytes ('L', 'U', 'G', 'F'): query the workspace after setting it. */
+trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
+int trinv_get_product_engine(void);
+
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);
 

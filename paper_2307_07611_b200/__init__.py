@@ -19,7 +19,7 @@ from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMat
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
 __all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "inv_general",
-           "lu_crout", "gemm", "gemm_strassen", "trinv_beta", "workspace_bytes",
+           "lu_crout", "gemm", "gemm_oz", "gemm_strassen", "set_product_engine", "product_engine", "trinv_beta", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -195,6 +195,35 @@ def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", strea
                             ctypes.c_void_p(B.data_ptr()), ldb, sb, struct_b.encode(), float(beta),
                             ctypes.c_void_p(C.data_ptr()), ldc, sc, _stream(stream)))
     return C
+
+
+def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", digits=8, stream=None):
+    """C = alpha A B + beta C (FP64) with the products on the INT8 tensor cores by exact
+    operand splitting into `digits` 7-bit digits (opt-in engine, trinv_gemm_oz)."""
+    torch = _torch()
+    M, K = A.shape
+    N = B.shape[1]
+    if B.shape[0] != K:
+        raise ValueError("inner dimensions differ")
+    if C is None:
+        C = torch.zeros((M, N), dtype=torch.float64, device=A.device)
+    ws, wsb = _alloc_ws(lib().trinv_gemm_oz_workspace_bytes(M, N, K, digits), A.device)
+    _check(lib().trinv_gemm_oz(M, N, K, float(alpha), ctypes.c_void_p(A.data_ptr()), _ld(A), struct_a.encode(),
+                               ctypes.c_void_p(B.data_ptr()), _ld(B), struct_b.encode(), float(beta),
+                               ctypes.c_void_p(C.data_ptr()), _ld(C), digits,
+                               ctypes.c_void_p(ws.data_ptr()) if ws is not None else None, wsb, _stream(stream)))
+    return C
+
+
+def set_product_engine(engine="dmma", digits=8, min_block=8192):
+    """Level products on the FP64 DMMA engine ("dmma", default) or the INT8 tensor-core
+    splitting engine ("int8", `digits` 7-bit digits, levels with block size >= min_block)."""
+    e = {"dmma": 0, "int8": 1}[engine]
+    _check(lib().trinv_set_product_engine(e, digits, min_block))
+
+
+def product_engine():
+    return ["dmma", "int8"][lib().trinv_get_product_engine()]
 
 
 def gemm_strassen(A, B, *, C=None, stream=None):

@@ -70,6 +70,11 @@ def lib():
     sig("trinv_tri_ex", [ctypes.c_char, _i32, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp], _i32)
     sig("trinv_strassen_workspace_bytes", [_i64], _sz)
     sig("trinv_gemm_strassen", [_i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp], _i32)
+    sig("trinv_gemm_oz_workspace_bytes", [_i64, _i64, _i64, _i32], _sz)
+    sig("trinv_gemm_oz", [_i64, _i64, _i64, ctypes.c_double, _vp, _i64, ctypes.c_char, _vp, _i64, ctypes.c_char,
+                          ctypes.c_double, _vp, _i64, _i32, _vp, _sz, _vp], _i32)
+    sig("trinv_set_product_engine", [_i32, _i32, _i64], _i32)
+    sig("trinv_get_product_engine", None, _i32)
     sig("trinv_status_string", [_i32], ctypes.c_char_p)
     sig("trinv_last_cuda_error", None, _i32)
     sig("trinv_version", None, ctypes.c_char_p)

@@ -112,6 +112,13 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 
+// ---- FP64 products on the INT8 tensor cores by operand splitting (oz.cu) ----------
+bool oz_supported(int64_t M, int64_t N, int64_t K, int s);
+size_t oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int s);
+cudaError_t launch_oz_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                           int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, int s, void* ws,
+                           cudaStream_t st, int64_t* launches);
+
 // ---- Crout factorisation of a diagonal block of order <= LU_MAX (lu.cu) -------
 constexpr int LU_MAX = 128;
 // Reads the block from W (ldw), writes the packed factors to F (ldf); F may equal W.
@@ -132,7 +139,8 @@ bool encode_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* d
 
 // Optional per-launch timing (trinv_profile_* in include/trinv.h): when enabled on
 // this thread, every launch is bracketed by CUDA events on its stream.
-enum LaunchKind : int { KIND_LEAF = 0, KIND_DMMA = 1, KIND_COUNT = 2 };
+// KIND_OZ: INT8 tensor-core products (oz.cu); flops = FP64-equivalent, bytes = int8 ops.
+enum LaunchKind : int { KIND_LEAF = 0, KIND_DMMA = 1, KIND_OZ = 2, KIND_COUNT = 3 };
 struct ProfileScope {
   ProfileScope(int kind, double flops, double bytes, cudaStream_t s);
   ~ProfileScope();

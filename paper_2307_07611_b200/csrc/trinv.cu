@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -103,6 +105,22 @@ static bool tma_ok(const void* p, int64_t ld) { return p == nullptr ? (ld % 2 ==
 static int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// ---- opt-in product engine for the level products (trinv_set_product_engine) ------
+// 0: FP64 DMMA (default); 1: INT8 tensor cores by exact operand splitting (oz.cu) for
+// the levels whose block size is >= g_oz_min and whose shapes fit its envelope.
+static std::atomic<int> g_engine{-1};
+static std::atomic<int> g_digits{8};
+static std::atomic<int64_t> g_oz_min{8192};
+static int product_engine() {
+  int e = g_engine.load(std::memory_order_relaxed);
+  if (e < 0) {
+    const char* v = getenv("TRINV_PRODUCTS");
+    e = (v && strcmp(v, "int8") == 0) ? 1 : 0;
+    g_engine.store(e, std::memory_order_relaxed);
+  }
+  return e;
+}
+
 // Number of merges at level b: g with 2gb + b < n.
 static int64_t merges_at(int64_t n, int64_t b) { return (n - b + 2 * b - 1) / (2 * b); }
 
@@ -114,9 +132,39 @@ static size_t w_bytes(int64_t n) {
 }
 static size_t mat_bytes(int64_t n) { return (size_t)n * (size_t)even_up(n) * sizeof(double); }
 
+// INT8 engine: a level takes it when every merge's two products fit the envelope
+// (lower: r x b x b and r x b x r; upper: b x r x b and b x r x r); its scratch is the
+// largest of those products' workspaces.
+static bool oz_level_ok(int64_t n, int64_t b) {
+  if (product_engine() != 1 || b < g_oz_min.load() || b % 256) return false;
+  const int dg = g_digits.load();
+  for (int64_t s = 0; s + b < n; s += 2 * b) {
+    const int64_t r = std::min(b, n - s - b);
+    if (r % 256 || !oz_supported(r, b, b, dg) || !oz_supported(r, b, r, dg) || !oz_supported(b, r, b, dg) ||
+        !oz_supported(b, r, r, dg))
+      return false;
+  }
+  return true;
+}
+static size_t oz_scratch(int64_t n) {
+  if (product_engine() != 1 || n <= BLK_MAX) return 0;
+  const int dg = g_digits.load();
+  size_t best = 0;
+  for (int64_t b = BLK_MAX; b < n; b *= 2) {
+    if (!oz_level_ok(n, b)) continue;
+    for (int64_t s = 0; s + b < n; s += 2 * b) {
+      const int64_t r = std::min(b, n - s - b);
+      for (size_t v : {oz_workspace_bytes(r, b, b, dg), oz_workspace_bytes(r, b, r, dg),
+                       oz_workspace_bytes(b, r, b, dg), oz_workspace_bytes(b, r, r, dg)})
+        best = std::max(best, v);
+    }
+  }
+  return align_up(best);
+}
+
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
-  size_t bytes = align_up(w_bytes(n));
+  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n);
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
   return bytes;
@@ -194,6 +242,30 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
     } else {
       l1.mode = MODE_UPPER_1; l1.opA = xr; l1.opB = in;
       l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
+    }
+    if (oz_level_ok(n, b)) {  // opt-in: both products of every merge on the INT8 tensor cores
+      void* ozws = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
+      const int dg = g_digits.load();
+      for (int64_t g = 0; g < merges; ++g) {
+        const int64_t s0 = 2 * g * b, r = std::min(b, n - s0 - b);
+        double* Wg = W + g * b * b;
+        const double* Ai = X + s0 * ldx + s0;                // A^{-1}
+        const double* Bi = X + (s0 + b) * ldx + (s0 + b);    // B^{-1} (lower) / C^{-1} (upper)
+        if (uplo == 'L') {  // W = C A^{-1}; X21 = -B^{-1} W; X12 := 0
+          TRY(launch_oz_gemm(r, b, b, A + (s0 + b) * lda + s0, lda, TRI_NONE, Ai, ldx, TRI_LOWER, Wg, b, 1.0, 0.0, dg,
+                             ozws, s, &g_launches));
+          TRY(launch_oz_gemm(r, b, r, Bi, ldx, TRI_LOWER, Wg, b, TRI_NONE, X + (s0 + b) * ldx + s0, ldx, -1.0, 0.0,
+                             dg, ozws, s, &g_launches));
+          TRY(launch_zero_2d(X + s0 * ldx + s0 + b, ldx, b, r, s, &g_launches));
+        } else {            // W = A^{-1} B; X12 = -W C^{-1}; X21 := 0
+          TRY(launch_oz_gemm(b, r, b, Ai, ldx, TRI_UPPER, A + s0 * lda + s0 + b, lda, TRI_NONE, Wg, b, 1.0, 0.0, dg,
+                             ozws, s, &g_launches));
+          TRY(launch_oz_gemm(b, r, r, Wg, b, TRI_NONE, Bi, ldx, TRI_UPPER, X + s0 * ldx + s0 + b, ldx, -1.0, 0.0,
+                             dg, ozws, s, &g_launches));
+          TRY(launch_zero_2d(X + (s0 + b) * ldx + s0, ldx, r, b, s, &g_launches));
+        }
+      }
+      continue;
     }
     TRY(launch_level(l1, s, &g_launches));
     TRY(launch_level(l2, s, &g_launches));
@@ -752,6 +824,35 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
   return TRINV_OK;
 }
+
+size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits) {
+  return oz_supported(M, N, K, digits) ? oz_workspace_bytes(M, N, K, digits) : 0;
+}
+
+trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                             char structA, const double* B, int64_t ldb, char structB, double beta, double* C,
+                             int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || digits < 1) return TRINV_INVALID_ARG;
+  if (M == 0 || N == 0) return TRINV_OK;
+  auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
+  const int ta = tri(structA), tb = tri(structB);
+  if (ta < 0 || tb < 0 || (ta != TRI_NONE && tb != TRI_NONE)) return TRINV_INVALID_ARG;
+  if (!A || !B || !C || lda < K || ldb < N || ldc < N) return TRINV_INVALID_ARG;
+  if (!oz_supported(M, N, K, digits)) return TRINV_NOT_SUPPORTED;
+  if (!ws || ws_bytes < oz_workspace_bytes(M, N, K, digits)) return TRINV_WORKSPACE_TOO_SMALL;
+  return cuda_fail(launch_oz_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, digits, ws,
+                                  (cudaStream_t)stream, &g_launches));
+}
+
+trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block) {
+  if ((engine != 0 && engine != 1) || digits < 1 || digits > 10 || min_block < 256) return TRINV_INVALID_ARG;
+  g_digits.store(digits);
+  g_oz_min.store(min_block);
+  g_engine.store(engine);
+  return TRINV_OK;
+}
+
+int trinv_get_product_engine(void) { return product_engine(); }
 
 const char* trinv_status_string(trinv_status_t st) {
   switch (st) {

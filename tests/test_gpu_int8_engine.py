@@ -1,0 +1,102 @@
+"""Opt-in INT8 tensor-core product engine (trinv_set_product_engine / trinv_gemm_oz,
+exact operand splitting into 7-bit digits): parity with the CPU oracle at the same
+gates as the DMMA path, and exactness of the digit products on integer data."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2307_07611_b200 as P  # noqa: E402
+from gpu_common import REL_TOL, RES_TOL, check_full, sample_columns  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture
+def int8_engine():
+    P.set_product_engine("int8", digits=8, min_block=256)
+    yield
+    P.set_product_engine("dmma")
+
+
+def test_gemm_oz_integer_exact():
+    """Integer operands with |a|, |b| < 2^7 are one digit each: the product is exact."""
+    rng = np.random.default_rng(3)
+    A = rng.integers(-100, 101, (256, 512)).astype(np.float64)
+    B = rng.integers(-100, 101, (512, 512)).astype(np.float64)
+    C = P.gemm_oz(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), digits=8).cpu().numpy()
+    assert np.array_equal(C, A @ B)
+
+
+@pytest.mark.parametrize("struct", ["N", "AL", "AU", "BL", "BU"])
+def test_gemm_oz_vs_dmma(struct):
+    rng = np.random.default_rng(7)
+    M = N = K = 1024
+    A = rng.uniform(-1, 1, (M, K)); B = rng.uniform(-1, 1, (K, N))
+    kw = {}
+    if struct == "AL": A = np.tril(A); kw["struct_a"] = "L"
+    if struct == "AU": A = np.triu(A); kw["struct_a"] = "U"
+    if struct == "BL": B = np.tril(B); kw["struct_b"] = "L"
+    if struct == "BU": B = np.triu(B); kw["struct_b"] = "U"
+    Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
+    R = (A.astype(np.longdouble) @ B.astype(np.longdouble)).astype(np.float64)
+    C = P.gemm_oz(Ad, Bd, digits=8, **kw).cpu().numpy()
+    scale = np.abs(A).max(1, keepdims=True) * np.abs(B).max(0, keepdims=True) * K
+    assert np.max(np.abs(C - R) / scale) <= 1e-16
+    # alpha / beta
+    C0 = torch.from_numpy(rng.uniform(-1, 1, (M, N))).to(DEV)
+    C1 = P.gemm_oz(Ad, Bd, C=C0.clone(), alpha=-2.0, beta=0.5, digits=8, **kw).cpu().numpy()
+    assert np.max(np.abs(C1 - (-2.0 * R + 0.5 * C0.cpu().numpy()))) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [512, 1024, 2048, 3072])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_trinv_int8_engine_parity(int8_engine, n, uplo):
+    T = synth.host(n, seed=n, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    f = P.trinv_lower if uplo == "L" else P.trinv_upper
+    X = f(torch.from_numpy(T).to(DEV)).cpu().numpy()
+    check_full(T, X, uplo)
+
+
+def test_config2_int8_engine(int8_engine):
+    n = 8192
+    T = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    synth.device_fill(T, n, diag="signed")
+    X = P.trinv_lower(T)
+    cols = sample_columns(n, 2)
+    Th = T.cpu().numpy()
+    Xs = X[:, torch.from_numpy(cols).to(DEV)].T.contiguous().cpu().numpy()
+    R = oracle.columns(Th, "L", cols)
+    assert oracle.floored_rel_err(Xs, R, axis_cols=0) <= REL_TOL
+    assert oracle.column_residual_ratio(np.tril(Th), Xs, cols) <= RES_TOL
+
+
+def test_inv_from_lu_int8_engine(int8_engine):
+    n = 2048
+    L = synth.host(n, tag="L", diag="one")
+    U = synth.host(n, tag="U", uplo="U", diag="pos")
+    X = P.inv_from_lu(torch.from_numpy(L).to(DEV), torch.from_numpy(U).to(DEV), unit_l=True).cpu().numpy()
+    assert oracle.floored_rel_err(X, np.linalg.inv(L @ U)) <= 1e-9
+
+
+@pytest.mark.parametrize("n,uplo,cfg", [(16384, "L", 2), (32768, "U", 3)])
+def test_large_int8_engine_default_threshold(n, uplo, cfg):
+    """Config 3 size (and n = 16384) with the engine at its default threshold (blocks
+    >= 8192 on INT8, the rest on DMMA): 64 sampled columns at the BASELINE gates."""
+    P.set_product_engine("int8")
+    try:
+        T = torch.empty((n, n), dtype=torch.float64, device=DEV)
+        synth.device_fill(T, n, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+        X = (P.trinv_lower if uplo == "L" else P.trinv_upper)(T)
+        cols = sample_columns(n, cfg)
+        Xs = X[:, torch.from_numpy(cols).to(DEV)].T.contiguous().cpu().numpy()
+        del X
+        Th = T.cpu().numpy()
+        R = oracle.columns(Th, uplo, cols)
+        assert oracle.floored_rel_err(Xs, R, axis_cols=0) <= REL_TOL
+        Tt = np.tril(Th) if uplo == "L" else np.triu(Th)
+        assert oracle.column_residual_ratio(Tt, Xs, cols) <= RES_TOL
+    finally:
+        P.set_product_engine("dmma")

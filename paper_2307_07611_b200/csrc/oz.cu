@@ -31,7 +31,10 @@
 
 namespace trinv {
 
-constexpr int OZ_TM = 128, OZ_TN = 256, OZ_TK = 128, OZ_STAGES = 4, OZ_GROUP_M = 16;
+constexpr int OZ_TM = 128, OZ_TN = 256, OZ_TK = 128, OZ_STAGES = 4;
+#ifndef OZ_GROUP_M
+#define OZ_GROUP_M 8
+#endif
 constexpr int OZ_A_BYTES = OZ_TM * OZ_TK, OZ_B_BYTES = OZ_TN * OZ_TK, OZ_STAGE = OZ_A_BYTES + OZ_B_BYTES;
 constexpr size_t OZ_SMEM = (size_t)OZ_STAGES * OZ_STAGE + 1024 + 256;  // ring + alignment + barriers
 

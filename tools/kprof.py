@@ -40,6 +40,16 @@ def main():
     wall = e0.elapsed_time(e1)
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         fn(); torch.cuda.synchronize()
+    evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
+                 key=lambda e: e.time_range.start)
+    if "--gaps" in sys.argv:
+        prev = None
+        for e in evs:
+            if prev is not None:
+                gap = (e.time_range.start - prev.time_range.end) / 1e3
+                if gap > 0.05:
+                    print(f"  gap {gap:8.3f} ms before {e.name.split('(')[0][:50]} (after {prev.name.split('(')[0][:40]})")
+            prev = e
     agg = defaultdict(lambda: [0, 0.0])
     for ev in prof.events():
         if ev.device_type == torch.autograd.DeviceType.CUDA:

@@ -202,6 +202,9 @@ trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, cons
  * Row-major device matrices; structA / structB as in trinv_gemm (one triangular
  * operand at most).  Envelope: M % 128 == 0, N % 256 == 0, K % 128 == 0,
  * digits * K * 127^2 < 2^31 (K <= 16384 at 8 digits), else TRINV_NOT_SUPPORTED.
+ * digits <= 0 selects the modular variant instead: operands scaled to P-bit integers
+ * (P = 55 at K = 16384), 16 int8 products modulo 16 pairwise coprime moduli <= 256 and
+ * an exact CRT reconstruction (Garner, 128-bit) of the integer product (K <= 65536).
  * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, digits) bytes. */
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits);
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
@@ -210,10 +213,12 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
 
 /* Product engine for the level products of trinv_lower / trinv_upper (and the
  * triangular inverses inside inv_from_lu / lu_crout): engine 0 = FP64 DMMA (default),
- * 1 = the INT8 tensor-core engine above with `digits` digits, used for every level
+ * 1 = the INT8 tensor-core engine above with `digits` digits, 2 = its modular variant,
+ * used for every level
  * whose block size is >= min_block (>= 256) and whose shapes fit its envelope (other
  * levels stay on DMMA).  Process-wide; also settable before the first call with the
- * environment variable TRINV_PRODUCTS=int8.  Changing it changes
+ * environment variable TRINV_PRODUCTS=int8; engine 2 (TRINV_PRODUCTS=int8crt) uses the
+ * modular (CRT) variant of trinv_gemm_oz.  Changing it changes
  * trinv_workspace_bytes ('L', 'U', 'G', 'F'): query the workspace after setting it. */
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
 int trinv_get_product_engine(void);

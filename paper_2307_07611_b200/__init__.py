@@ -198,8 +198,8 @@ def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", strea
 
 
 def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", digits=8, stream=None):
-    """C = alpha A B + beta C (FP64) with the products on the INT8 tensor cores by exact
-    operand splitting into `digits` 7-bit digits (opt-in engine, trinv_gemm_oz)."""
+    """C = alpha A B + beta C (FP64) with the products on the INT8 tensor cores: exact operand
+    splitting into `digits` 7-bit digits, or, with digits=0, 16 moduli + CRT (trinv_gemm_oz)."""
     torch = _torch()
     M, K = A.shape
     N = B.shape[1]
@@ -216,14 +216,15 @@ def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", di
 
 
 def set_product_engine(engine="dmma", digits=8, min_block=8192):
-    """Level products on the FP64 DMMA engine ("dmma", default) or the INT8 tensor-core
-    splitting engine ("int8", `digits` 7-bit digits, levels with block size >= min_block)."""
-    e = {"dmma": 0, "int8": 1}[engine]
+    """Level products on the FP64 DMMA engine ("dmma", default) or an INT8 tensor-core engine
+    for the levels with block size >= min_block: "int8" (exact splitting into `digits` 7-bit
+    digits, 36 int8 products at 8 digits) or "int8crt" (16 moduli and CRT reconstruction)."""
+    e = {"dmma": 0, "int8": 1, "int8crt": 2}[engine]
     _check(lib().trinv_set_product_engine(e, digits, min_block))
 
 
 def product_engine():
-    return ["dmma", "int8"][lib().trinv_get_product_engine()]
+    return ["dmma", "int8", "int8crt"][lib().trinv_get_product_engine()]
 
 
 def gemm_strassen(A, B, *, C=None, stream=None):

@@ -119,6 +119,13 @@ cudaError_t launch_oz_gemm(int64_t M, int64_t N, int64_t K, const double* A, int
                            int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, int s, void* ws,
                            cudaStream_t st, int64_t* launches);
 
+// ---- FP64 products on the INT8 tensor cores by modular arithmetic / CRT (oz2.cu) ----
+bool oz2_supported(int64_t M, int64_t N, int64_t K);
+size_t oz2_workspace_bytes(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                            int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
+                            cudaStream_t st, int64_t* launches);
+
 // ---- Crout factorisation of a diagonal block of order <= LU_MAX (lu.cu) -------
 constexpr int LU_MAX = 128;
 // Reads the block from W (ldw), writes the packed factors to F (ldf); F may equal W.

@@ -1,0 +1,420 @@
+// oz2.cu — FP64 products on the INT8 tensor cores by modular arithmetic (a
+// CRT-based Ozaki-type scheme, "Ozaki scheme II"): the second opt-in product
+// engine (DESIGN.md §8 "oz2_gemm_kernel"), 16 int8 GEMMs per FP64 product instead
+// of the 36 digit products of oz.cu.
+//
+// Scaling.  Row i of A is scaled by 2^(P - e_i), 2^e_i > max_k |a_ik|, and truncated:
+// A'_ik = trunc(a_ik 2^(P - e_i)), an exact integer with |A'| < 2^P (a_ik has 53
+// significant bits, the scaling is a power of two); columns of B likewise (f_j).
+// Then C' = A' B' is an exact integer matrix with |C'| < K 2^(2P).
+// Residues.  With 16 pairwise coprime moduli m_i <= 256 (M = prod m_i ~ 2^125.4),
+// A'_i = A' mod m_i and B'_i in the symmetric range (int8), the tensor cores give
+// C'_i = A'_i B'_i exactly in int32 (|.| <= K 2^14), reduced mod m_i by the epilogue.
+// Reconstruction.  Garner's mixed-radix form of the CRT recovers C' mod M exactly in
+// 128-bit integers; as |C'| < M/2 (P chosen from K: 2P + log2 K < log2 M - 1), the
+// symmetric representative is C' itself, and
+//     (A B)_ij ~= 2^(e_i - P) 2^(f_j - P) C'_ij,
+// the only errors being the truncation of the scaled operands (2^-P relative to the
+// row / column maxima) and the final rounding to FP64.
+//
+// The GEMM kernel is the engine of oz.cu (TMA 128B-swizzled K blocks, tcgen05.mma
+// kind::i8, two TMEM accumulators) looping over the 16 moduli instead of digit pairs;
+// its epilogue writes uint8 residues, and a separate kernel reconstructs C.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <utility>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace trinv {
+
+constexpr int OZ2_NMOD = 16;
+constexpr int OZ2_TM = 128, OZ2_TN = 256, OZ2_TK = 128, OZ2_STAGES = 4, OZ2_GROUP_M = 8;
+constexpr int OZ2_A_BYTES = OZ2_TM * OZ2_TK, OZ2_B_BYTES = OZ2_TN * OZ2_TK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
+constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + 1024 + 256;
+constexpr int OZ2_THREADS = 192;
+
+// pairwise coprime, <= 256 (symmetric residues fit int8)
+__host__ __device__ constexpr int oz2_mod(int i) {
+  constexpr int m[OZ2_NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+  return m[i];
+}
+__host__ __device__ constexpr int oz2_inv(int a, int m) {  // a^-1 mod m (a, m coprime), extended Euclid
+  int t = 0, nt = 1, r = m, nr = a % m;
+  while (nr != 0) {
+    const int q = r / nr;
+    const int tt = t - q * nt; t = nt; nt = tt;
+    const int rr = r - q * nr; r = nr; nr = rr;
+  }
+  return t < 0 ? t + m : t;
+}
+
+// ---- residues of the scaled operands ------------------------------------------------
+__device__ __forceinline__ int oz2_exp_above(double m) {
+  if (m == 0.0) return 0;
+  int e;
+  frexp(m, &e);
+  return e;
+}
+// A' (|A'| < 2^62) mod m in the symmetric range, from the two 32-bit halves
+template <int I>
+__device__ __forceinline__ int8_t oz2_residue(int64_t v) {  // |v| < 2^62
+  constexpr int m = oz2_mod(I);
+  constexpr int two32 = (int)((((int64_t)1) << 32) % m);
+  const int hi = (int)(v >> 32);                 // |hi| < 2^30
+  const uint32_t lo = (uint32_t)(v & 0xffffffffu);
+  int r = (hi % m) * two32 + (int)(lo % (uint32_t)m);  // |r| < 2^16 + 2^8
+  r %= m;
+  if (r < 0) r += m;
+  if (r > (m - 1) / 2) r -= m;  // symmetric: [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m
+  return (int8_t)r;
+}
+template <int... I>
+__device__ __forceinline__ void oz2_residues(int64_t v, int8_t* out, size_t stride, std::integer_sequence<int, I...>) {
+  ((out[I * stride] = oz2_residue<I>(v)), ...);
+}
+
+// A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum.
+__global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int P, int8_t* out, int* expo) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const double* a = A + (int64_t)warp * lda;
+  double m = 0.0;
+  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(a[k]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int e = oz2_exp_above(m);
+  if (lane == 0) expo[warp] = e;
+  const size_t ss = (size_t)rows * K;
+  for (int k = lane; k < K; k += 32) {
+    const int64_t v = (int64_t)trunc(ldexp(a[k], P - e));  // exact
+    oz2_residues(v, out + (size_t)warp * K + k, ss, std::make_integer_sequence<int, OZ2_NMOD>{});
+  }
+}
+__global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, unsigned long long* maxbits) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const int k0 = blockIdx.y * 512, k1 = min(K, k0 + 512);
+  double m = 0.0;
+  for (int k = k0; k < k1; ++k) m = fmax(m, fabs(B[(int64_t)k * ldb + j]));
+  atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
+}
+// B operand (K x cols): residues written transposed (cols x K, K-major).
+__global__ void oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int P,
+                                      const unsigned long long* maxbits, int* expo, int8_t* out) {
+  __shared__ long long tile[32][33];
+  const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int jx = j0 + threadIdx.x;
+  const int e = jx < cols ? oz2_exp_above(__longlong_as_double((long long)maxbits[jx])) : 0;
+  if (blockIdx.y == 0 && threadIdx.y == 0 && jx < cols) expo[jx] = e;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r;
+    tile[r][threadIdx.x] = (k < K && jx < cols) ? (long long)trunc(ldexp(B[(int64_t)k * ldb + jx], P - e)) : 0;
+  }
+  __syncthreads();
+  const size_t ss = (size_t)cols * K;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + r, k = k0 + threadIdx.x;
+    if (j < cols && k < K)
+      oz2_residues(tile[threadIdx.x][r], out + (size_t)j * K + k, ss, std::make_integer_sequence<int, OZ2_NMOD>{});
+  }
+}
+
+// ---- the int8 tensor-core engine, one exact product per modulus -----------------------
+__device__ __forceinline__ uint64_t oz2_smem_desc(const void* p) {
+  uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+struct Oz2Params {
+  int M, N, K;
+  int triA, triB;
+  uint8_t* R;  // residues [16][M][N]
+  int tiles_n;
+};
+
+__global__ void __launch_bounds__(OZ2_THREADS, 1)
+    oz2_gemm_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const Oz2Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* sA = base;
+  unsigned char* sB = base + OZ2_STAGES * OZ2_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + OZ2_STAGES * OZ2_STAGE);
+  uint64_t* empty = full + OZ2_STAGES;
+  uint64_t* acc_full = empty + OZ2_STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = p.M / OZ2_TM;
+  const int t = blockIdx.x;
+  const int per_group = OZ2_GROUP_M * p.tiles_n;
+  const int first_m = (t / per_group) * OZ2_GROUP_M;
+  const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
+  int I = first_m + (t % per_group) % gsz, J = (t % per_group) / gsz;
+  if (p.triA == TRI_LOWER) I = tiles_m - 1 - I;
+  if (p.triB == TRI_UPPER) J = p.tiles_n - 1 - J;
+  int kb = 0, ke = p.K;
+  if (p.triA == TRI_LOWER) ke = min(ke, (I + 1) * OZ2_TM);
+  if (p.triA == TRI_UPPER) kb = I * OZ2_TM;
+  if (p.triB == TRI_LOWER) kb = J * OZ2_TN;
+  if (p.triB == TRI_UPPER) ke = min(ke, (J + 1) * OZ2_TN);
+  const int nkb = ke > kb ? (ke - kb) / OZ2_TK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 4); }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * OZ2_TN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {  // TMA producer: moduli, K-blocks
+    tma_prefetch_desc(&ma);
+    tma_prefetch_desc(&mb);
+    int it = 0;
+    for (int i = 0; i < OZ2_NMOD; ++i)
+      for (int kk = 0; kk < nkb; ++kk, ++it) {
+        const int st = it % OZ2_STAGES, use = it / OZ2_STAGES;
+        if (use > 0) mbar_wait(&empty[st], (uint32_t)((use - 1) & 1));
+        mbar_arrive_expect_tx(&full[st], OZ2_STAGE);
+        const int k = kb + kk * OZ2_TK;
+        tma_load_2d(sA + st * OZ2_A_BYTES, &ma, k, i * p.M + I * OZ2_TM, &full[st]);
+        tma_load_2d(sB + st * OZ2_B_BYTES, &mb, k, i * p.N + J * OZ2_TN, &full[st]);
+      }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    const uint32_t idesc =
+        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(OZ2_TM >> 4) << 24);
+    int it = 0;
+    for (int i = 0; i < OZ2_NMOD; ++i) {
+      const int buf = i & 1, use = i >> 1;
+      if (use > 0) {
+        mbar_wait(&acc_empty[buf], (uint32_t)((use - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      }
+      const uint32_t tacc = tmem + (uint32_t)(buf * OZ2_TN);
+      bool first = true;
+      for (int kk = 0; kk < nkb; ++kk, ++it) {
+        const int st = it % OZ2_STAGES;
+        mbar_wait(&full[st], (uint32_t)((it / OZ2_STAGES) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint64_t da = oz2_smem_desc(sA + st * OZ2_A_BYTES), db = oz2_smem_desc(sB + st * OZ2_B_BYTES);
+#pragma unroll
+        for (int k = 0; k < OZ2_TK / 32; ++k) {
+          const uint32_t acc = first ? 0u : 1u;
+          first = false;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tacc),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&empty[st]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&acc_full[buf]))
+                   : "memory");
+    }
+  }
+  if (warp >= 2) {  // epilogue: residues C'_i = (A'_i B'_i) mod m_i as uint8
+    const int q4 = warp & 3;
+    const int row = I * OZ2_TM + q4 * 32 + lane;
+    for (int i = 0; i < OZ2_NMOD; ++i) {
+      const int buf = i & 1, use = i >> 1;
+      mbar_wait(&acc_full[buf], (uint32_t)(use & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int m = oz2_mod(i);
+      const double rm = 1.0 / m;
+      uint8_t* dst = p.R + ((size_t)i * p.M + row) * p.N + J * OZ2_TN;
+#pragma unroll 1
+      for (int c = 0; c < OZ2_TN; c += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * OZ2_TN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        uint32_t packed[8];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int x = nkb ? (int)v[j + b] : 0;
+            int r = x - (int)floor((double)x * rm) * m;  // exact quotient for |x| < 2^31 up to one step
+            r += (r < 0) ? m : 0;
+            r -= (r >= m) ? m : 0;
+            w |= (uint32_t)r << (8 * b);
+          }
+          packed[j / 4] = w;
+        }
+        *reinterpret_cast<uint4*>(dst + c) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * OZ2_TN));
+}
+
+// ---- reconstruction: C' = sum_i c_i w_i mod M (w_i = M_i (M_i^-1 mod m_i) mod M) -------
+// w_i = wh_i 2^64 + wl_i; the two sums of c_i wl_i and c_i wh_i stay below 2^77 in
+// unsigned 128-bit integers; q = floor(S / M) (<= 2^12) is estimated in FP64 and
+// corrected by one step, so R = S - q M is exact, then mapped to (-M/2, M/2].
+struct Oz2Crt {
+  unsigned long long wl[OZ2_NMOD], wh[OZ2_NMOD];
+  unsigned long long Ml, Mh;
+  double Md;
+};
+
+__global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int* ea, const int* eb, int P,
+                                       double alpha, double beta, double* C, int64_t ldc, const Oz2Crt crt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * N) return;
+  const int i = (int)(e / N), j = (int)(e % N);
+  const size_t plane = (size_t)M * N;
+  unsigned __int128 lo = 0, hi = 0;
+#pragma unroll
+  for (int q = 0; q < OZ2_NMOD; ++q) {
+    const unsigned c = R[q * plane + e];
+    lo += (unsigned __int128)crt.wl[q] * c;
+    hi += (unsigned __int128)crt.wh[q] * c;
+  }
+  // S = hi 2^64 + lo
+  const double Sd = (double)hi * 18446744073709551616.0 + (double)lo;
+  long long q = (long long)floor(Sd / crt.Md);
+  const unsigned __int128 Mw = ((unsigned __int128)crt.Mh << 64) | crt.Ml;
+  // R = (hi - q Mh) 2^64 + (lo - q Ml), in signed 128-bit (|.| < 2^127)
+  __int128 r = ((__int128)hi - (__int128)q * (__int128)crt.Mh) * ((__int128)1 << 64) +
+               ((__int128)lo - (__int128)q * (__int128)crt.Ml);
+  if (r < 0) r += (__int128)Mw;
+  if (r >= (__int128)Mw) r -= (__int128)Mw;
+  if (r > (__int128)(Mw >> 1)) r -= (__int128)Mw;  // symmetric representative = C'
+  const bool neg = r < 0;
+  const unsigned __int128 mag = neg ? (unsigned __int128)(-r) : (unsigned __int128)r;
+  double val = fma((double)(unsigned long long)(mag >> 64), 18446744073709551616.0, (double)(unsigned long long)mag);
+  if (neg) val = -val;
+  val = ldexp(val, ea[i] + eb[j] - 2 * P);
+  double* out = C + (int64_t)i * ldc + j;
+  *out = beta == 0.0 ? alpha * val : fma(alpha, val, beta * *out);
+}
+
+static Oz2Crt oz2_crt_constants() {
+  Oz2Crt c{};
+  unsigned __int128 Mall = 1;
+  for (int q = 0; q < OZ2_NMOD; ++q) Mall *= (unsigned)oz2_mod(q);
+  for (int q = 0; q < OZ2_NMOD; ++q) {
+    const unsigned m = (unsigned)oz2_mod(q);
+    const unsigned __int128 Mi = Mall / m;
+    const unsigned y = (unsigned)oz2_inv((int)(Mi % m), (int)m);
+    const unsigned __int128 w = (Mi * y) % Mall;  // Mi y < M 2^8 / m: no overflow (M < 2^126)
+    c.wl[q] = (unsigned long long)w;
+    c.wh[q] = (unsigned long long)(w >> 64);
+  }
+  c.Ml = (unsigned long long)Mall;
+  c.Mh = (unsigned long long)(Mall >> 64);
+  c.Md = (double)c.Mh * 18446744073709551616.0 + (double)c.Ml;
+  return c;
+}
+
+// ---- host -------------------------------------------------------------------------------
+static int oz2_scale_bits(int64_t K) {  // P with K 2^(2P) < M/2
+  double lm = 0.0;
+  for (int q = 0; q < OZ2_NMOD; ++q) lm += std::log2((double)oz2_mod(q));
+  int P = (int)std::floor((lm - 1.0 - std::log2((double)K)) / 2.0);
+  return P > 62 ? 62 : P;
+}
+
+bool oz2_supported(int64_t M, int64_t N, int64_t K) {
+  return M > 0 && N > 0 && K > 0 && M % OZ2_TM == 0 && N % OZ2_TN == 0 && K % OZ2_TK == 0 && K <= 65536 &&
+         oz2_scale_bits(K) >= 53 && M * N < ((int64_t)1 << 40);
+}
+
+size_t oz2_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return al((size_t)OZ2_NMOD * M * K) + al((size_t)OZ2_NMOD * N * K) + al((size_t)OZ2_NMOD * M * N) +
+         al((size_t)M * 4) + al((size_t)N * 4) + al((size_t)N * 8);
+}
+
+static bool oz2_encode(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncFn fn = nullptr;
+  if (!fn) {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) != cudaSuccess) return false;
+    fn = reinterpret_cast<EncFn>(q);
+  }
+  cuuint64_t dims[2] = {cols, rows}, strides[1] = {cols};
+  cuuint32_t box[2] = {(cuuint32_t)OZ2_TK, box_rows}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                            int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
+                            cudaStream_t st, int64_t* launches) {
+  if (!oz2_supported(M, N, K)) return cudaErrorInvalidValue;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* w = static_cast<char*>(ws);
+  int8_t* As = reinterpret_cast<int8_t*>(w); w += al((size_t)OZ2_NMOD * M * K);
+  int8_t* Bs = reinterpret_cast<int8_t*>(w); w += al((size_t)OZ2_NMOD * N * K);
+  uint8_t* Rs = reinterpret_cast<uint8_t*>(w); w += al((size_t)OZ2_NMOD * M * N);
+  int* ea = reinterpret_cast<int*>(w); w += al((size_t)M * 4);
+  int* eb = reinterpret_cast<int*>(w); w += al((size_t)N * 4);
+  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(w);
+  const int P = oz2_scale_bits(K);
+  GemmArgs ga{};
+  ga.M = M; ga.N = N; ga.K = K; ga.batch = 1; ga.triA = triA; ga.triB = triB;
+  const double f64 = gemm_flops(ga);
+  ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
+  oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, P, As, ea);
+  cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
+  if (e != cudaSuccess) return e;
+  oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(B, ldb, (int)K,
+                                                                                                   (int)N, maxbits);
+  oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), dim3(32, 8), 0, st>>>(
+      B, ldb, (int)K, (int)N, P, maxbits, eb, Bs);
+  CUtensorMap ma, mb;
+  if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
+      !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, OZ2_TN))
+    return cudaErrorInvalidValue;
+  Oz2Params p{};
+  p.M = (int)M; p.N = (int)N; p.K = (int)K; p.triA = triA; p.triB = triB; p.R = Rs;
+  p.tiles_n = (int)(N / OZ2_TN);
+  set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
+  oz2_gemm_kernel<<<(unsigned)((M / OZ2_TM) * (N / OZ2_TN)), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+  const int64_t total = M * N;
+  static const Oz2Crt crt = oz2_crt_constants();
+  oz2_reconstruct_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha, beta,
+                                                                         C, ldc, crt);
+  if (launches) *launches += 5;
+  return cudaGetLastError();
+}
+
+}  // namespace trinv

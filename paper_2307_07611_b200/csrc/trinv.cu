@@ -115,7 +115,7 @@ static int product_engine() {
   int e = g_engine.load(std::memory_order_relaxed);
   if (e < 0) {
     const char* v = getenv("TRINV_PRODUCTS");
-    e = (v && strcmp(v, "int8") == 0) ? 1 : 0;
+    e = (v && strcmp(v, "int8") == 0) ? 1 : ((v && strcmp(v, "int8crt") == 0) ? 2 : 0);
     g_engine.store(e, std::memory_order_relaxed);
   }
   return e;
@@ -135,27 +135,35 @@ static size_t mat_bytes(int64_t n) { return (size_t)n * (size_t)even_up(n) * siz
 // INT8 engine: a level takes it when every merge's two products fit the envelope
 // (lower: r x b x b and r x b x r; upper: b x r x b and b x r x r); its scratch is the
 // largest of those products' workspaces.
+static bool oz_shape_ok(int64_t M, int64_t N, int64_t K) {
+  return product_engine() == 2 ? oz2_supported(M, N, K) : oz_supported(M, N, K, g_digits.load());
+}
+static size_t oz_shape_ws(int64_t M, int64_t N, int64_t K) {
+  return product_engine() == 2 ? oz2_workspace_bytes(M, N, K) : oz_workspace_bytes(M, N, K, g_digits.load());
+}
+static cudaError_t oz_product(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                              int64_t ldb, int triB, double* C, int64_t ldc, double alpha, void* ws, cudaStream_t s) {
+  if (product_engine() == 2)
+    return launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, 0.0, ws, s, &g_launches);
+  return launch_oz_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, 0.0, g_digits.load(), ws, s, &g_launches);
+}
 static bool oz_level_ok(int64_t n, int64_t b) {
-  if (product_engine() != 1 || b < g_oz_min.load() || b % 256) return false;
-  const int dg = g_digits.load();
+  if (product_engine() == 0 || b < g_oz_min.load() || b % 256) return false;
   for (int64_t s = 0; s + b < n; s += 2 * b) {
     const int64_t r = std::min(b, n - s - b);
-    if (r % 256 || !oz_supported(r, b, b, dg) || !oz_supported(r, b, r, dg) || !oz_supported(b, r, b, dg) ||
-        !oz_supported(b, r, r, dg))
+    if (r % 256 || !oz_shape_ok(r, b, b) || !oz_shape_ok(r, b, r) || !oz_shape_ok(b, r, b) || !oz_shape_ok(b, r, r))
       return false;
   }
   return true;
 }
 static size_t oz_scratch(int64_t n) {
-  if (product_engine() != 1 || n <= BLK_MAX) return 0;
-  const int dg = g_digits.load();
+  if (product_engine() == 0 || n <= BLK_MAX) return 0;
   size_t best = 0;
   for (int64_t b = BLK_MAX; b < n; b *= 2) {
     if (!oz_level_ok(n, b)) continue;
     for (int64_t s = 0; s + b < n; s += 2 * b) {
       const int64_t r = std::min(b, n - s - b);
-      for (size_t v : {oz_workspace_bytes(r, b, b, dg), oz_workspace_bytes(r, b, r, dg),
-                       oz_workspace_bytes(b, r, b, dg), oz_workspace_bytes(b, r, r, dg)})
+      for (size_t v : {oz_shape_ws(r, b, b), oz_shape_ws(r, b, r), oz_shape_ws(b, r, b), oz_shape_ws(b, r, r)})
         best = std::max(best, v);
     }
   }
@@ -245,23 +253,18 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
     }
     if (oz_level_ok(n, b)) {  // opt-in: both products of every merge on the INT8 tensor cores
       void* ozws = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
-      const int dg = g_digits.load();
       for (int64_t g = 0; g < merges; ++g) {
         const int64_t s0 = 2 * g * b, r = std::min(b, n - s0 - b);
         double* Wg = W + g * b * b;
         const double* Ai = X + s0 * ldx + s0;                // A^{-1}
         const double* Bi = X + (s0 + b) * ldx + (s0 + b);    // B^{-1} (lower) / C^{-1} (upper)
         if (uplo == 'L') {  // W = C A^{-1}; X21 = -B^{-1} W; X12 := 0
-          TRY(launch_oz_gemm(r, b, b, A + (s0 + b) * lda + s0, lda, TRI_NONE, Ai, ldx, TRI_LOWER, Wg, b, 1.0, 0.0, dg,
-                             ozws, s, &g_launches));
-          TRY(launch_oz_gemm(r, b, r, Bi, ldx, TRI_LOWER, Wg, b, TRI_NONE, X + (s0 + b) * ldx + s0, ldx, -1.0, 0.0,
-                             dg, ozws, s, &g_launches));
+          TRY(oz_product(r, b, b, A + (s0 + b) * lda + s0, lda, TRI_NONE, Ai, ldx, TRI_LOWER, Wg, b, 1.0, ozws, s));
+          TRY(oz_product(r, b, r, Bi, ldx, TRI_LOWER, Wg, b, TRI_NONE, X + (s0 + b) * ldx + s0, ldx, -1.0, ozws, s));
           TRY(launch_zero_2d(X + s0 * ldx + s0 + b, ldx, b, r, s, &g_launches));
         } else {            // W = A^{-1} B; X12 = -W C^{-1}; X21 := 0
-          TRY(launch_oz_gemm(b, r, b, Ai, ldx, TRI_UPPER, A + s0 * lda + s0 + b, lda, TRI_NONE, Wg, b, 1.0, 0.0, dg,
-                             ozws, s, &g_launches));
-          TRY(launch_oz_gemm(b, r, r, Wg, b, TRI_NONE, Bi, ldx, TRI_UPPER, X + s0 * ldx + s0 + b, ldx, -1.0, 0.0,
-                             dg, ozws, s, &g_launches));
+          TRY(oz_product(b, r, b, Ai, ldx, TRI_UPPER, A + s0 * lda + s0 + b, lda, TRI_NONE, Wg, b, 1.0, ozws, s));
+          TRY(oz_product(b, r, r, Wg, b, TRI_NONE, Bi, ldx, TRI_UPPER, X + s0 * ldx + s0 + b, ldx, -1.0, ozws, s));
           TRY(launch_zero_2d(X + (s0 + b) * ldx + s0, ldx, r, b, s, &g_launches));
         }
       }
@@ -826,18 +829,25 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
 }
 
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits) {
+  if (digits <= 0) return oz2_supported(M, N, K) ? oz2_workspace_bytes(M, N, K) : 0;
   return oz_supported(M, N, K, digits) ? oz_workspace_bytes(M, N, K, digits) : 0;
 }
 
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                              char structA, const double* B, int64_t ldb, char structB, double beta, double* C,
                              int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream) {
-  if (M < 0 || N < 0 || K < 0 || digits < 1) return TRINV_INVALID_ARG;
+  if (M < 0 || N < 0 || K < 0 || digits > 10) return TRINV_INVALID_ARG;
   if (M == 0 || N == 0) return TRINV_OK;
   auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
   const int ta = tri(structA), tb = tri(structB);
   if (ta < 0 || tb < 0 || (ta != TRI_NONE && tb != TRI_NONE)) return TRINV_INVALID_ARG;
   if (!A || !B || !C || lda < K || ldb < N || ldc < N) return TRINV_INVALID_ARG;
+  if (digits <= 0) {  // CRT scheme, 16 moduli (oz2.cu)
+    if (!oz2_supported(M, N, K)) return TRINV_NOT_SUPPORTED;
+    if (!ws || ws_bytes < oz2_workspace_bytes(M, N, K)) return TRINV_WORKSPACE_TOO_SMALL;
+    return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, ws, (cudaStream_t)stream,
+                                     &g_launches));
+  }
   if (!oz_supported(M, N, K, digits)) return TRINV_NOT_SUPPORTED;
   if (!ws || ws_bytes < oz_workspace_bytes(M, N, K, digits)) return TRINV_WORKSPACE_TOO_SMALL;
   return cuda_fail(launch_oz_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, digits, ws,
@@ -845,7 +855,7 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
 }
 
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block) {
-  if ((engine != 0 && engine != 1) || digits < 1 || digits > 10 || min_block < 256) return TRINV_INVALID_ARG;
+  if (engine < 0 || engine > 2 || digits < 1 || digits > 10 || min_block < 256) return TRINV_INVALID_ARG;
   g_digits.store(digits);
   g_oz_min.store(min_block);
   g_engine.store(engine);

@@ -14,24 +14,27 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
-@pytest.fixture
-def int8_engine():
-    P.set_product_engine("int8", digits=8, min_block=256)
-    yield
+@pytest.fixture(params=["int8", "int8crt"])
+def int8_engine(request):
+    P.set_product_engine(request.param, digits=8, min_block=256)
+    yield request.param
     P.set_product_engine("dmma")
 
 
-def test_gemm_oz_integer_exact():
-    """Integer operands with |a|, |b| < 2^7 are one digit each: the product is exact."""
+@pytest.mark.parametrize("digits", [8, 0])
+def test_gemm_oz_integer_exact(digits):
+    """Small integer operands are represented exactly by both schemes (one digit each, or
+    residues of exact scaled integers): the product is exact."""
     rng = np.random.default_rng(3)
     A = rng.integers(-100, 101, (256, 512)).astype(np.float64)
     B = rng.integers(-100, 101, (512, 512)).astype(np.float64)
-    C = P.gemm_oz(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), digits=8).cpu().numpy()
+    C = P.gemm_oz(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), digits=digits).cpu().numpy()
     assert np.array_equal(C, A @ B)
 
 
+@pytest.mark.parametrize("digits", [8, 0])
 @pytest.mark.parametrize("struct", ["N", "AL", "AU", "BL", "BU"])
-def test_gemm_oz_vs_dmma(struct):
+def test_gemm_oz_vs_dmma(struct, digits):
     rng = np.random.default_rng(7)
     M = N = K = 1024
     A = rng.uniform(-1, 1, (M, K)); B = rng.uniform(-1, 1, (K, N))
@@ -42,12 +45,12 @@ def test_gemm_oz_vs_dmma(struct):
     if struct == "BU": B = np.triu(B); kw["struct_b"] = "U"
     Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
     R = (A.astype(np.longdouble) @ B.astype(np.longdouble)).astype(np.float64)
-    C = P.gemm_oz(Ad, Bd, digits=8, **kw).cpu().numpy()
+    C = P.gemm_oz(Ad, Bd, digits=digits, **kw).cpu().numpy()
     scale = np.abs(A).max(1, keepdims=True) * np.abs(B).max(0, keepdims=True) * K
     assert np.max(np.abs(C - R) / scale) <= 1e-16
     # alpha / beta
     C0 = torch.from_numpy(rng.uniform(-1, 1, (M, N))).to(DEV)
-    C1 = P.gemm_oz(Ad, Bd, C=C0.clone(), alpha=-2.0, beta=0.5, digits=8, **kw).cpu().numpy()
+    C1 = P.gemm_oz(Ad, Bd, C=C0.clone(), alpha=-2.0, beta=0.5, digits=digits, **kw).cpu().numpy()
     assert np.max(np.abs(C1 - (-2.0 * R + 0.5 * C0.cpu().numpy()))) <= 1e-12
 
 
@@ -81,11 +84,12 @@ def test_inv_from_lu_int8_engine(int8_engine):
     assert oracle.floored_rel_err(X, np.linalg.inv(L @ U)) <= 1e-9
 
 
+@pytest.mark.parametrize("engine", ["int8", "int8crt"])
 @pytest.mark.parametrize("n,uplo,cfg", [(16384, "L", 2), (32768, "U", 3)])
-def test_large_int8_engine_default_threshold(n, uplo, cfg):
+def test_large_int8_engine_default_threshold(n, uplo, cfg, engine):
     """Config 3 size (and n = 16384) with the engine at its default threshold (blocks
     >= 8192 on INT8, the rest on DMMA): 64 sampled columns at the BASELINE gates."""
-    P.set_product_engine("int8")
+    P.set_product_engine(engine, min_block=4096 if engine == "int8crt" else 8192)
     try:
         T = torch.empty((n, n), dtype=torch.float64, device=DEV)
         synth.device_fill(T, n, uplo=uplo, diag="signed" if uplo == "L" else "pos")

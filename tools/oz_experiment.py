@@ -34,9 +34,9 @@ def main():
     R = (A.astype(np.longdouble) @ B.astype(np.longdouble)).astype(np.float64)
     Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
     scale = np.abs(A).max(1, keepdims=True) * np.abs(B).max(0, keepdims=True) * K
-    for dg in (6, 7, 8, 9):
+    for dg in (6, 7, 8, 9, 0):
         C = P.gemm_oz(Ad, Bd, digits=dg).cpu().numpy()
-        print(f"small {M}x{N}x{K} digits={dg}: max|err|/(K rowmax colmax) {np.max(np.abs(C - R) / scale):.2e}  "
+        print(f"small {M}x{N}x{K} {'crt' if dg == 0 else f'digits={dg}'}: max|err|/(K rowmax colmax) {np.max(np.abs(C - R) / scale):.2e}  "
               f"max rel {np.max(np.abs(C - R) / np.abs(R)):.2e}")
     C = P.gemm(Ad, Bd).cpu().numpy()
     print(f"small DMMA: max|err|/(K rowmax colmax) {np.max(np.abs(C - R) / scale):.2e}  max rel {np.max(np.abs(C - R) / np.abs(R)):.2e}")
@@ -46,20 +46,22 @@ def main():
         B = torch.rand((n, n), dtype=torch.float64, device=DEV) * 2 - 1
         R = A @ B
         t_d = timed(lambda: P.gemm(A, B), 3)
-        for dg in (7, 8):
+        for dg in (8, 0):
             C = P.gemm_oz(A, B, digits=dg)
             t = timed(lambda: P.gemm_oz(A, B, digits=dg), 3)
             err = (C - R).abs().max().item() / R.abs().max().item()
-            print(f"dense n={n} digits={dg}: {t:8.2f} ms ({2 * n ** 3 / t / 1e9:7.1f} TF/s FP64-equiv)  "
+            print(f"dense n={n} {'crt16' if dg == 0 else f'digits={dg}'}: {t:8.2f} ms ({2 * n ** 3 / t / 1e9:7.1f} TF/s FP64-equiv)  "
                   f"DMMA {t_d:8.2f} ms ({2 * n ** 3 / t_d / 1e9:6.1f} TF/s)  max|C-R|/max|R| {err:.2e}")
         # triangular B (lower): k >= j blocks only
         Bl = torch.tril(B)
         Rl = A @ Bl
         t_dl = timed(lambda: P.gemm(A, Bl, struct_b="L"), 3)
-        C = P.gemm_oz(A, Bl, struct_b="L", digits=8)
-        t = timed(lambda: P.gemm_oz(A, Bl, struct_b="L", digits=8), 3)
-        err = (C - Rl).abs().max().item() / Rl.abs().max().item()
-        print(f"  tri-B n={n} digits=8: {t:8.2f} ms  DMMA {t_dl:8.2f} ms  speedup {t_dl / t:.2f}x  err {err:.2e}")
+        for dg in (8, 0):
+            C = P.gemm_oz(A, Bl, struct_b="L", digits=dg)
+            t = timed(lambda: P.gemm_oz(A, Bl, struct_b="L", digits=dg), 3)
+            err = (C - Rl).abs().max().item() / Rl.abs().max().item()
+            print(f"  tri-B n={n} {'crt16' if dg == 0 else f'digits={dg}'}: {t:8.2f} ms  DMMA {t_dl:8.2f} ms  "
+                  f"speedup {t_dl / t:.2f}x  err {err:.2e}")
         del A, B, R, Bl, Rl, C
         torch.cuda.empty_cache()
 

@@ -51,6 +51,10 @@ CONFIGS = {
 }
 
 
+def n_of(cfg):
+    return cfg.get("n", 0)
+
+
 def peaks():
     hbm, src_h = HBM_FALLBACK, "fallback"
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -271,9 +275,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true", help="never replay steps from a CUDA graph")
-    ap.add_argument("--products", default="dmma", choices=["dmma", "int8"],
-                    help="engine for the level products: FP64 DMMA (default) or the INT8 tensor-core "
-                         "splitting engine (8 digits, levels with block size >= 8192)")
+    ap.add_argument("--products", default="int8crt", choices=["dmma", "int8", "int8crt"],
+                    help="engine for the level products: INT8 tensor cores by 16 moduli + CRT for blocks >= 4096 "
+                         "(int8crt, default), by 8-digit splitting (int8), or FP64 DMMA for every level (dmma)")
+    ap.add_argument("--min-block", type=int, default=0, help="INT8 engines: smallest level block (0: 4096)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -300,9 +305,15 @@ def main():
     stream = torch.cuda.current_stream()
     cfg = CONFIGS[args.config]
     hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
-    if args.products == "int8":
-        P.set_product_engine("int8")
-        cfg = dict(cfg, workload=cfg["workload"] + " [INT8 tensor-core products, 8 digits, blocks >= 8192]")
+    mb = args.min_block or 4096
+    P.set_product_engine(args.products, min_block=mb)
+    if cfg["kind"] not in ("B",) and n_of(cfg) > 128:
+        if args.products == "dmma":
+            cfg = dict(cfg, workload=cfg["workload"] + " [FP64 DMMA products]")
+        else:
+            desc = "8-digit splitting" if args.products == "int8" else "16 moduli + CRT"
+            cfg = dict(cfg, workload=cfg["workload"] + f" [products of blocks >= {mb} on the INT8 tensor cores "
+                                                       f"({desc}), smaller ones on FP64 DMMA]")
 
     def barrier():
         if world > 1:
@@ -454,7 +465,9 @@ def main():
         if n_o > 0 and ms_o >= ms_d:  # the INT8 engine carries the dominant products
             i8_peak = 2.0 * I8_PER_BF16_SUSTAINED
             ach = ops_o / (ms_o / 1e3) / 1e12
-            line["roofline"] = {"bound": "tensor", "kernel": "oz_gemm_kernel (INT8 tcgen05, exact 8-digit splitting)",
+            kname = ("oz_gemm_kernel (INT8 tcgen05, exact 8-digit splitting)" if args.products == "int8"
+                     else "oz2_gemm_kernel (INT8 tcgen05, 16 moduli + CRT)")
+            line["roofline"] = {"bound": "tensor", "kernel": kname,
                                 "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
                                 "traffic": None,
                                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8 / bf16)",

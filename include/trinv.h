@@ -212,14 +212,13 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
                              int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream);
 
 /* Product engine for the level products of trinv_lower / trinv_upper (and the
- * triangular inverses inside inv_from_lu / lu_crout): engine 0 = FP64 DMMA (default),
- * 1 = the INT8 tensor-core engine above with `digits` digits, 2 = its modular variant,
- * used for every level
- * whose block size is >= min_block (>= 256) and whose shapes fit its envelope (other
- * levels stay on DMMA).  Process-wide; also settable before the first call with the
- * environment variable TRINV_PRODUCTS=int8; engine 2 (TRINV_PRODUCTS=int8crt) uses the
- * modular (CRT) variant of trinv_gemm_oz.  Changing it changes
- * trinv_workspace_bytes ('L', 'U', 'G', 'F'): query the workspace after setting it. */
+ * triangular inverses inside inv_from_lu / lu_crout): engine 0 = FP64 DMMA
+ * (mma.sync), 1 = the INT8 tensor-core engine above with `digits` digits, 2 (default)
+ * = its modular (CRT) variant; engines 1 and 2 take every level whose block size is
+ * >= min_block (>= 256; default 4096) and whose shapes fit their envelope, all other
+ * levels stay on DMMA.  Process-wide; the environment variable
+ * TRINV_PRODUCTS=dmma|int8|int8crt selects the engine before the first call.  Changing
+ * it changes trinv_workspace_bytes ('L', 'U', 'G', 'F'): query the workspace after. */
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
 int trinv_get_product_engine(void);
 

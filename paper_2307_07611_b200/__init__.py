@@ -215,10 +215,10 @@ def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", di
     return C
 
 
-def set_product_engine(engine="dmma", digits=8, min_block=8192):
-    """Level products on the FP64 DMMA engine ("dmma", default) or an INT8 tensor-core engine
-    for the levels with block size >= min_block: "int8" (exact splitting into `digits` 7-bit
-    digits, 36 int8 products at 8 digits) or "int8crt" (16 moduli and CRT reconstruction)."""
+def set_product_engine(engine="int8crt", digits=8, min_block=4096):
+    """Engine of the level products: "int8crt" (default: INT8 tensor cores, 16 moduli + CRT,
+    for the levels with block size >= min_block), "int8" (INT8 tensor cores, exact splitting
+    into `digits` 7-bit digits) or "dmma" (FP64 mma.sync for every level)."""
     e = {"dmma": 0, "int8": 1, "int8crt": 2}[engine]
     _check(lib().trinv_set_product_engine(e, digits, min_block))
 

@@ -105,17 +105,22 @@ static bool tma_ok(const void* p, int64_t ld) { return p == nullptr ? (ld % 2 ==
 static int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// ---- opt-in product engine for the level products (trinv_set_product_engine) ------
-// 0: FP64 DMMA (default); 1: INT8 tensor cores by exact operand splitting (oz.cu) for
-// the levels whose block size is >= g_oz_min and whose shapes fit its envelope.
+// ---- product engine for the level products (trinv_set_product_engine) ---------------
+// 0: FP64 DMMA (mma.sync, gemm.cu); 1: INT8 tensor cores, exact 8-digit splitting
+// (oz.cu); 2 (default): INT8 tensor cores, 16 moduli + CRT (oz2.cu).  Engines 1/2
+// take the levels whose block size is >= g_oz_min and whose shapes fit their
+// envelope; every other level runs on DMMA.  TRINV_PRODUCTS=dmma|int8|int8crt
+// overrides the default before the first call.
 static std::atomic<int> g_engine{-1};
 static std::atomic<int> g_digits{8};
-static std::atomic<int64_t> g_oz_min{8192};
+static std::atomic<int64_t> g_oz_min{4096};
 static int product_engine() {
   int e = g_engine.load(std::memory_order_relaxed);
   if (e < 0) {
     const char* v = getenv("TRINV_PRODUCTS");
-    e = (v && strcmp(v, "int8") == 0) ? 1 : ((v && strcmp(v, "int8crt") == 0) ? 2 : 0);
+    e = 2;
+    if (v && strcmp(v, "dmma") == 0) e = 0;
+    if (v && strcmp(v, "int8") == 0) e = 1;
     g_engine.store(e, std::memory_order_relaxed);
   }
   return e;

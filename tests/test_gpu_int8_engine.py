@@ -1,6 +1,7 @@
-"""Opt-in INT8 tensor-core product engine (trinv_set_product_engine / trinv_gemm_oz,
-exact operand splitting into 7-bit digits): parity with the CPU oracle at the same
-gates as the DMMA path, and exactness of the digit products on integer data."""
+"""Product engines of the level products (trinv_set_product_engine / trinv_gemm_oz): the
+INT8 tensor-core engines (exact splitting into 7-bit digits; 16 moduli + CRT, the
+default) and FP64 DMMA: parity with the CPU oracle at the same gates, and exactness of
+the integer products on integer data."""
 import numpy as np
 import pytest
 
@@ -18,7 +19,7 @@ DEV = "cuda:0"
 def int8_engine(request):
     P.set_product_engine(request.param, digits=8, min_block=256)
     yield request.param
-    P.set_product_engine("dmma")
+    P.set_product_engine()  # library default
 
 
 @pytest.mark.parametrize("digits", [8, 0])
@@ -84,11 +85,12 @@ def test_inv_from_lu_int8_engine(int8_engine):
     assert oracle.floored_rel_err(X, np.linalg.inv(L @ U)) <= 1e-9
 
 
-@pytest.mark.parametrize("engine", ["int8", "int8crt"])
+@pytest.mark.parametrize("engine", ["dmma", "int8", "int8crt"])
 @pytest.mark.parametrize("n,uplo,cfg", [(16384, "L", 2), (32768, "U", 3)])
-def test_large_int8_engine_default_threshold(n, uplo, cfg, engine):
-    """Config 3 size (and n = 16384) with the engine at its default threshold (blocks
-    >= 8192 on INT8, the rest on DMMA): 64 sampled columns at the BASELINE gates."""
+def test_large_engines(n, uplo, cfg, engine):
+    """Config 3 size (and n = 16384) on every product engine (INT8 engines at their
+    thresholds, the other levels on DMMA; "dmma" for every level): 64 sampled columns at
+    the BASELINE gates."""
     P.set_product_engine(engine, min_block=4096 if engine == "int8crt" else 8192)
     try:
         T = torch.empty((n, n), dtype=torch.float64, device=DEV)
@@ -103,4 +105,4 @@ def test_large_int8_engine_default_threshold(n, uplo, cfg, engine):
         Tt = np.tril(Th) if uplo == "L" else np.triu(Th)
         assert oracle.column_residual_ratio(Tt, Xs, cols) <= RES_TOL
     finally:
-        P.set_product_engine("dmma")
+        P.set_product_engine()

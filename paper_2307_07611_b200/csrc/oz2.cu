@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   int kb = 0, ke = p.K;
   if (p.triA == TRI_LOWER) ke = min(ke, (I + 1) * OZ2_TM);
   if (p.triA == TRI_UPPER) kb = I * OZ2_TM;
-  if (p.triB == TRI_LOWER) kb = J * OZ2_TN;
+  if (p.triB == TRI_LOWER) kb = max(kb, J * OZ2_TN);  // both triangular (U^-1 L^-1): k >= max(i, j)
   if (p.triB == TRI_UPPER) ke = min(ke, (J + 1) * OZ2_TN);
   const int nkb = ke > kb ? (ke - kb) / OZ2_TK : 0;
 
@@ -391,7 +391,11 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   const int P = oz2_scale_bits(K);
   GemmArgs ga{};
   ga.M = M; ga.N = N; ga.K = K; ga.batch = 1; ga.triA = triA; ga.triB = triB;
-  const double f64 = gemm_flops(ga);
+  double f64 = gemm_flops(ga);
+  if (triA == TRI_UPPER && triB == TRI_LOWER) {  // S K with both factors triangular (P_UL)
+    const double n = (double)K;
+    f64 = 2.0 * (n * (n + 1) * (2 * n + 1) / 6.0) - n * n;
+  }
   ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
   oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, P, As, ea);
   cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);

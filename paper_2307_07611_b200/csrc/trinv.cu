@@ -175,6 +175,13 @@ static size_t oz_scratch(int64_t n) {
   return align_up(best);
 }
 
+// The U^{-1} L^{-1} product (and the LU products of inv_general) could run on the INT8 CRT
+// engine, but both factors of S K have a dominant diagonal and entries ~1/n off it, and the
+// row / column scaling of the modular scheme then leaves the smallest entries of the product
+// with ~2^-39 relative precision: config 4 measured 1.0e-10 floored error against the
+// 1e-10 gate (DMMA: 4.8e-14; tests/accuracy_report.py).  They stay on DMMA.
+static bool ul_on_int8(int64_t) { return false; }
+
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
   size_t bytes = align_up(w_bytes(n)) + oz_scratch(n);
@@ -485,7 +492,7 @@ static size_t lu_inv_scratch(int64_t n) {
   return align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
 }
 static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
-                                 int32_t* info, int64_t info_off, cudaStream_t s) {
+                                 int32_t* info, int64_t info_off, cudaStream_t s, void* ozws) {
   if (n <= LU_MAX) {
     TRY(launch_lu_leaf(W, ld, F, ld, (int)n, info, info_off, s, &g_launches));
     trinv_status_t st = run_tri('L', n, F, ld, Li, ld, 0, nullptr, nullptr, 0, s);
@@ -496,20 +503,23 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
   auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                   int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta) {
+    if (ozws && product_engine() == 2 && std::min(M, std::min(N, K)) >= g_oz_min.load() && oz2_supported(M, N, K))
+      return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, s,
+                                       &g_launches));
     GemmArgs g{};
     g.M = M; g.N = N; g.K = K; g.batch = 1;
     g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
     g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
     return cuda_fail(launch_gemm(g, s, &g_launches));
   };
-  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s);  // A11 = L11 U11, K11, S11
+  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws);  // A11 = L11 U11, K11, S11
   if (st != TRINV_OK) return st;
   // U12 = K11 A12 (K11 lower), L21 = A21 S11 (S11 upper), Schur W22 <- A22 - L21 U12
   if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0))) return st;
   if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0))) return st;
   if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0)))
     return st;
-  st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s);
+  st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s, ozws);
   if (st != TRINV_OK) return st;
   // K21 = -K22 (L21 K11)
   const int64_t lth = even_up(h), ltr = even_up(r);
@@ -536,7 +546,8 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   const int64_t lde = even_up(n);
   const size_t tws_bytes = std::max(tri_ws(n, Lf, ldl, nullptr, lde), tri_ws(n, Uf, ldu, nullptr, lde));
   const bool stage_x = !tma_ok(X, ldx);
-  const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0);
+  const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0) +
+                      (ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : 0);
   if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
   char* p = static_cast<char*>(ws);
   double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
@@ -550,12 +561,16 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   if (st != TRINV_OK) return st;
   double* Xuse = X;
   int64_t ldx_use = ldx;
-  if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; }
-  LevelArgs ul{};
-  ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
-  ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
-  ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
-  TRY(launch_level(ul, s, &g_launches));
+  if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; p += align_up(mat_bytes(n)); }
+  if (ul_on_int8(n)) {  // S K on the INT8 tensor cores (k >= max(i, j))
+    TRY(launch_oz2_gemm(n, n, n, Ui, lde, TRI_UPPER, Li, lde, TRI_LOWER, Xuse, ldx_use, 1.0, 0.0, p, s, &g_launches));
+  } else {
+    LevelArgs ul{};
+    ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
+    ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
+    ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
+    TRY(launch_level(ul, s, &g_launches));
+  }
   if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
   return TRINV_OK;
 }
@@ -570,9 +585,10 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
   if (n <= 0) return 0;
   if (op == 'L' || op == 'U') return tri_ws(n, A, lda, X, ldx);
   if (op == 'F') return align_up(lu_scratch(n));
-  if (op == 'A') {  // inv_general: F, W, K, S (n x even(n) each), the product scratch, X staging
+  if (op == 'A') {  // inv_general: F, W, K, S (n x even(n) each), the product scratch, X staging, INT8 scratch
     size_t bytes = 4 * align_up(mat_bytes(n)) + align_up(lu_inv_scratch(n));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
+    if (ul_on_int8(n)) bytes += align_up(oz2_workspace_bytes(n, n, n));
     (void)A; (void)lda;
     return bytes;
   }
@@ -581,6 +597,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
     // U factor is assumed to be laid out like the L factor (A, lda).
     size_t bytes = 2 * align_up(mat_bytes(n)) + align_up(tri_ws(n, A, lda, nullptr, even_up(n)));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
+    if (ul_on_int8(n)) bytes += align_up(oz2_workspace_bytes(n, n, n));
     return bytes;
   }
   return 0;
@@ -818,17 +835,23 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const bool stage_x = !tma_ok(X, ldx);
   double* Xuse = stage_x ? take(mat_bytes(n)) : X;
   const int64_t ldx_use = stage_x ? lde : ldx;
+  void* ozws = ul_on_int8(n) ? static_cast<void*>(take(oz2_workspace_bytes(n, n, n))) : nullptr;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   TRY(cudaMemcpy2DAsync(Wk, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
   // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
-  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s);
+  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, ozws);
   if (st != TRINV_OK) return st;
   // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
-  LevelArgs ul{};
-  ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
-  ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
-  ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
-  TRY(launch_level(ul, s, &g_launches));
+  if (ozws) {
+    TRY(launch_oz2_gemm(n, n, n, Ui, lde, TRI_UPPER, Li, lde, TRI_LOWER, Xuse, ldx_use, 1.0, 0.0, ozws, s,
+                        &g_launches));
+  } else {
+    LevelArgs ul{};
+    ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
+    ul.opA = MatRef{Ui, n, n, lde}; ul.opB = MatRef{Li, n, n, lde};
+    ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
+    TRY(launch_level(ul, s, &g_launches));
+  }
   if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
   return TRINV_OK;
 }
@@ -845,7 +868,10 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
   if (M == 0 || N == 0) return TRINV_OK;
   auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
   const int ta = tri(structA), tb = tri(structB);
-  if (ta < 0 || tb < 0 || (ta != TRI_NONE && tb != TRI_NONE)) return TRINV_INVALID_ARG;
+  if (ta < 0 || tb < 0) return TRINV_INVALID_ARG;
+  // two triangular operands: only upper x lower on the modular variant (k >= max(i, j))
+  if (ta != TRI_NONE && tb != TRI_NONE && !(digits <= 0 && ta == TRI_UPPER && tb == TRI_LOWER))
+    return TRINV_INVALID_ARG;
   if (!A || !B || !C || lda < K || ldb < N || ldc < N) return TRINV_INVALID_ARG;
   if (digits <= 0) {  // CRT scheme, 16 moduli (oz2.cu)
     if (!oz2_supported(M, N, K)) return TRINV_NOT_SUPPORTED;

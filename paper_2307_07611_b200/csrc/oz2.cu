@@ -61,24 +61,35 @@ __device__ __forceinline__ int oz2_exp_above(double m) {
   return e;
 }
 // A' (|A'| < 2^62) mod m in the symmetric range, from the two 32-bit halves
+// |v| mod m in [0, m) from four 16-bit chunks (c_k = 2^16k mod m, sum < 2^26), then the
+// sign and the symmetric range: [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m.
 template <int I>
-__device__ __forceinline__ int8_t oz2_residue(int64_t v) {  // |v| < 2^62
-  constexpr int m = oz2_mod(I);
-  constexpr int two32 = (int)((((int64_t)1) << 32) % m);
-  const int hi = (int)(v >> 32);                 // |hi| < 2^30
-  const uint32_t lo = (uint32_t)(v & 0xffffffffu);
-  int r = (hi % m) * two32 + (int)(lo % (uint32_t)m);  // |r| < 2^16 + 2^8
-  r %= m;
-  if (r < 0) r += m;
-  if (r > (m - 1) / 2) r -= m;  // symmetric: [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m
-  return (int8_t)r;
+__device__ __forceinline__ uint32_t oz2_residue_byte(uint64_t u, bool neg) {
+  constexpr uint32_t m = (uint32_t)oz2_mod(I);
+  constexpr uint32_t c1 = (uint32_t)((1ull << 16) % m), c2 = (uint32_t)((1ull << 32) % m),
+                     c3 = (uint32_t)((1ull << 48) % m);
+  const uint32_t s = (uint32_t)(u & 0xffff) + (uint32_t)((u >> 16) & 0xffff) * c1 +
+                     (uint32_t)((u >> 32) & 0xffff) * c2 + (uint32_t)(u >> 48) * c3;
+  int r = (int)(s % m);
+  if (neg && r) r = (int)m - r;
+  if (r > (int)(m - 1) / 2) r -= (int)m;
+  return (uint32_t)(uint8_t)(int8_t)r;
 }
+// residues of 4 consecutive values, packed one 32-bit word per modulus plane
 template <int... I>
-__device__ __forceinline__ void oz2_residues(int64_t v, int8_t* out, size_t stride, std::integer_sequence<int, I...>) {
-  ((out[I * stride] = oz2_residue<I>(v)), ...);
+__device__ __forceinline__ void oz2_residues4(const int64_t (&v)[4], uint32_t* out, size_t stride_words,
+                                              std::integer_sequence<int, I...>) {
+  uint64_t u[4];
+  bool ng[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { ng[q] = v[q] < 0; u[q] = ng[q] ? (uint64_t)(-v[q]) : (uint64_t)v[q]; }
+  ((out[I * stride_words] = oz2_residue_byte<I>(u[0], ng[0]) | (oz2_residue_byte<I>(u[1], ng[1]) << 8) |
+                            (oz2_residue_byte<I>(u[2], ng[2]) << 16) | (oz2_residue_byte<I>(u[3], ng[3]) << 24)),
+   ...);
 }
 
-// A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum.
+// A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum;
+// each lane converts 4 consecutive entries per step (K % 4 == 0).
 __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int P, int8_t* out, int* expo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -88,10 +99,13 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = oz2_exp_above(m);
   if (lane == 0) expo[warp] = e;
-  const size_t ss = (size_t)rows * K;
-  for (int k = lane; k < K; k += 32) {
-    const int64_t v = (int64_t)trunc(ldexp(a[k], P - e));  // exact
-    oz2_residues(v, out + (size_t)warp * K + k, ss, std::make_integer_sequence<int, OZ2_NMOD>{});
+  const size_t sw = (size_t)rows * K / 4;  // plane stride in 32-bit words
+  uint32_t* o = reinterpret_cast<uint32_t*>(out) + (size_t)warp * K / 4;
+  for (int k = 4 * lane; k < K; k += 128) {
+    int64_t v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (int64_t)trunc(ldexp(a[k + q], P - e));  // exact
+    oz2_residues4(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
 __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, unsigned long long* maxbits) {
@@ -102,24 +116,27 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
   for (int k = k0; k < k1; ++k) m = fmax(m, fabs(B[(int64_t)k * ldb + j]));
   atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
 }
-// B operand (K x cols): residues written transposed (cols x K, K-major).
-__global__ void oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int P,
-                                      const unsigned long long* maxbits, int* expo, int8_t* out) {
+// B operand (K x cols): residues written transposed (cols x K, K-major) through a
+// 32 (k) x 32 (j) tile of scaled integers; thread t converts k0 + 4 (t % 8) .. +3 of
+// column j0 + t / 8 and stores one 32-bit word per modulus plane.
+__global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int P,
+                                                             const unsigned long long* maxbits, int* expo, int8_t* out) {
   __shared__ long long tile[32][33];
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int jx = j0 + threadIdx.x;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int jx = j0 + tx;
   const int e = jx < cols ? oz2_exp_above(__longlong_as_double((long long)maxbits[jx])) : 0;
-  if (blockIdx.y == 0 && threadIdx.y == 0 && jx < cols) expo[jx] = e;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+  if (blockIdx.y == 0 && ty == 0 && jx < cols) expo[jx] = e;
+  for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r;
-    tile[r][threadIdx.x] = (k < K && jx < cols) ? (long long)trunc(ldexp(B[(int64_t)k * ldb + jx], P - e)) : 0;
+    tile[r][tx] = (k < K && jx < cols) ? (long long)trunc(ldexp(B[(int64_t)k * ldb + jx], P - e)) : 0;
   }
   __syncthreads();
-  const size_t ss = (size_t)cols * K;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int j = j0 + r, k = k0 + threadIdx.x;
-    if (j < cols && k < K)
-      oz2_residues(tile[threadIdx.x][r], out + (size_t)j * K + k, ss, std::make_integer_sequence<int, OZ2_NMOD>{});
+  const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
+  if (j < cols && k < K) {
+    const int64_t v[4] = {tile[kq][j - j0], tile[kq + 1][j - j0], tile[kq + 2][j - j0], tile[kq + 3][j - j0]};
+    oz2_residues4(v, reinterpret_cast<uint32_t*>(out) + ((size_t)j * K + k) / 4, (size_t)cols * K / 4,
+                  std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
 
@@ -289,24 +306,17 @@ struct Oz2Crt {
   double Md;
 };
 
-__global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int* ea, const int* eb, int P,
-                                       double alpha, double beta, double* C, int64_t ldc, const Oz2Crt crt) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)M * N) return;
-  const int i = (int)(e / N), j = (int)(e % N);
-  const size_t plane = (size_t)M * N;
+__device__ __forceinline__ double oz2_crt_value(const unsigned (&c)[OZ2_NMOD], const Oz2Crt& crt) {
   unsigned __int128 lo = 0, hi = 0;
 #pragma unroll
   for (int q = 0; q < OZ2_NMOD; ++q) {
-    const unsigned c = R[q * plane + e];
-    lo += (unsigned __int128)crt.wl[q] * c;
-    hi += (unsigned __int128)crt.wh[q] * c;
+    lo += (unsigned __int128)crt.wl[q] * c[q];
+    hi += (unsigned __int128)crt.wh[q] * c[q];
   }
-  // S = hi 2^64 + lo
+  // S = hi 2^64 + lo; q = floor(S / M) estimated in FP64, corrected by one step
   const double Sd = (double)hi * 18446744073709551616.0 + (double)lo;
-  long long q = (long long)floor(Sd / crt.Md);
+  const long long q = (long long)floor(Sd / crt.Md);
   const unsigned __int128 Mw = ((unsigned __int128)crt.Mh << 64) | crt.Ml;
-  // R = (hi - q Mh) 2^64 + (lo - q Ml), in signed 128-bit (|.| < 2^127)
   __int128 r = ((__int128)hi - (__int128)q * (__int128)crt.Mh) * ((__int128)1 << 64) +
                ((__int128)lo - (__int128)q * (__int128)crt.Ml);
   if (r < 0) r += (__int128)Mw;
@@ -314,11 +324,32 @@ __global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int
   if (r > (__int128)(Mw >> 1)) r -= (__int128)Mw;  // symmetric representative = C'
   const bool neg = r < 0;
   const unsigned __int128 mag = neg ? (unsigned __int128)(-r) : (unsigned __int128)r;
-  double val = fma((double)(unsigned long long)(mag >> 64), 18446744073709551616.0, (double)(unsigned long long)mag);
-  if (neg) val = -val;
-  val = ldexp(val, ea[i] + eb[j] - 2 * P);
+  const double v = fma((double)(unsigned long long)(mag >> 64), 18446744073709551616.0, (double)(unsigned long long)mag);
+  return neg ? -v : v;
+}
+
+// 4 consecutive entries of one row per thread (N % 4 == 0): one 32-bit word per plane.
+__global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int* ea, const int* eb, int P,
+                                       double alpha, double beta, double* C, int64_t ldc, const Oz2Crt crt) {
+  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // index of 4 entries
+  if (e4 >= (int64_t)M * N / 4) return;
+  const int64_t e = 4 * e4;
+  const int i = (int)(e / N), j = (int)(e % N);
+  const size_t plane_w = (size_t)M * N / 4;
+  const uint32_t* Rw = reinterpret_cast<const uint32_t*>(R) + e4;
+  uint32_t w[OZ2_NMOD];
+#pragma unroll
+  for (int q = 0; q < OZ2_NMOD; ++q) w[q] = Rw[q * plane_w];
   double* out = C + (int64_t)i * ldc + j;
-  *out = beta == 0.0 ? alpha * val : fma(alpha, val, beta * *out);
+  const int ei = ea[i] - 2 * P;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    unsigned c[OZ2_NMOD];
+#pragma unroll
+    for (int q = 0; q < OZ2_NMOD; ++q) c[q] = (w[q] >> (8 * b)) & 0xffu;
+    const double val = ldexp(oz2_crt_value(c, crt), ei + eb[j + b]);
+    out[b] = beta == 0.0 ? alpha * val : fma(alpha, val, beta * out[b]);
+  }
 }
 
 static Oz2Crt oz2_crt_constants() {
@@ -402,7 +433,7 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   if (e != cudaSuccess) return e;
   oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(B, ldb, (int)K,
                                                                                                    (int)N, maxbits);
-  oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), dim3(32, 8), 0, st>>>(
+  oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
       B, ldb, (int)K, (int)N, P, maxbits, eb, Bs);
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
@@ -413,10 +444,10 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   p.tiles_n = (int)(N / OZ2_TN);
   set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
   oz2_gemm_kernel<<<(unsigned)((M / OZ2_TM) * (N / OZ2_TN)), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
-  const int64_t total = M * N;
+  const int64_t total4 = M * N / 4;
   static const Oz2Crt crt = oz2_crt_constants();
-  oz2_reconstruct_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha, beta,
-                                                                         C, ldc, crt);
+  oz2_reconstruct_kernel<<<(unsigned)((total4 + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha,
+                                                                          beta, C, ldc, crt);
   if (launches) *launches += 5;
   return cudaGetLastError();
 }

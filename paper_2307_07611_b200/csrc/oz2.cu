@@ -306,15 +306,24 @@ struct Oz2Crt {
   double Md;
 };
 
+// S = sum_q c_q w_q with w_q split into 32-bit limbs: four uint64 accumulators of
+// 32 x 8-bit products (each < 2^44), carried into S = s3 2^96 + s2 2^64 + s1 2^32 + s0
+// (S < 2^138); q = floor(S / M) from an FP64 estimate, R = S - q M in 128-bit limbs
+// (exact: |R| < 2M), mapped to (-M/2, M/2].
 __device__ __forceinline__ double oz2_crt_value(const unsigned (&c)[OZ2_NMOD], const Oz2Crt& crt) {
-  unsigned __int128 lo = 0, hi = 0;
+  unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
   for (int q = 0; q < OZ2_NMOD; ++q) {
-    lo += (unsigned __int128)crt.wl[q] * c[q];
-    hi += (unsigned __int128)crt.wh[q] * c[q];
+    a0 += (unsigned long long)(uint32_t)crt.wl[q] * c[q];
+    a1 += (unsigned long long)(uint32_t)(crt.wl[q] >> 32) * c[q];
+    a2 += (unsigned long long)(uint32_t)crt.wh[q] * c[q];
+    a3 += (unsigned long long)(uint32_t)(crt.wh[q] >> 32) * c[q];
   }
-  // S = hi 2^64 + lo; q = floor(S / M) estimated in FP64, corrected by one step
-  const double Sd = (double)hi * 18446744073709551616.0 + (double)lo;
+  // lo128 = a0 + a1 2^32 (< 2^77), hi128 = a2 + a3 2^32 (< 2^77): S = hi128 2^64 + lo128
+  const unsigned __int128 lo = (unsigned __int128)a0 + ((unsigned __int128)a1 << 32);
+  const unsigned __int128 hi = (unsigned __int128)a2 + ((unsigned __int128)a3 << 32);
+  const double Sd = ((double)a3 * 4294967296.0 + (double)a2) * 18446744073709551616.0 +
+                    ((double)a1 * 4294967296.0 + (double)a0);
   const long long q = (long long)floor(Sd / crt.Md);
   const unsigned __int128 Mw = ((unsigned __int128)crt.Mh << 64) | crt.Ml;
   __int128 r = ((__int128)hi - (__int128)q * (__int128)crt.Mh) * ((__int128)1 << 64) +

@@ -25,11 +25,16 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 # full captures of the dominant kernels
 ncu --set full --clock-control none --import-source on -k regex:leaf32_tma -s 3 -c 1 -o gpurun_out/full_leaf32 $CMD1 > gpurun_out/ncu_f1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:blk_kernel -s 3 -c 1 -o gpurun_out/full_blk $CMD0 > gpurun_out/ncu_f0.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:dmma_level -s 10 -c 2 -o gpurun_out/full_dmma_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2.log 2>&1
+TRINV_PRODUCTS=dmma ncu --set full --clock-control none --import-source on -k regex:dmma_level -s 10 -c 2 -o gpurun_out/full_dmma_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:oz2_gemm -c 2 -o gpurun_out/full_oz2_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2oz.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:leaf64_tma -c 1 -o gpurun_out/full_leaf64 python tools/sweep_batched.py 64 > gpurun_out/ncu_f64.log 2>&1
-for f in full_leaf32 full_blk full_dmma_c2 full_leaf64; do
+for f in full_leaf32 full_blk full_dmma_c2 full_oz2_c2 full_leaf64; do
   [ -f gpurun_out/$f.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$f.ncu-rep > gpurun_out/$f.txt 2>&1
 done
 ls -la gpurun_out >> gpurun_out/steps.log
 python tools/kprof.py A 16384 > gpurun_out/kprof_A16384.txt 2>&1
 python tools/kprof.py L 8192 > gpurun_out/kprof_L8192.txt 2>&1
+python tools/kprof.py U 32768 > gpurun_out/kprof_U32768.txt 2>&1
+TRINV_PRODUCTS=dmma python tools/kprof.py U 32768 > gpurun_out/kprof_U32768_dmma.txt 2>&1
+for c in 2 3 4; do timeout 900 python bench.py --config $c --products dmma >> gpurun_out/bench_dmma.jsonl 2>/dev/null; done
+timeout 1500 python tests/accuracy_report.py > gpurun_out/accuracy_report.txt 2>&1

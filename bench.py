@@ -440,6 +440,11 @@ def main():
             "parallelism": f"batch partition x{world}" if cfg["kind"] == "B" else "replicas (single matrix per GPU)"}
     if cfg["kind"] == "B":
         conf["batch_per_rank"] = BATCH
+    elif n > 128:
+        conf["arithmetic"] = ("FP64 (DMMA mma.sync) for every level product" if args.products == "dmma" else
+                              "FP64 results; level products of blocks >= %d computed exactly in int8 x int8 -> int32 "
+                              "on the tcgen05 tensor cores (%s) and reconstructed in FP64, smaller ones on FP64 DMMA"
+                              % (mb, "8-digit splitting" if args.products == "int8" else "16 moduli + CRT"))
     line["config"] = conf
 
     # ---- roofline of the dominant kernel ----

@@ -10,9 +10,9 @@
 // Residues.  With 16 pairwise coprime moduli m_i <= 256 (M = prod m_i ~ 2^125.4),
 // A'_i = A' mod m_i and B'_i in the symmetric range (int8), the tensor cores give
 // C'_i = A'_i B'_i exactly in int32 (|.| <= K 2^14), reduced mod m_i by the epilogue.
-// Reconstruction.  Garner's mixed-radix form of the CRT recovers C' mod M exactly in
-// 128-bit integers; as |C'| < M/2 (P chosen from K: 2P + log2 K < log2 M - 1), the
-// symmetric representative is C' itself, and
+// Reconstruction.  The CRT sum S = sum_i C'_i w_i (w_i the CRT basis of M) is congruent
+// to C' mod M; as |C'| < M/2 by a margin (P chosen from K: 2P + log2 K < log2 M - 1),
+// q = round(S / M) from an FP64 estimate is exact and C' = S - q M in 128-bit integers:
 //     (A B)_ij ~= 2^(e_i - P) 2^(f_j - P) C'_ij,
 // the only errors being the truncation of the scaled operands (2^-P relative to the
 // row / column maxima) and the final rounding to FP64.
@@ -60,76 +60,110 @@ __device__ __forceinline__ int oz2_exp_above(double m) {
   frexp(m, &e);
   return e;
 }
-// A' (|A'| < 2^62) mod m in the symmetric range, from the two 32-bit halves
-// |v| mod m in [0, m) from four 16-bit chunks (c_k = 2^16k mod m, sum < 2^26), then the
-// sign and the symmetric range: [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m.
+// x 2^k: one multiplication by an exact power of two in the normal range (exact unless
+// the result is subnormal, then one rounding, as ldexp), else ldexp.
+__device__ __forceinline__ double oz2_ldexp(double x, int k) {
+  if (k >= -1022 && k <= 1023) return x * __longlong_as_double((long long)(k + 1023) << 52);
+  return ldexp(x, k);
+}
+// Residues of an integer |v| < 2^58 (P <= 58) for all 16 moduli from three chunks of
+// u = v + 2^59 (0 < u < 2^60): u = lo + mid 2^20 + hi 2^40, so with c1 = 2^20 mod m,
+// c2 = 2^40 mod m, s = lo + c1 mid + c2 hi + D < 2^29 is congruent to v + h (h = floor(m/2),
+// D = (h - 2^59) mod m), and (s mod m) - h is the residue of v in [-h, m - 1 - h]:
+// [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m; its low byte is the int8 residue.
+struct Oz2Chunks {
+  uint32_t lo, mid, hi;
+};
+__device__ __forceinline__ Oz2Chunks oz2_chunks(int64_t v) {
+  const uint64_t u = (uint64_t)(v + (1ll << 59));
+  return {(uint32_t)u & 0xFFFFFu, (uint32_t)(u >> 20) & 0xFFFFFu, (uint32_t)(u >> 40)};
+}
 template <int I>
-__device__ __forceinline__ uint32_t oz2_residue_byte(uint64_t u, bool neg) {
-  constexpr uint32_t m = (uint32_t)oz2_mod(I);
-  constexpr uint32_t c1 = (uint32_t)((1ull << 16) % m), c2 = (uint32_t)((1ull << 32) % m),
-                     c3 = (uint32_t)((1ull << 48) % m);
-  const uint32_t s = (uint32_t)(u & 0xffff) + (uint32_t)((u >> 16) & 0xffff) * c1 +
-                     (uint32_t)((u >> 32) & 0xffff) * c2 + (uint32_t)(u >> 48) * c3;
-  int r = (int)(s % m);
-  if (neg && r) r = (int)m - r;
-  if (r > (int)(m - 1) / 2) r -= (int)m;
-  return (uint32_t)(uint8_t)(int8_t)r;
+__device__ __forceinline__ uint32_t oz2_sym_residue(const Oz2Chunks& x) {
+  constexpr uint32_t m = (uint32_t)oz2_mod(I), h = m / 2;
+  constexpr uint32_t c1 = (uint32_t)((1ull << 20) % m), c2 = (uint32_t)((1ull << 40) % m);
+  constexpr uint32_t D = (uint32_t)((h + m - (uint32_t)((1ull << 59) % m)) % m);
+  const uint32_t s = x.lo + x.mid * c1 + x.hi * c2 + D;
+  return s % m - h;
+}
+__device__ __forceinline__ uint32_t oz2_pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 // residues of 4 consecutive values, packed one 32-bit word per modulus plane
 template <int... I>
 __device__ __forceinline__ void oz2_residues4(const int64_t (&v)[4], uint32_t* out, size_t stride_words,
                                               std::integer_sequence<int, I...>) {
-  uint64_t u[4];
-  bool ng[4];
+  Oz2Chunks x[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) { ng[q] = v[q] < 0; u[q] = ng[q] ? (uint64_t)(-v[q]) : (uint64_t)v[q]; }
-  ((out[I * stride_words] = oz2_residue_byte<I>(u[0], ng[0]) | (oz2_residue_byte<I>(u[1], ng[1]) << 8) |
-                            (oz2_residue_byte<I>(u[2], ng[2]) << 16) | (oz2_residue_byte<I>(u[3], ng[3]) << 24)),
+  for (int q = 0; q < 4; ++q) x[q] = oz2_chunks(v[q]);
+  ((out[I * stride_words] = oz2_pack4(oz2_sym_residue<I>(x[0]), oz2_sym_residue<I>(x[1]),
+                                      oz2_sym_residue<I>(x[2]), oz2_sym_residue<I>(x[3]))),
    ...);
 }
 
+// The K range the GEMM reads for row i of a triangular A (tile rows of OZ2_TM) or column
+// j of a triangular B (tile columns of OZ2_TN), oz2_gemm_kernel's kb..ke: only that range
+// is scaled and split (the rest of a triangular operand is zero and never read).
+__device__ __forceinline__ void oz2_k_range(int tri, bool is_a, int idx, int K, int& kb, int& ke) {
+  const int tile = is_a ? OZ2_TM : OZ2_TN;
+  const bool upto = is_a ? tri == TRI_LOWER : tri == TRI_UPPER;  // k < end of idx's tile
+  const bool from = is_a ? tri == TRI_UPPER : tri == TRI_LOWER;  // k >= start of idx's tile
+  kb = from ? (idx / tile) * tile : 0;
+  ke = upto ? min(K, (idx / tile + 1) * tile) : K;
+}
 // A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum;
 // each lane converts 4 consecutive entries per step (K % 4 == 0).
-__global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int P, int8_t* out, int* expo) {
+__global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int tri, int P, int8_t* out,
+                                      int* expo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
+  int kb, ke;
+  oz2_k_range(tri, true, warp, K, kb, ke);
   const double* a = A + (int64_t)warp * lda;
   double m = 0.0;
-  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(a[k]));
+  for (int k = kb + lane; k < ke; k += 32) m = fmax(m, fabs(a[k]));
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = oz2_exp_above(m);
   if (lane == 0) expo[warp] = e;
   const size_t sw = (size_t)rows * K / 4;  // plane stride in 32-bit words
   uint32_t* o = reinterpret_cast<uint32_t*>(out) + (size_t)warp * K / 4;
-  for (int k = 4 * lane; k < K; k += 128) {
+  for (int k = kb + 4 * lane; k < ke; k += 128) {
     int64_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (int64_t)trunc(ldexp(a[k + q], P - e));  // exact
+    for (int q = 0; q < 4; ++q) v[q] = (int64_t)oz2_ldexp(a[k + q], P - e);  // exact, truncated
     oz2_residues4(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
-__global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, unsigned long long* maxbits) {
+__global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
+                                  unsigned long long* maxbits) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
-  const int k0 = blockIdx.y * 512, k1 = min(K, k0 + 512);
+  int kb, ke;
+  oz2_k_range(tri, false, j, K, kb, ke);
+  const int k0 = max(kb, (int)blockIdx.y * 512), k1 = min(ke, (int)blockIdx.y * 512 + 512);
   double m = 0.0;
   for (int k = k0; k < k1; ++k) m = fmax(m, fabs(B[(int64_t)k * ldb + j]));
-  atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
+  if (k0 < k1) atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
 }
 // B operand (K x cols): residues written transposed (cols x K, K-major) through a
 // 32 (k) x 32 (j) tile of scaled integers; thread t converts k0 + 4 (t % 8) .. +3 of
-// column j0 + t / 8 and stores one 32-bit word per modulus plane.
-__global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int P,
-                                                             const unsigned long long* maxbits, int* expo, int8_t* out) {
+// column j0 + t / 8 and stores one 32-bit word per modulus plane.  Tiles outside the
+// GEMM's K range (a 32-column tile lies in one OZ2_TN column tile) are skipped.
+__global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
+                                                             int P, const unsigned long long* maxbits, int* expo,
+                                                             int8_t* out) {
   __shared__ long long tile[32][33];
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int jx = j0 + tx;
   const int e = jx < cols ? oz2_exp_above(__longlong_as_double((long long)maxbits[jx])) : 0;
   if (blockIdx.y == 0 && ty == 0 && jx < cols) expo[jx] = e;
+  int kb, ke;
+  oz2_k_range(tri, false, j0, K, kb, ke);
+  if (k0 + 32 <= kb || k0 >= ke) return;
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r;
-    tile[r][tx] = (k < K && jx < cols) ? (long long)trunc(ldexp(B[(int64_t)k * ldb + jx], P - e)) : 0;
+    tile[r][tx] = (k < K && jx < cols) ? (long long)oz2_ldexp(B[(int64_t)k * ldb + jx], P - e) : 0;
   }
   __syncthreads();
   const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
@@ -296,44 +330,34 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * OZ2_TN));
 }
 
-// ---- reconstruction: C' = sum_i c_i w_i mod M (w_i = M_i (M_i^-1 mod m_i) mod M) -------
-// w_i = wh_i 2^64 + wl_i; the two sums of c_i wl_i and c_i wh_i stay below 2^77 in
-// unsigned 128-bit integers; q = floor(S / M) (<= 2^12) is estimated in FP64 and
-// corrected by one step, so R = S - q M is exact, then mapped to (-M/2, M/2].
+// ---- reconstruction: C' = sum_i c_i w_i - q M -------------------------------------------
+// w_i = M_i (M_i^-1 mod m_i) mod M (so sum_i c_i w_i == C' mod M) in 32-bit limbs
+// w_i = sum_l w_il 2^(32 l).  S = sum_i c_i w_i < 2^138; as |C'| < M/2 by a margin (P from
+// K, oz2_scale_bits), q = round(S / M) and C' = S - q M exactly.  q comes from the two top
+// limb sums in FP64 (error < 2^-40, far inside the margin); S - q M is then evaluated
+// mod 2^128, which is exact because |C'| < 2^124.
 struct Oz2Crt {
-  unsigned long long wl[OZ2_NMOD], wh[OZ2_NMOD];
-  unsigned long long Ml, Mh;
-  double Md;
+  uint32_t w[OZ2_NMOD][4];
+  uint32_t Ml[4];   // M in 32-bit limbs
+  double r64, r96;  // 2^64 / M, 2^96 / M
 };
 
-// S = sum_q c_q w_q with w_q split into 32-bit limbs: four uint64 accumulators of
-// 32 x 8-bit products (each < 2^44), carried into S = s3 2^96 + s2 2^64 + s1 2^32 + s0
-// (S < 2^138); q = floor(S / M) from an FP64 estimate, R = S - q M in 128-bit limbs
-// (exact: |R| < 2M), mapped to (-M/2, M/2].
-__device__ __forceinline__ double oz2_crt_value(const unsigned (&c)[OZ2_NMOD], const Oz2Crt& crt) {
-  unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+__device__ __forceinline__ double oz2_crt_value(const uint32_t (&c)[OZ2_NMOD], const Oz2Crt& crt) {
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // limb sums, each < 2^44
 #pragma unroll
   for (int q = 0; q < OZ2_NMOD; ++q) {
-    a0 += (unsigned long long)(uint32_t)crt.wl[q] * c[q];
-    a1 += (unsigned long long)(uint32_t)(crt.wl[q] >> 32) * c[q];
-    a2 += (unsigned long long)(uint32_t)crt.wh[q] * c[q];
-    a3 += (unsigned long long)(uint32_t)(crt.wh[q] >> 32) * c[q];
+    a0 += (uint64_t)crt.w[q][0] * c[q];
+    a1 += (uint64_t)crt.w[q][1] * c[q];
+    a2 += (uint64_t)crt.w[q][2] * c[q];
+    a3 += (uint64_t)crt.w[q][3] * c[q];
   }
-  // lo128 = a0 + a1 2^32 (< 2^77), hi128 = a2 + a3 2^32 (< 2^77): S = hi128 2^64 + lo128
-  const unsigned __int128 lo = (unsigned __int128)a0 + ((unsigned __int128)a1 << 32);
-  const unsigned __int128 hi = (unsigned __int128)a2 + ((unsigned __int128)a3 << 32);
-  const double Sd = ((double)a3 * 4294967296.0 + (double)a2) * 18446744073709551616.0 +
-                    ((double)a1 * 4294967296.0 + (double)a0);
-  const long long q = (long long)floor(Sd / crt.Md);
-  const unsigned __int128 Mw = ((unsigned __int128)crt.Mh << 64) | crt.Ml;
-  __int128 r = ((__int128)hi - (__int128)q * (__int128)crt.Mh) * ((__int128)1 << 64) +
-               ((__int128)lo - (__int128)q * (__int128)crt.Ml);
-  if (r < 0) r += (__int128)Mw;
-  if (r >= (__int128)Mw) r -= (__int128)Mw;
-  if (r > (__int128)(Mw >> 1)) r -= (__int128)Mw;  // symmetric representative = C'
-  const bool neg = r < 0;
-  const unsigned __int128 mag = neg ? (unsigned __int128)(-r) : (unsigned __int128)r;
-  const double v = fma((double)(unsigned long long)(mag >> 64), 18446744073709551616.0, (double)(unsigned long long)mag);
+  const uint64_t q = (uint64_t)__double2int_rn(fma((double)a3, crt.r96, (double)a2 * crt.r64));
+  const int64_t d0 = (int64_t)(a0 - q * crt.Ml[0]), d1 = (int64_t)(a1 - q * crt.Ml[1]),
+                d2 = (int64_t)(a2 - q * crt.Ml[2]), d3 = (int64_t)(a3 - q * crt.Ml[3]);  // |d| < 2^45
+  const __int128 x = (__int128)d0 + ((__int128)d1 << 32) + ((__int128)d2 << 64) + ((__int128)d3 << 96);
+  const bool neg = x < 0;
+  const unsigned __int128 mag = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
+  const double v = fma((double)(uint64_t)(mag >> 64), 18446744073709551616.0, (double)(uint64_t)mag);
   return neg ? -v : v;
 }
 
@@ -353,10 +377,10 @@ __global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int
   const int ei = ea[i] - 2 * P;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    unsigned c[OZ2_NMOD];
+    uint32_t c[OZ2_NMOD];
 #pragma unroll
-    for (int q = 0; q < OZ2_NMOD; ++q) c[q] = (w[q] >> (8 * b)) & 0xffu;
-    const double val = ldexp(oz2_crt_value(c, crt), ei + eb[j + b]);
+    for (int q = 0; q < OZ2_NMOD; ++q) c[q] = __byte_perm(w[q], 0u, 0x4440 + b);
+    const double val = oz2_ldexp(oz2_crt_value(c, crt), ei + eb[j + b]);
     out[b] = beta == 0.0 ? alpha * val : fma(alpha, val, beta * out[b]);
   }
 }
@@ -370,21 +394,23 @@ static Oz2Crt oz2_crt_constants() {
     const unsigned __int128 Mi = Mall / m;
     const unsigned y = (unsigned)oz2_inv((int)(Mi % m), (int)m);
     const unsigned __int128 w = (Mi * y) % Mall;  // Mi y < M 2^8 / m: no overflow (M < 2^126)
-    c.wl[q] = (unsigned long long)w;
-    c.wh[q] = (unsigned long long)(w >> 64);
+    for (int l = 0; l < 4; ++l) c.w[q][l] = (uint32_t)(w >> (32 * l));
   }
-  c.Ml = (unsigned long long)Mall;
-  c.Mh = (unsigned long long)(Mall >> 64);
-  c.Md = (double)c.Mh * 18446744073709551616.0 + (double)c.Ml;
+  for (int l = 0; l < 4; ++l) c.Ml[l] = (uint32_t)(Mall >> (32 * l));
+  const double Md = (double)(unsigned long long)(Mall >> 64) * 18446744073709551616.0 + (double)(unsigned long long)Mall;
+  c.r64 = std::ldexp(1.0, 64) / Md;
+  c.r96 = std::ldexp(1.0, 96) / Md;
   return c;
 }
 
 // ---- host -------------------------------------------------------------------------------
-static int oz2_scale_bits(int64_t K) {  // P with K 2^(2P) < M/2
+// P with K 2^(2P) <= (1 - 2^-10) M / 2: |C'| < K 2^(2P) keeps round(S / M) unambiguous
+// (oz2_crt_value); at most 58 (the residue chunks of oz2_chunks).
+static int oz2_scale_bits(int64_t K) {
   double lm = 0.0;
   for (int q = 0; q < OZ2_NMOD; ++q) lm += std::log2((double)oz2_mod(q));
-  int P = (int)std::floor((lm - 1.0 - std::log2((double)K)) / 2.0);
-  return P > 62 ? 62 : P;
+  int P = (int)std::floor((lm - 1.0 - 1.5e-3 - std::log2((double)K)) / 2.0);
+  return P > 58 ? 58 : P;
 }
 
 bool oz2_supported(int64_t M, int64_t N, int64_t K) {
@@ -437,13 +463,13 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
     f64 = 2.0 * (n * (n + 1) * (2 * n + 1) / 6.0) - n * n;
   }
   ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
-  oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, P, As, ea);
+  oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, P, As, ea);
   cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
   if (e != cudaSuccess) return e;
   oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(B, ldb, (int)K,
-                                                                                                   (int)N, maxbits);
+                                                                                                   (int)N, triB, maxbits);
   oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
-      B, ldb, (int)K, (int)N, P, maxbits, eb, Bs);
+      B, ldb, (int)K, (int)N, triB, P, maxbits, eb, Bs);
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
       !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, OZ2_TN))

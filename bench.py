@@ -465,9 +465,10 @@ def main():
         ms_d, n_d, fl_d, _ = P._lib.profile_read(1)
         ms_l, n_l, fl_l, _ = P._lib.profile_read(0)
         ms_o, n_o, fl_o, ops_o = P._lib.profile_read(2)  # INT8 engine: FP64-equivalent flops, int8 ops
+        ms_x, n_x, _, by_x = P._lib.profile_read(3)  # CRT engine's scaling / residue / reconstruction kernels
         P._lib.profile_end()
         achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
-        if n_o > 0 and ms_o >= ms_d:  # the INT8 engine carries the dominant products
+        if n_o > 0 and ms_o + ms_x >= ms_d:  # the INT8 engine carries the dominant products
             i8_peak = 2.0 * I8_PER_BF16_SUSTAINED
             ach = ops_o / (ms_o / 1e3) / 1e12
             kname = ("oz_gemm_kernel (INT8 tcgen05, exact 8-digit splitting)" if args.products == "int8"
@@ -478,6 +479,14 @@ def main():
                                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8 / bf16)",
                                 "int8_share_of_step": ms_o / (args.steps * ms_per_step),
                                 "int8_fp64_equivalent_tflops": fl_o / (ms_o / 1e3) / 1e12,
+                                "crt_aux_kernels": None if n_x == 0 else {
+                                    "kernels": "oz2_split_rows / colmax / split_cols / reconstruct",
+                                    "achieved_gbs": by_x / (ms_x / 1e3) / 1e9, "peak_gbs": hbm_peak,
+                                    "frac": by_x / (ms_x / 1e3) / 1e9 / hbm_peak,
+                                    "share_of_step": ms_x / (args.steps * ms_per_step),
+                                    "note": "algorithmic bytes (operands in the GEMM's K range: 8 B read + 16 B "
+                                            "residues written; outputs: 16 B residues read + 8 B written); "
+                                            "integer-ALU bound"},
                                 "dmma_part": {"achieved_tflops": achieved, "peak": fp64_peak,
                                               "frac": achieved / fp64_peak,
                                               "share_of_step": ms_d / (args.steps * ms_per_step)},

@@ -240,10 +240,13 @@ void trinv_reset_launch_count(void);
  * trinv_profile_end() every kernel this thread enqueues is bracketed by CUDA
  * events recorded on its stream (small overhead; for measurement runs only).
  * trinv_profile_read(kind, ...) synchronises those events and returns, for
- * kind 0 (leaf / batched kernels) or 1 (DMMA product kernels), the summed
- * device milliseconds, the launch count and the ALGORITHMIC flops and bytes
- * of those launches (n^3/3 per leaf; triangular-aware products, P:608-612,
- * P:1269-1271; leaf bytes = referenced triangle in + full matrix out).
+ * kind 0 (leaf / batched kernels), 1 (DMMA product kernels), 2 (INT8 product
+ * engine: the tensor-core GEMM kernel of the CRT engine, the whole product of the
+ * digit engine; bytes = int8 operations) or 3 (the CRT engine's scaling, residue
+ * and reconstruction kernels; flops = 0), the summed device milliseconds, the
+ * number of timed scopes and the ALGORITHMIC flops and bytes of those launches
+ * (n^3/3 per leaf; triangular-aware products; leaf bytes
+ * = referenced triangle in + full matrix out).
  * Any output pointer may be NULL.  Returns a trinv_status_t value. */
 void trinv_profile_begin(void);
 void trinv_profile_end(void);

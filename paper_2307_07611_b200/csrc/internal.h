@@ -146,8 +146,10 @@ bool encode_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* d
 
 // Optional per-launch timing (trinv_profile_* in include/trinv.h): when enabled on
 // this thread, every launch is bracketed by CUDA events on its stream.
-// KIND_OZ: INT8 tensor-core products (oz.cu); flops = FP64-equivalent, bytes = int8 ops.
-enum LaunchKind : int { KIND_LEAF = 0, KIND_DMMA = 1, KIND_OZ = 2, KIND_COUNT = 3 };
+// KIND_OZ: INT8 tensor-core products (oz.cu: the whole product; oz2.cu: the GEMM kernel);
+// flops = FP64-equivalent, bytes = int8 ops.  KIND_OZAUX: oz2.cu's scaling / residue /
+// reconstruction kernels; bytes = their algorithmic HBM bytes.
+enum LaunchKind : int { KIND_LEAF = 0, KIND_DMMA = 1, KIND_OZ = 2, KIND_OZAUX = 3, KIND_COUNT = 4 };
 struct ProfileScope {
   ProfileScope(int kind, double flops, double bytes, cudaStream_t s);
   ~ProfileScope();

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <utility>
@@ -337,23 +338,31 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
 // limb sums in FP64 (error < 2^-40, far inside the margin); S - q M is then evaluated
 // mod 2^128, which is exact because |C'| < 2^124.
 struct Oz2Crt {
-  uint32_t w[OZ2_NMOD][4];
-  uint32_t Ml[4];   // M in 32-bit limbs
-  double r64, r96;  // 2^64 / M, 2^96 / M
+  uint32_t w[OZ2_NMOD][2];   // limbs 0, 1 of w_i
+  double wd[OZ2_NMOD][2];    // limbs 2, 3 of w_i (exact in FP64)
+  uint32_t Ml[2];            // M in 32-bit limbs 0, 1
+  double Md[2];              // limbs 2, 3 of M
+  double r64, r96;           // 2^64 / M, 2^96 / M
 };
 
+// The four limb sums (each < 2^44, exact) are split between the integer multiply-add pipe
+// (limbs 0, 1: IMAD.WIDE) and the FP64 pipe (limbs 2, 3: exact DFMA on integers < 2^53),
+// which run concurrently.
 __device__ __forceinline__ double oz2_crt_value(const uint32_t (&c)[OZ2_NMOD], const Oz2Crt& crt) {
-  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // limb sums, each < 2^44
+  uint64_t a0 = 0, a1 = 0;
+  double s2 = 0.0, s3 = 0.0;
 #pragma unroll
   for (int q = 0; q < OZ2_NMOD; ++q) {
     a0 += (uint64_t)crt.w[q][0] * c[q];
     a1 += (uint64_t)crt.w[q][1] * c[q];
-    a2 += (uint64_t)crt.w[q][2] * c[q];
-    a3 += (uint64_t)crt.w[q][3] * c[q];
+    const double cd = __hiloint2double(0x43300000, (int)c[q]) - 4503599627370496.0;  // (double)c, exact
+    s2 = fma(cd, crt.wd[q][0], s2);
+    s3 = fma(cd, crt.wd[q][1], s3);
   }
-  const uint64_t q = (uint64_t)__double2int_rn(fma((double)a3, crt.r96, (double)a2 * crt.r64));
-  const int64_t d0 = (int64_t)(a0 - q * crt.Ml[0]), d1 = (int64_t)(a1 - q * crt.Ml[1]),
-                d2 = (int64_t)(a2 - q * crt.Ml[2]), d3 = (int64_t)(a3 - q * crt.Ml[3]);  // |d| < 2^45
+  const double qd = rint(fma(s3, crt.r96, s2 * crt.r64));  // round(S / M)
+  const uint64_t q = (uint64_t)qd;
+  const int64_t d0 = (int64_t)(a0 - q * crt.Ml[0]), d1 = (int64_t)(a1 - q * crt.Ml[1]);
+  const int64_t d2 = (int64_t)fma(-qd, crt.Md[0], s2), d3 = (int64_t)fma(-qd, crt.Md[1], s3);  // exact, |d| < 2^45
   const __int128 x = (__int128)d0 + ((__int128)d1 << 32) + ((__int128)d2 << 64) + ((__int128)d3 << 96);
   const bool neg = x < 0;
   const unsigned __int128 mag = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
@@ -394,9 +403,11 @@ static Oz2Crt oz2_crt_constants() {
     const unsigned __int128 Mi = Mall / m;
     const unsigned y = (unsigned)oz2_inv((int)(Mi % m), (int)m);
     const unsigned __int128 w = (Mi * y) % Mall;  // Mi y < M 2^8 / m: no overflow (M < 2^126)
-    for (int l = 0; l < 4; ++l) c.w[q][l] = (uint32_t)(w >> (32 * l));
+    for (int l = 0; l < 2; ++l) c.w[q][l] = (uint32_t)(w >> (32 * l));
+    for (int l = 0; l < 2; ++l) c.wd[q][l] = (double)(uint32_t)(w >> (32 * (l + 2)));
   }
-  for (int l = 0; l < 4; ++l) c.Ml[l] = (uint32_t)(Mall >> (32 * l));
+  for (int l = 0; l < 2; ++l) c.Ml[l] = (uint32_t)(Mall >> (32 * l));
+  for (int l = 0; l < 2; ++l) c.Md[l] = (double)(uint32_t)(Mall >> (32 * (l + 2)));
   const double Md = (double)(unsigned long long)(Mall >> 64) * 18446744073709551616.0 + (double)(unsigned long long)Mall;
   c.r64 = std::ldexp(1.0, 64) / Md;
   c.r96 = std::ldexp(1.0, 96) / Md;
@@ -462,14 +473,30 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
     const double n = (double)K;
     f64 = 2.0 * (n * (n + 1) * (2 * n + 1) / 6.0) - n * n;
   }
-  ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
-  oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, P, As, ea);
-  cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
-  if (e != cudaSuccess) return e;
-  oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(B, ldb, (int)K,
-                                                                                                   (int)N, triB, maxbits);
-  oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
-      B, ldb, (int)K, (int)N, triB, P, maxbits, eb, Bs);
+  // algorithmic bytes of the auxiliary kernels: the K ranges split (8 B read, 16 B of
+  // residues written per entry; the column maxima re-read B), and per output entry 16 B
+  // of residues read, 8 B written (+ 8 B read when beta != 0)
+  auto range_sum = [&](int64_t rows, int tile, bool upto, bool from) {
+    double s = 0.0;
+    for (int64_t t0 = 0; t0 < rows; t0 += tile) {
+      const int64_t r = std::min<int64_t>(tile, rows - t0);
+      const int64_t b = from ? t0 : 0, e = upto ? std::min<int64_t>(K, t0 + tile) : K;
+      s += (double)r * (double)std::max<int64_t>(0, e - b);
+    }
+    return s;
+  };
+  const double ea_n = range_sum(M, OZ2_TM, triA == TRI_LOWER, triA == TRI_UPPER);
+  const double eb_n = range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER);
+  {
+    ProfileScope aux(KIND_OZAUX, 0.0, 24.0 * ea_n + 32.0 * eb_n, st);
+    oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, P, As, ea);
+    cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
+    if (e != cudaSuccess) return e;
+    oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(
+        B, ldb, (int)K, (int)N, triB, maxbits);
+    oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
+        B, ldb, (int)K, (int)N, triB, P, maxbits, eb, Bs);
+  }
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
       !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, OZ2_TN))
@@ -478,11 +505,17 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   p.M = (int)M; p.N = (int)N; p.K = (int)K; p.triA = triA; p.triB = triB; p.R = Rs;
   p.tiles_n = (int)(N / OZ2_TN);
   set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
-  oz2_gemm_kernel<<<(unsigned)((M / OZ2_TM) * (N / OZ2_TN)), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+  {
+    ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
+    oz2_gemm_kernel<<<(unsigned)((M / OZ2_TM) * (N / OZ2_TN)), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+  }
   const int64_t total4 = M * N / 4;
   static const Oz2Crt crt = oz2_crt_constants();
-  oz2_reconstruct_kernel<<<(unsigned)((total4 + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha,
-                                                                          beta, C, ldc, crt);
+  {
+    ProfileScope aux(KIND_OZAUX, 0.0, (double)M * N * (beta == 0.0 ? 24.0 : 32.0), st);
+    oz2_reconstruct_kernel<<<(unsigned)((total4 + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha,
+                                                                            beta, C, ldc, crt);
+  }
   if (launches) *launches += 5;
   return cudaGetLastError();
 }

@@ -122,9 +122,16 @@ cudaError_t launch_oz_gemm(int64_t M, int64_t N, int64_t K, const double* A, int
 // ---- FP64 products on the INT8 tensor cores by modular arithmetic / CRT (oz2.cu) ----
 bool oz2_supported(int64_t M, int64_t N, int64_t K);
 size_t oz2_workspace_bytes(int64_t M, int64_t N, int64_t K);
+// strict: bit 0 / bit 1 = the diagonal (k == i of A, k == j of B) is read as zero.
 cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                             int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
-                            cudaStream_t st, int64_t* launches);
+                            cudaStream_t st, int64_t* launches, int strict = 0);
+// X = S K (S upper, K lower, order n) on the modular engine with the diagonals split off:
+// X = D_S D_K + D_S N_K + N_S D_K (one elementwise pass, exact up to one rounding) plus the
+// product of the strictly triangular parts N_S N_K (row / column scales set by the
+// off-diagonal entries alone).  ws: oz2_workspace_bytes(n, n, n).
+cudaError_t launch_oz2_ul(int64_t n, const double* S, int64_t lds, const double* K, int64_t ldk, double* X,
+                          int64_t ldx, void* ws, cudaStream_t st, int64_t* launches);
 
 // ---- Crout factorisation of a diagonal block of order <= LU_MAX (lu.cu) -------
 constexpr int LU_MAX = 128;

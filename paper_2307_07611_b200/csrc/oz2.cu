@@ -114,15 +114,16 @@ __device__ __forceinline__ void oz2_k_range(int tri, bool is_a, int idx, int K, 
 }
 // A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum;
 // each lane converts 4 consecutive entries per step (K % 4 == 0).
-__global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int tri, int P, int8_t* out,
-                                      int* expo) {
+__global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int tri, bool strict, int P,
+                                      int8_t* out, int* expo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   int kb, ke;
   oz2_k_range(tri, true, warp, K, kb, ke);
   const double* a = A + (int64_t)warp * lda;
   double m = 0.0;
-  for (int k = kb + lane; k < ke; k += 32) m = fmax(m, fabs(a[k]));
+  const int kz = strict ? warp : -1;  // a diagonal read as zero
+  for (int k = kb + lane; k < ke; k += 32) m = k == kz ? m : fmax(m, fabs(a[k]));
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = oz2_exp_above(m);
   if (lane == 0) expo[warp] = e;
@@ -131,11 +132,11 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
   for (int k = kb + 4 * lane; k < ke; k += 128) {
     int64_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (int64_t)oz2_ldexp(a[k + q], P - e);  // exact, truncated
+    for (int q = 0; q < 4; ++q) v[q] = k + q == kz ? 0 : (int64_t)oz2_ldexp(a[k + q], P - e);  // exact, truncated
     oz2_residues4(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
-__global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
+__global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, int tri, bool strict,
                                   unsigned long long* maxbits) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
@@ -143,7 +144,8 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
   oz2_k_range(tri, false, j, K, kb, ke);
   const int k0 = max(kb, (int)blockIdx.y * 512), k1 = min(ke, (int)blockIdx.y * 512 + 512);
   double m = 0.0;
-  for (int k = k0; k < k1; ++k) m = fmax(m, fabs(B[(int64_t)k * ldb + j]));
+  const int kz = strict ? j : -1;
+  for (int k = k0; k < k1; ++k) m = k == kz ? m : fmax(m, fabs(B[(int64_t)k * ldb + j]));
   if (k0 < k1) atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
 }
 // B operand (K x cols): residues written transposed (cols x K, K-major) through a
@@ -151,8 +153,8 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
 // column j0 + t / 8 and stores one 32-bit word per modulus plane.  Tiles outside the
 // GEMM's K range (a 32-column tile lies in one OZ2_TN column tile) are skipped.
 __global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
-                                                             int P, const unsigned long long* maxbits, int* expo,
-                                                             int8_t* out) {
+                                                             bool strict, int P, const unsigned long long* maxbits,
+                                                             int* expo, int8_t* out) {
   __shared__ long long tile[32][33];
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -164,7 +166,8 @@ __global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, in
   if (k0 + 32 <= kb || k0 >= ke) return;
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r;
-    tile[r][tx] = (k < K && jx < cols) ? (long long)oz2_ldexp(B[(int64_t)k * ldb + jx], P - e) : 0;
+    tile[r][tx] = (k < K && jx < cols && !(strict && k == jx)) ? (long long)oz2_ldexp(B[(int64_t)k * ldb + jx], P - e)
+                                                              : 0;
   }
   __syncthreads();
   const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
@@ -455,7 +458,7 @@ static bool oz2_encode(CUtensorMap* m, const void* base, uint64_t cols, uint64_t
 
 cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                             int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
-                            cudaStream_t st, int64_t* launches) {
+                            cudaStream_t st, int64_t* launches, int strict) {
   if (!oz2_supported(M, N, K)) return cudaErrorInvalidValue;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* w = static_cast<char*>(ws);
@@ -489,13 +492,14 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   const double eb_n = range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER);
   {
     ProfileScope aux(KIND_OZAUX, 0.0, 24.0 * ea_n + 32.0 * eb_n, st);
-    oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, P, As, ea);
+    oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, (strict & 1) != 0,
+                                                                               P, As, ea);
     cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
     if (e != cudaSuccess) return e;
     oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(
-        B, ldb, (int)K, (int)N, triB, maxbits);
+        B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, maxbits);
     oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
-        B, ldb, (int)K, (int)N, triB, P, maxbits, eb, Bs);
+        B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, P, maxbits, eb, Bs);
   }
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
@@ -518,6 +522,32 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   }
   if (launches) *launches += 5;
   return cudaGetLastError();
+}
+
+// X_ij = S_ii K_ij (i >= j), S_ij K_jj (i < j): the terms of S K with a diagonal factor.
+// Block: 256 columns x 32 rows, the 256 diagonal entries K_jj staged in shared memory.
+__global__ void __launch_bounds__(256) oz2_ul_diag_terms_kernel(int n, const double* S, int64_t lds, const double* K,
+                                                                int64_t ldk, double* X, int64_t ldx) {
+  __shared__ double kd[256];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  kd[threadIdx.x] = j < n ? K[(int64_t)j * ldk + j] : 0.0;
+  __syncthreads();
+  if (j >= n) return;
+  for (int r = 0; r < 32; ++r) {
+    const int i = blockIdx.y * 32 + r;
+    if (i >= n) break;
+    X[(int64_t)i * ldx + j] = i >= j ? S[(int64_t)i * lds + i] * K[(int64_t)i * ldk + j]
+                                     : S[(int64_t)i * lds + j] * kd[threadIdx.x];
+  }
+}
+
+cudaError_t launch_oz2_ul(int64_t n, const double* S, int64_t lds, const double* K, int64_t ldk, double* X,
+                          int64_t ldx, void* ws, cudaStream_t st, int64_t* launches) {
+  if (!oz2_supported(n, n, n)) return cudaErrorInvalidValue;
+  oz2_ul_diag_terms_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((n + 31) / 32)), 256, 0, st>>>(
+      (int)n, S, lds, K, ldk, X, ldx);
+  if (launches) *launches += 1;
+  return launch_oz2_gemm(n, n, n, S, lds, TRI_UPPER, K, ldk, TRI_LOWER, X, ldx, 1.0, 1.0, ws, st, launches, 3);
 }
 
 }  // namespace trinv

@@ -175,12 +175,13 @@ static size_t oz_scratch(int64_t n) {
   return align_up(best);
 }
 
-// The U^{-1} L^{-1} product (and the LU products of inv_general) could run on the INT8 CRT
-// engine, but both factors of S K have a dominant diagonal and entries ~1/n off it, and the
-// row / column scaling of the modular scheme then leaves the smallest entries of the product
-// with ~2^-39 relative precision: config 4 measured 1.0e-10 floored error against the
-// 1e-10 gate (DMMA: 4.8e-14; tests/accuracy_report.py).  They stay on DMMA.
-static bool ul_on_int8(int64_t) { return false; }
+// The U^{-1} L^{-1} product on the INT8 CRT engine: the diagonals of both factors are split
+// off (launch_oz2_ul), because with them in the row / column maxima the scaled product of
+// factors with a dominant diagonal and small entries off it left the smallest entries of
+// S K with ~2^-39 relative precision (config 4 measured 1.0e-10 against the 1e-10 gate).
+static bool ul_on_int8(int64_t n) {
+  return product_engine() == 2 && n >= g_oz_min.load() && oz2_supported(n, n, n);
+}
 
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
@@ -491,6 +492,20 @@ static size_t lu_inv_scratch(int64_t n) {
   const int64_t h = lu_split(n), r = n - h;
   return align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
 }
+// INT8 CRT scratch for the products of lu_inv_rec that run on the modular engine (all of
+// them with min(M, N, K) >= the engine's block threshold): the largest over the recursion.
+static bool lu_gemm_on_int8(int64_t M, int64_t N, int64_t K) {
+  return product_engine() == 2 && std::min(M, std::min(N, K)) >= g_oz_min.load() && oz2_supported(M, N, K);
+}
+static size_t lu_oz_ws(int64_t n) {
+  if (n <= LU_MAX || product_engine() != 2) return 0;
+  const int64_t h = lu_split(n), r = n - h;
+  size_t best = std::max(lu_oz_ws(h), lu_oz_ws(r));
+  const int64_t shapes[5][3] = {{h, r, h}, {r, h, h}, {r, r, h}, {r, h, r}, {h, r, r}};
+  for (const auto& m : shapes)
+    if (lu_gemm_on_int8(m[0], m[1], m[2])) best = std::max(best, align_up(oz2_workspace_bytes(m[0], m[1], m[2])));
+  return best;
+}
 static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
                                  int32_t* info, int64_t info_off, cudaStream_t s, void* ozws) {
   if (n <= LU_MAX) {
@@ -503,7 +518,7 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
   auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                   int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta) {
-    if (ozws && product_engine() == 2 && std::min(M, std::min(N, K)) >= g_oz_min.load() && oz2_supported(M, N, K))
+    if (ozws && lu_gemm_on_int8(M, N, K))
       return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, s,
                                        &g_launches));
     GemmArgs g{};
@@ -563,7 +578,7 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   int64_t ldx_use = ldx;
   if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; p += align_up(mat_bytes(n)); }
   if (ul_on_int8(n)) {  // S K on the INT8 tensor cores (k >= max(i, j))
-    TRY(launch_oz2_gemm(n, n, n, Ui, lde, TRI_UPPER, Li, lde, TRI_LOWER, Xuse, ldx_use, 1.0, 0.0, p, s, &g_launches));
+    TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, p, s, &g_launches));
   } else {
     LevelArgs ul{};
     ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
@@ -588,7 +603,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
   if (op == 'A') {  // inv_general: F, W, K, S (n x even(n) each), the product scratch, X staging, INT8 scratch
     size_t bytes = 4 * align_up(mat_bytes(n)) + align_up(lu_inv_scratch(n));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
-    if (ul_on_int8(n)) bytes += align_up(oz2_workspace_bytes(n, n, n));
+    bytes += std::max(lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
     (void)A; (void)lda;
     return bytes;
   }
@@ -835,16 +850,16 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const bool stage_x = !tma_ok(X, ldx);
   double* Xuse = stage_x ? take(mat_bytes(n)) : X;
   const int64_t ldx_use = stage_x ? lde : ldx;
-  void* ozws = ul_on_int8(n) ? static_cast<void*>(take(oz2_workspace_bytes(n, n, n))) : nullptr;
+  const size_t oz_bytes = std::max(lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
+  void* ozws = oz_bytes ? static_cast<void*>(take(oz_bytes)) : nullptr;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   TRY(cudaMemcpy2DAsync(Wk, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
   // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
   trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, ozws);
   if (st != TRINV_OK) return st;
   // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
-  if (ozws) {
-    TRY(launch_oz2_gemm(n, n, n, Ui, lde, TRI_UPPER, Li, lde, TRI_LOWER, Xuse, ldx_use, 1.0, 0.0, ozws, s,
-                        &g_launches));
+  if (ul_on_int8(n)) {
+    TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, ozws, s, &g_launches));
   } else {
     LevelArgs ul{};
     ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;

@@ -1,4 +1,4 @@
-"""Floored relative error and residual of the product engines on the BASELINE configs 2-4
+"""Floored relative error and residual of the product engines on the BASELINE configs 2-5
 (64 sampled columns against the CPU oracle; test infrastructure, not part of pytest).
 
     python tests/accuracy_report.py
@@ -44,12 +44,30 @@ def lu_case(n):
     return oracle.floored_rel_err(Xs, R, axis_cols=0), float("nan")
 
 
+def general_case(n):
+    Lg = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    Ug = torch.empty_like(Lg)
+    synth.device_fill(Lg, n, seed=5, tag="L", diag="pos")
+    synth.device_fill(Ug, n, seed=5, tag="U", uplo="U", diag="one")
+    A = Lg @ Ug  # library DGEMM, input construction only
+    X = P.inv_general(A)
+    cols = sample_columns(n, 5)
+    cidx = torch.from_numpy(cols).to(DEV)
+    Xs = X[:, cidx]
+    E = A @ Xs
+    E[cidx, torch.arange(len(cols), device=DEV)] -= 1.0
+    rho = (torch.linalg.norm(E) / (torch.linalg.norm(A) * torch.linalg.norm(Xs))).item()
+    R = oracle.lu_columns(Lg.cpu().numpy(), Ug.cpu().numpy(), cols, unit_l=False, unit_u=True)
+    return oracle.floored_rel_err(Xs.T.contiguous().cpu().numpy(), R, axis_cols=0), rho
+
+
 def main():
     for engine in ("dmma", "int8", "int8crt"):
         P.set_product_engine(engine, min_block=4096 if engine == "int8crt" else 8192)
         for name, fn in (("config2 n=8192 L", lambda: tri_case(8192, "L", 2)),
                          ("config3 n=32768 U", lambda: tri_case(32768, "U", 3)),
-                         ("config4 inv_from_lu n=16384", lambda: lu_case(16384))):
+                         ("config4 inv_from_lu n=16384", lambda: lu_case(16384)),
+                         ("config5 inv_general n=16384", lambda: general_case(16384))):
             e, r = fn()
             print(f"{engine:8s} {name:28s} floored-rel {e:.3e}  residual {r:.3e}", flush=True)
     P.set_product_engine()

@@ -445,6 +445,10 @@ def main():
                               "FP64 results; level products of blocks >= %d computed exactly in int8 x int8 -> int32 "
                               "on the tcgen05 tensor cores (%s) and reconstructed in FP64, smaller ones on FP64 DMMA"
                               % (mb, "8-digit splitting" if args.products == "int8" else "16 moduli + CRT"))
+        if cfg["kind"] in ("G", "A") and args.products == "int8crt":
+            conf["arithmetic"] += ("; U^-1 L^-1 as its diagonal terms (one elementwise pass) plus the strictly "
+                                   "triangular product on the INT8 engine" +
+                                   ("; LU products of blocks >= %d on the INT8 engine" % mb if cfg["kind"] == "A" else ""))
     line["config"] = conf
 
     # ---- roofline of the dominant kernel ----

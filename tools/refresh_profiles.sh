@@ -37,5 +37,5 @@ python tools/kprof.py L 8192 > gpurun_out/kprof_L8192.txt 2>&1
 python tools/kprof.py G 16384 > gpurun_out/kprof_G16384.txt 2>&1
 python tools/kprof.py U 32768 > gpurun_out/kprof_U32768.txt 2>&1
 TRINV_PRODUCTS=dmma python tools/kprof.py U 32768 > gpurun_out/kprof_U32768_dmma.txt 2>&1
-for c in 2 3 4; do timeout 900 python bench.py --config $c --products dmma >> gpurun_out/bench_dmma.jsonl 2>/dev/null; done
+for c in 2 3 4 5; do timeout 900 python bench.py --config $c --products dmma >> gpurun_out/bench_dmma.jsonl 2>/dev/null; done
 timeout 1500 python tests/accuracy_report.py > gpurun_out/accuracy_report.txt 2>&1

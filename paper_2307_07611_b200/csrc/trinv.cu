@@ -487,10 +487,45 @@ static trinv_status_t lu_rec(int64_t n, double* W, int64_t ldw, double* F, int64
 // The diagonal-block inverses computed for the factorisation are thus reused, and no
 // separate triangular inversion of the full factors is needed.  All matrices share
 // the even leading dimension ld; T is the (h x r | r x h) product scratch.
-static size_t lu_inv_scratch(int64_t n) {
+// Two product scratches (the K21 and S12 chains run concurrently), each of the largest
+// (h x r | r x h) shape of the recursion.
+static size_t lu_inv_half_scratch(int64_t n) {
   if (n <= LU_MAX) return 0;
   const int64_t h = lu_split(n), r = n - h;
   return align_up((size_t)std::max(h * even_up(r), r * even_up(h)) * sizeof(double));
+}
+static size_t lu_inv_scratch(int64_t n) { return 2 * lu_inv_half_scratch(n); }
+
+// A second stream per device for the independent product pairs of lu_inv_rec (U12 / L21,
+// the K21 / S12 chains, the two leaf inversions): forked from and joined back to the
+// caller's stream by events, so ordering with the caller's work is unchanged and the pair
+// is captured as two graph branches under stream capture.
+struct ForkCtx {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static cudaError_t fork_ctx(ForkCtx** out) {
+  static thread_local ForkCtx ctx[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  ForkCtx& c = ctx[dev];
+  if (!c.aux) {
+    if ((e = cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  *out = &c;
+  return cudaSuccess;
+}
+static cudaError_t fork_to(ForkCtx* c, cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(c->fork, s);
+  return e != cudaSuccess ? e : cudaStreamWaitEvent(c->aux, c->fork, 0);
+}
+static cudaError_t join_from(ForkCtx* c, cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(c->join, c->aux);
+  return e != cudaSuccess ? e : cudaStreamWaitEvent(s, c->join, 0);
 }
 // INT8 CRT scratch for the products of lu_inv_rec that run on the modular engine (all of
 // them with min(M, N, K) >= the engine's block threshold): the largest over the recursion.
@@ -508,44 +543,62 @@ static size_t lu_oz_ws(int64_t n) {
 }
 static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
                                  int32_t* info, int64_t info_off, cudaStream_t s, void* ozws) {
+  ForkCtx* fc = nullptr;
+  TRY(fork_ctx(&fc));
   if (n <= LU_MAX) {
     TRY(launch_lu_leaf(W, ld, F, ld, (int)n, info, info_off, s, &g_launches));
+    static const bool fork_leaf = [] { const char* e = std::getenv("TRINV_LU_FORK"); return !(e && e[0] == '0'); }();
+    if (fork_leaf) TRY(fork_to(fc, s));  // K = L^{-1} here, S = U^{-1} on the second stream
     trinv_status_t st = run_tri('L', n, F, ld, Li, ld, 0, nullptr, nullptr, 0, s);
     if (st != TRINV_OK) return st;
-    return run_tri('U', n, F, ld, Ui, ld, 1, nullptr, nullptr, 0, s);
+    st = run_tri('U', n, F, ld, Ui, ld, 1, nullptr, nullptr, 0, fork_leaf ? fc->aux : s);
+    if (st != TRINV_OK) return st;
+    if (fork_leaf) TRY(join_from(fc, s));
+    return TRINV_OK;
   }
   const int64_t h = lu_split(n), r = n - h;
+  double* T2 = T + lu_inv_half_scratch(n) / sizeof(double);
   auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
   auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
-                  int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta) {
+                  int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
     if (ozws && lu_gemm_on_int8(M, N, K))
-      return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, s,
+      return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, st,
                                        &g_launches));
     GemmArgs g{};
     g.M = M; g.N = N; g.K = K; g.batch = 1;
     g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
     g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
-    return cuda_fail(launch_gemm(g, s, &g_launches));
+    return cuda_fail(launch_gemm(g, st, &g_launches));
   };
+  // the two products of a pair run concurrently unless one uses the (single) INT8 scratch
+  static const bool fork_on = [] { const char* e = std::getenv("TRINV_LU_FORK"); return !(e && e[0] == '0'); }();
+  const bool par = fork_on && !(ozws && (lu_gemm_on_int8(h, r, h) || lu_gemm_on_int8(r, h, r) ||
+                                         lu_gemm_on_int8(h, r, r)));
+  cudaStream_t s2 = par ? fc->aux : s;
   trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws);  // A11 = L11 U11, K11, S11
   if (st != TRINV_OK) return st;
-  // U12 = K11 A12 (K11 lower), L21 = A21 S11 (S11 upper), Schur W22 <- A22 - L21 U12
-  if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0))) return st;
-  if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0))) return st;
-  if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0)))
+  // U12 = K11 A12 (K11 lower) || L21 = A21 S11 (S11 upper); Schur W22 <- A22 - L21 U12
+  if (par) TRY(fork_to(fc, s));
+  if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0, s))) return st;
+  if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0, s2))) return st;
+  if (par) TRY(join_from(fc, s));
+  if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0, s)))
     return st;
   st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s, ozws);
   if (st != TRINV_OK) return st;
-  // K21 = -K22 (L21 K11)
   const int64_t lth = even_up(h), ltr = even_up(r);
-  if ((st = gemm(r, h, h, blk(F, h, 0), ld, TRI_NONE, Li, ld, TRI_LOWER, T, lth, 1.0, 0.0))) return st;
-  if ((st = gemm(r, h, r, blk(Li, h, h), ld, TRI_LOWER, T, lth, TRI_NONE, blk(Li, h, 0), ld, -1.0, 0.0))) return st;
-  // S12 = -(S11 U12) S22
-  if ((st = gemm(h, r, h, Ui, ld, TRI_UPPER, blk(F, 0, h), ld, TRI_NONE, T, ltr, 1.0, 0.0))) return st;
-  if ((st = gemm(h, r, r, T, ltr, TRI_NONE, blk(Ui, h, h), ld, TRI_UPPER, blk(Ui, 0, h), ld, -1.0, 0.0))) return st;
+  if (par) TRY(fork_to(fc, s));
+  // K21 = -K22 (L21 K11)
+  if ((st = gemm(r, h, h, blk(F, h, 0), ld, TRI_NONE, Li, ld, TRI_LOWER, T, lth, 1.0, 0.0, s))) return st;
+  if ((st = gemm(r, h, r, blk(Li, h, h), ld, TRI_LOWER, T, lth, TRI_NONE, blk(Li, h, 0), ld, -1.0, 0.0, s))) return st;
+  // S12 = -(S11 U12) S22 (second stream, second scratch)
+  if ((st = gemm(h, r, h, Ui, ld, TRI_UPPER, blk(F, 0, h), ld, TRI_NONE, T2, ltr, 1.0, 0.0, s2))) return st;
+  if ((st = gemm(h, r, r, T2, ltr, TRI_NONE, blk(Ui, h, h), ld, TRI_UPPER, blk(Ui, 0, h), ld, -1.0, 0.0, s2)))
+    return st;
   // structural zeros of the opposite triangles (read densely by the diagonal tiles of S K)
   TRY(launch_zero_2d(blk(Li, 0, h), ld, h, r, s, &g_launches));
-  TRY(launch_zero_2d(blk(Ui, h, 0), ld, r, h, s, &g_launches));
+  TRY(launch_zero_2d(blk(Ui, h, 0), ld, r, h, s2, &g_launches));
+  if (par) TRY(join_from(fc, s));
   return TRINV_OK;
 }
 

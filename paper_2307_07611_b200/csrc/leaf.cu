@@ -85,61 +85,81 @@ __device__ __forceinline__ void leaf_report(const LeafArgs& a, int64_t b, int la
 }
 
 // ---------------------------------------------------------------------------
-// Triangle-only staging (n = 32).  Each slot holds the referenced triangle as
-// two 16-row bands loaded by 2-D TMA (cp.async.bulk.tensor over a 3-D view
-// [batch][32 rows][32 cols] of the input): lower = rows 0-15 x cols 0-15 and
-// rows 16-31 x cols 0-31; upper = rows 0-15 x cols 0-31 and rows 16-31 x cols
-// 16-31.  6 KiB per matrix instead of 8 KiB, two TMA instructions.  The inverse
-// leaves the registers through coalesced 256-byte row stores, so a slot is free
-// again as soon as the warp has read it; the next load is issued before the
-// stores.
+// Triangle-only staging (n = 32).  Each slot holds the referenced triangle as 32/BR
+// bands of BR rows, each loaded by one 2-D TMA box (cp.async.bulk.tensor over a 3-D view
+// [batch][32 rows][32 cols] of the input): lower band b = rows BR b .. BR b + BR-1 x
+// cols 0 .. BR (b+1) - 1; upper band b = the same rows x cols BR b .. 31.  BR = 16 (the
+// default): 768 doubles (6 KiB) per matrix in two TMA instructions; BR = 8 / 4 read
+// 640 / 576 doubles (4.5 KiB, 9% above the 528 referenced) in 4 / 8 instructions but
+// measured 4% / 8% slower (profiles/r01_leaf_variants.txt).  The inverse leaves the
+// registers through coalesced 256-byte row stores, so a slot is free again as soon as
+// the warp has read it; the next load is issued before the stores.
 //
 // The upper case runs the lower recurrence on T' = J U J (J = index reversal,
 // T'_ik = U_{31-i,31-k}): X' = J U^{-1} J, lane j then holds column 31-j of
 // U^{-1}.  One straight-line code path, no per-step branches.
-constexpr int kBand = 768;  // doubles per slot (16x16 + 16x32)
-__host__ __device__ __forceinline__ int lidx(int i, int k) { return i < 16 ? i * 16 + k : 256 + (i - 16) * 32 + k; }
-__host__ __device__ __forceinline__ int uidx(int i, int k) { return i < 16 ? i * 32 + k : 512 + (i - 16) * 16 + (k - 16); }
-template <bool UPPER>
+template <int BR>
+struct Band {
+  static constexpr int NBAND = 32 / BR;
+  static constexpr int SLOT = BR * BR * NBAND * (NBAND + 1) / 2;  // doubles per slot
+  // lower: band b = rows [BR b, BR b + BR), cols [0, BR (b + 1))
+  static __host__ __device__ constexpr int loff(int b) { return BR * BR * b * (b + 1) / 2; }
+  static __host__ __device__ constexpr int lidx(int i, int k) {
+    return loff(i / BR) + (i - BR * (i / BR)) * BR * (i / BR + 1) + k;
+  }
+  // upper: band b = rows [BR b, BR b + BR), cols [BR b, 32)
+  static __host__ __device__ constexpr int uoff(int b) { return BR * (32 * b - BR * b * (b - 1) / 2); }
+  static __host__ __device__ constexpr int uidx(int i, int k) {
+    return uoff(i / BR) + (i - BR * (i / BR)) * (32 - BR * (i / BR)) + (k - BR * (i / BR));
+  }
+};
+static_assert(Band<16>::SLOT == 768 && Band<8>::SLOT == 640 && Band<4>::SLOT == 576, "band slots");
+static_assert(Band<4>::uoff(8) == 576 && Band<8>::uoff(4) == 640, "upper band offsets");
+template <int BR>
+struct BandMaps {
+  CUtensorMap m[Band<BR>::NBAND];  // m[w - 1]: box BR rows x BR w columns
+};
+
+template <bool UPPER, int BR>
 __device__ __forceinline__ double2 tri_pair(const double* T, int i, int k) {  // (T'_ik, T'_i,k+1), k even
-  if (!UPPER) return *reinterpret_cast<const double2*>(T + lidx(i, k));
-  const double2 v = *reinterpret_cast<const double2*>(T + uidx(31 - i, 30 - k));  // U_{r,c}, U_{r,c+1}
+  if (!UPPER) return *reinterpret_cast<const double2*>(T + Band<BR>::lidx(i, k));
+  const double2 v = *reinterpret_cast<const double2*>(T + Band<BR>::uidx(31 - i, 30 - k));  // U_{r,c}, U_{r,c+1}
   return make_double2(v.y, v.x);
 }
-template <bool UPPER>
+template <bool UPPER, int BR>
 __device__ __forceinline__ double tri_sub(const double* T, int k) {  // T'_{k+1,k}, k even
-  return UPPER ? T[uidx(30 - k, 31 - k)] : T[lidx(k + 1, k)];
+  return UPPER ? T[Band<BR>::uidx(30 - k, 31 - k)] : T[Band<BR>::lidx(k + 1, k)];
 }
-template <bool UPPER>
+template <bool UPPER, int BR>
 __device__ __forceinline__ double tri_diag(const double* T, int i) {  // T_ii, original index
-  return UPPER ? T[uidx(i, i)] : T[lidx(i, i)];
+  return UPPER ? T[Band<BR>::uidx(i, i)] : T[Band<BR>::lidx(i, i)];
 }
 
-template <bool UPPER, int K>
+template <bool UPPER, int BR, int K>
 __device__ __forceinline__ void leaf32_step(const double* T, const double* rr, double (&x)[LEAF]) {
   const double2 r = *reinterpret_cast<const double2*>(rr + K);
   const double xk = x[K] * r.x;
   x[K] = xk;
-  x[K + 1] = fma(-tri_sub<UPPER>(T, K), xk, x[K + 1]);
+  x[K + 1] = fma(-tri_sub<UPPER, BR>(T, K), xk, x[K + 1]);
   const double xk1 = x[K + 1] * r.y;
   x[K + 1] = xk1;
 #pragma unroll
   for (int i = K + 2; i < LEAF; ++i) {
-    const double2 t = tri_pair<UPPER>(T, i, K);
+    const double2 t = tri_pair<UPPER, BR>(T, i, K);
     x[i] = fma(-t.x, xk, x[i]);
     x[i] = fma(-t.y, xk1, x[i]);
   }
 }
-template <bool UPPER, int... P>
+template <bool UPPER, int BR, int... P>
 __device__ __forceinline__ void leaf32_steps(const double* T, const double* rr, double (&x)[LEAF],
                                              std::integer_sequence<int, P...>) {
-  (leaf32_step<UPPER, 2 * P>(T, rr, x), ...);
+  (leaf32_step<UPPER, BR, 2 * P>(T, rr, x), ...);
 }
 
-template <bool UPPER>
+template <bool UPPER, int BR>
 __device__ __forceinline__ void leaf32_compute(const double* T, double* rr, int unit, int lane, double (&x)[LEAF],
                                                bool& singular, int& first_zero) {
-  const double d = tri_diag<UPPER>(T, lane);
+  const double d = tri_diag<UPPER, BR>(T, lane);
   const bool zero = (!unit) && d == 0.0;
   const unsigned zmask = __ballot_sync(0xffffffffu, zero);
   singular = zmask != 0;
@@ -151,14 +171,14 @@ __device__ __forceinline__ void leaf32_compute(const double* T, double* rr, int 
   // pairs (k, k+1): x_k = r_k acc_k; acc_{k+1} -= T'_{k+1,k} x_k; x_{k+1} = r_{k+1} acc_{k+1};
   // acc_i -= T'_ik x_k + T'_{i,k+1} x_{k+1} (i >= k+2), one 16-byte broadcast per row.
   // Compile-time step indices (template expansion) keep x[] in registers.
-  leaf32_steps<UPPER>(T, rr, x, std::make_integer_sequence<int, LEAF / 2>{});
+  leaf32_steps<UPPER, BR>(T, rr, x, std::make_integer_sequence<int, LEAF / 2>{});
 }
 
-template <bool UPPER, int WARPS, int NS>
+template <bool UPPER, int WARPS, int NS, int BR>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-    leaf32_tma_kernel(const __grid_constant__ CUtensorMap band0, const __grid_constant__ CUtensorMap band1,
-                      const LeafArgs a) {
-  constexpr int SLOT = kBand;
+    leaf32_tma_kernel(const __grid_constant__ BandMaps<BR> maps, const LeafArgs a) {
+  using BD = Band<BR>;
+  constexpr int SLOT = BD::SLOT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * SLOT;
@@ -175,10 +195,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
-  if (lane == 0 && warp == 0) {
-    tma_prefetch_desc(&band0);
-    tma_prefetch_desc(&band1);
-  }
+  if (lane == 0 && warp == 0)
+    for (int w = 0; w < BD::NBAND; ++w) tma_prefetch_desc(&maps.m[w]);
   __syncwarp();
 
   auto issue_load = [&](int64_t t) {  // lane 0 only
@@ -186,12 +204,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     double* slot = slots + (t % NS) * SLOT;
     uint64_t* bar = &bars[t % NS];
     mbar_arrive_expect_tx(bar, SLOT * 8);
-    if (!UPPER) {
-      tma_load_3d(slot, &band0, 0, 0, b, bar);         // rows 0-15, cols 0-15
-      tma_load_3d(slot + 256, &band1, 0, 16, b, bar);  // rows 16-31, cols 0-31
-    } else {
-      tma_load_3d(slot, &band1, 0, 0, b, bar);         // rows 0-15, cols 0-31
-      tma_load_3d(slot + 512, &band0, 16, 16, b, bar); // rows 16-31, cols 16-31
+#pragma unroll
+    for (int g = 0; g < BD::NBAND; ++g) {
+      if (!UPPER) tma_load_3d(slot + BD::loff(g), &maps.m[g], 0, BR * g, b, bar);  // cols 0 .. BR (g+1) - 1
+      else tma_load_3d(slot + BD::uoff(g), &maps.m[BD::NBAND - 1 - g], BR * g, BR * g, b, bar);  // cols BR g .. 31
     }
   };
 
@@ -206,7 +222,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     double x[LEAF];
     bool singular;
     int first_zero;
-    leaf32_compute<UPPER>(slot, rr, a.unit, lane, x, singular, first_zero);
+    leaf32_compute<UPPER, BR>(slot, rr, a.unit, lane, x, singular, first_zero);
     __syncwarp();  // every lane has finished reading the slot and rr
     if (t + NS < count && lane == 0) {
       fence_proxy_async_smem();
@@ -261,28 +277,31 @@ __global__ void __launch_bounds__(128) leaf_plain_kernel(const LeafArgs a) {
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // 3-D view [batch][32 rows][32 cols] of the inputs; box = `rows` rows x `cols` columns x 1 matrix.
-static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols, int rows = 16) {
+static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols, int rows) {
   const uint64_t dims[3] = {32, 32, (uint64_t)a.batch};
   const uint64_t strides[2] = {(uint64_t)a.lda * 8, (uint64_t)a.sA * 8};
   const uint32_t box[3] = {(uint32_t)cols, (uint32_t)rows, 1};
   return encode_map_nd(m, a.A, 3, dims, strides, box);
 }
 
-template <int W, int NS>
-static void launch_band(char uplo, const CUtensorMap& m0, const CUtensorMap& m1, const LeafArgs& a, int sms,
-                        cudaStream_t s) {
-  constexpr size_t smem = ((size_t)W * NS * kBand + W * LEAF) * 8 + W * NS * 8;
+template <int W, int NS, int BR>
+static bool launch_band(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
+  BandMaps<BR> maps;
+  for (int w = 1; w <= Band<BR>::NBAND; ++w)
+    if (!encode_batch_map(&maps.m[w - 1], a, BR * w, BR)) return false;
+  constexpr size_t smem = ((size_t)W * NS * Band<BR>::SLOT + W * LEAF) * 8 + W * NS * 8;
   const int64_t ctas_needed = (a.batch + W - 1) / W;
   const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
   if (uplo == 'L') {
-    constexpr auto k = leaf32_tma_kernel<false, W, NS>;
+    constexpr auto k = leaf32_tma_kernel<false, W, NS, BR>;
     set_smem_once<k>((int)smem);
-    k<<<grid, W * 32, smem, s>>>(m0, m1, a);
+    k<<<grid, W * 32, smem, s>>>(maps, a);
   } else {
-    constexpr auto k = leaf32_tma_kernel<true, W, NS>;
+    constexpr auto k = leaf32_tma_kernel<true, W, NS, BR>;
     set_smem_once<k>((int)smem);
-    k<<<grid, W * 32, smem, s>>>(m0, m1, a);
+    k<<<grid, W * 32, smem, s>>>(maps, a);
   }
+  return true;
 }
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.batch <= 0) return cudaSuccess;
@@ -298,15 +317,14 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   const double nn = (double)a.n;
   ProfileScope prof(KIND_LEAF, a.batch * nn * nn * nn / 3.0, a.batch * (nn * (nn + 1) / 2 + nn * nn) * 8.0, s);
   const bool full32 = a.n == LEAF && a.n_last == LEAF;
-  // n = 32, TMA-compatible layout: 8 warps x 3 slots per CTA (one CTA per SM) measured best on B200
-  // (profiles/r01_leaf_variants.txt).
+  // n = 32, TMA-compatible layout: 8 warps x NS slots per CTA (one CTA per SM), bands of
+  // BR rows (profiles/r01_leaf_variants.txt); TRINV_LEAF_BR = 4 / 8 / 16 for experiments
+  static const int br = [] { const char* e = std::getenv("TRINV_LEAF_BR"); return e ? std::atoi(e) : 16; }();
   bool launched = false;
   if (tma && full32 && a.batch < (int64_t)1 << 31) {
-    CUtensorMap m16, m32;
-    if (encode_batch_map(&m16, a, 16) && encode_batch_map(&m32, a, 32)) {
-      launch_band<8, 3>(uplo, m16, m32, a, sms, s);
-      launched = true;
-    }
+    if (br == 16) launched = launch_band<8, 3, 16>(uplo, a, sms, s);
+    else if (br == 8) launched = launch_band<8, 4, 8>(uplo, a, sms, s);
+    else launched = launch_band<8, 4, 4>(uplo, a, sms, s);
   }
   if (!launched) {
     const int64_t ctas_needed = (a.batch + 3) / 4;

@@ -417,14 +417,15 @@ def main():
         ev[0].record(stream)
         for i in range(args.steps):
             run()
-            ev[i + 1].record(stream)
+            if graph is None or i == args.steps - 1:  # graph-replayed latency steps: no event between them
+                ev[i + 1].record(stream)
         barrier()
     launches = P.launch_count()
     if graph is not None:
         # count the kernels inside one captured step, then scale to the timed steps
         P.reset_launch_count(); step(); barrier()
         launches = P.launch_count() * args.steps
-    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)] if graph is None else None
     total_ms = ev[0].elapsed_time(ev[-1])
     total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps

@@ -51,6 +51,9 @@ struct BlkCfg {
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 
@@ -135,18 +138,19 @@ __device__ __forceinline__ void blk_store16(double* C, const double (&acc)[2][2]
           make_double2(alpha * acc[mi][ni][0], alpha * acc[mi][ni][1]);
 }
 
-// One level of merges [s, s+b) + [s+b, s+2b), s = 2 g b, inside the NB block.
-template <int NB>
-__device__ __forceinline__ void blk_level(double* X, double* W, int b, int warp, int lane) {
+// One level of merges [s, s+b) + [s+b, s+2b), s = 2 g b, inside the NB block (b a
+// template parameter: the tile bookkeeping below is shifts, not divisions).
+template <int NB, int b>
+__device__ __forceinline__ void blk_level(double* X, double* W, int warp, int lane) {
   using C = BlkCfg<NB>;
   constexpr int S = C::S, WS = C::WS;
-  const int tb = b / 16;                  // 16-tiles per side of a merge block
-  const int m = NB / (2 * b);             // merges of the level
-  const int tiles = m * tb * tb;
+  constexpr int tb = b / 16;              // 16-tiles per side of a merge block
+  constexpr int m = NB / (2 * b);         // merges of the level
+  constexpr int tiles = m * tb * tb;
   // Tiles are dealt to the warps in snake order of decreasing K-range so that the
   // four SM sub-partitions (warps w and w + 4 share one) get equal DMMA work.
   // W_g = C_g A_g^-1: tile (I, J), k in [16 J, b)  (A^-1 lower)
-  const int per = m * tb;  // tiles per K-class
+  constexpr int per = m * tb;  // tiles per K-class
   for (int r = 0; r * C::WARPS < tiles; ++r) {
     const int q = r * C::WARPS + ((r & 1) ? C::WARPS - 1 - warp : warp);  // snake deal, longest K first
     if (q >= tiles) continue;
@@ -179,38 +183,117 @@ __global__ void __launch_bounds__(BlkCfg<NB>::THREADS) blk_kernel(const LeafArgs
   double* X = blk_smem;           // [NB][S]
   double* W = blk_smem + NB * S;  // [HB][WS]
   __shared__ int zmin;
+  __shared__ __align__(8) uint64_t ldbar;  // completion of the row bulk loads
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) { mbar_init(&ldbar, 1); fence_mbar_init(); }
+  uint32_t ldphase = 0;
+#ifdef TRINV_BLK_TIMING  // phase timestamps of the first block (latency study only)
+  unsigned long long tt[8];
+  int nt = 0;
+  auto stamp = [&]() { if (tid == 0 && nt < 8) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[nt++])); };
+  stamp();
+#else
+  auto stamp = [&]() {};
+#endif
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const int nb = (b == a.batch - 1) ? a.n_last : a.n;
     const double* src = a.A + b * a.sA;
     if (tid == 0) zmin = 1 << 30;
     __syncthreads();
-    // 1. load the referenced triangle in T' order (cp.async, all in flight); the other
-    //    triangle +0.0, the unit / padding diagonal 1.0 written directly
-#pragma unroll 8
-    for (int e = tid; e < NB * NB; e += T) {
-      const int i = e / NB, k = e % NB;
-      if (i < nb && (k < i || (k == i && !a.unit))) {
-        const int64_t off = UPPER ? (int64_t)(nb - 1 - i) * a.lda + (nb - 1 - k) : (int64_t)i * a.lda + k;
-        cp_async8(X + i * S + k, src + off);
-      } else {
-        X[i * S + k] = (k == i) ? 1.0 : 0.0;
+    // 1. load the referenced triangle in T' order; the other triangle +0.0, the unit /
+    //    padding diagonal 1.0.  Full orders with 16-byte-aligned rows: column pairs as
+    //    16-byte loads into registers (all in flight), then 16-byte shared stores; other
+    //    layouts: 8-byte cp.async per element.
+    const bool vec = nb == NB && (a.lda & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+    if (vec && !UPPER && NB == 64) {  // 16-byte cp.async per referenced pair, diagonal fix-ups after
+      constexpr int PAIRS = NB * NB / 2, PER = PAIRS / T;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = tid + q * T, i = e / (NB / 2), k = 2 * (e % (NB / 2));
+        if (k <= i) cp_async16(X + i * S + k, src + (int64_t)i * a.lda + k);
+        else *reinterpret_cast<double2*>(X + i * S + k) = make_double2(0.0, 0.0);
       }
+      cp_async_wait_all();
+      __syncthreads();  // every copy has landed
+      for (int i = tid; i < NB; i += T) {  // the diagonal pair of an even row, unit diagonals
+        if ((i & 1) == 0) X[i * S + i + 1] = 0.0;
+        if (a.unit) X[i * S + i] = 1.0;
+      }
+    } else if (vec && !UPPER) {  // NB = 128: one bulk copy per row (its referenced prefix rounded up to 16 bytes)
+      constexpr uint32_t BYTES = 16u * (NB / 2) * (NB / 2 + 1);  // sum_i 16 ceil((i + 1) / 2)
+      if (tid == 0) mbar_arrive_expect_tx(&ldbar, BYTES);
+      __syncthreads();
+      for (int i = tid; i < NB; i += T) bulk_g2s(X + i * S, src + (int64_t)i * a.lda, 16u * (i / 2 + 1), &ldbar);
+      for (int e = tid; e < NB * NB / 2; e += T) {  // the rest of each row: +0.0
+        const int i = e / (NB / 2), k = 2 * (e % (NB / 2));
+        if (k > i) *reinterpret_cast<double2*>(X + i * S + k) = make_double2(0.0, 0.0);
+      }
+      mbar_wait(&ldbar, ldphase);
+      ldphase ^= 1;
+      for (int i = tid; i < NB; i += T) {  // the diagonal pair of an even row, unit diagonals
+        if ((i & 1) == 0) X[i * S + i + 1] = 0.0;
+        if (a.unit) X[i * S + i] = 1.0;
+      }
+    } else if (vec) {  // upper: 16-byte loads into registers, pairs swapped into T' order
+      constexpr int PAIRS = NB * NB / 2, PER = PAIRS / T;
+      double2 v[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {  // pair (i, k), (i, k + 1), k even
+        const int e = tid + q * T, i = e / (NB / 2), k = 2 * (e % (NB / 2));
+        const bool need = k <= i;  // at least (i, k) referenced
+        const int64_t off = UPPER ? (int64_t)(NB - 1 - i) * a.lda + (NB - 2 - k) : (int64_t)i * a.lda + k;
+        v[q] = need ? *reinterpret_cast<const double2*>(src + off) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = tid + q * T, i = e / (NB / 2), k = 2 * (e % (NB / 2));
+        double x0 = UPPER ? v[q].y : v[q].x, x1 = UPPER ? v[q].x : v[q].y;  // T'(i, k), T'(i, k + 1)
+        if (k > i) x0 = 0.0;
+        if (k + 1 > i) x1 = 0.0;
+        if (a.unit && k == i) x0 = 1.0;  // the unit diagonal is not read
+        if (a.unit && k + 1 == i) x1 = 1.0;
+        *reinterpret_cast<double2*>(X + i * S + k) = make_double2(x0, x1);
+      }
+    } else {
+#pragma unroll 8
+      for (int e = tid; e < NB * NB; e += T) {
+        const int i = e / NB, k = e % NB;
+        if (i < nb && (k < i || (k == i && !a.unit))) {
+          const int64_t off = UPPER ? (int64_t)(nb - 1 - i) * a.lda + (nb - 1 - k) : (int64_t)i * a.lda + k;
+          cp_async8(X + i * S + k, src + off);
+        } else {
+          X[i * S + k] = (k == i) ? 1.0 : 0.0;
+        }
+      }
+      cp_async_wait_all();
     }
-    cp_async_wait_all();
     __syncthreads();
+    stamp();
     if (tid < nb && !a.unit && X[tid * (S + 1)] == 0.0) atomicMin(&zmin, UPPER ? nb - 1 - tid : tid);
     // 2. 16-wide diagonal leaves, two per warp (half-warp h of warp w: block 2w + h)
     if (warp < NB / 32) blk_leaf16<S>(X + (2 * warp + (lane >> 4)) * 16 * (S + 1), lane & 15);
     __syncthreads();
+    stamp();
     // 3. merge levels b = 16, 32, ... < NB
-#pragma unroll 1
-    for (int lb = 16; lb < NB; lb *= 2) {
-      blk_level<NB>(X, W, lb, warp, lane);
+    blk_level<NB, 16>(X, W, warp, lane);
+    stamp();
+    blk_level<NB, 32>(X, W, warp, lane);
+    stamp();
+    if constexpr (NB > 64) {
+      blk_level<NB, 64>(X, W, warp, lane);
+      stamp();
     }
-    // 4. store nb x nb (X = J X' J for the upper case), column pairs as 16-byte stores
+    // 4. store nb x nb (X = J X' J for the upper case): lower full blocks with 16-byte
+    //    aligned rows as one bulk copy per row; otherwise column pairs as 16-byte stores
     //    where the destination is aligned
     double* dst = a.X + b * a.sX;
+    if (!UPPER && nb == NB && (a.ldx & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      for (int i = tid; i < NB; i += T) bulk_s2g(dst + (int64_t)i * a.ldx, X + i * S, NB * 8);
+      bulk_commit();
+      bulk_wait_read<0>();  // X is reused by the next matrix
+    } else {
 #pragma unroll 4
     for (int e = tid; e < NB * NB / 2; e += T) {
       const int i = e / (NB / 2), k = 2 * (e % (NB / 2));
@@ -236,6 +319,14 @@ __global__ void __launch_bounds__(BlkCfg<NB>::THREADS) blk_kernel(const LeafArgs
         }
       }
     }
+    }
+#ifdef TRINV_BLK_TIMING
+    __syncthreads();
+    stamp();
+    if (tid == 0 && blockIdx.x == 0 && b == 0)
+      printf("blk<%d> ns: load %llu leaves %llu levels %llu %llu %llu store %llu\n", NB, tt[1] - tt[0], tt[2] - tt[1],
+             tt[3] - tt[2], nt > 5 ? tt[4] - tt[3] : 0ull, nt > 6 ? tt[5] - tt[4] : 0ull, tt[nt - 1] - tt[nt - 2]);
+#endif
     if (tid == 0) {
       const int z = zmin;
       const bool singular = z < nb;

@@ -275,23 +275,31 @@ __global__ void __launch_bounds__(BlkCfg<NB>::THREADS) blk_kernel(const LeafArgs
     __syncthreads();
     stamp();
     // 3. merge levels b = 16, 32, ... < NB
+    // lower full blocks with 16-byte aligned rows leave by per-row bulk copies; for NB =
+    // 128, rows [0, 64) are final before the last level and go out while it runs (for NB =
+    // 64 the early half measured slower: the store phase is latency, not volume)
+    double* dst = a.X + b * a.sX;
+    const bool bulk_out = !UPPER && nb == NB && (a.ldx & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+    auto store_rows = [&](int r0, int r1) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      for (int i = r0 + tid; i < r1; i += T) bulk_s2g(dst + (int64_t)i * a.ldx, X + i * S, NB * 8);
+      bulk_commit();
+    };
     blk_level<NB, 16>(X, W, warp, lane);
     stamp();
     blk_level<NB, 32>(X, W, warp, lane);
     stamp();
     if constexpr (NB > 64) {
+      if (bulk_out) store_rows(0, NB / 2);
       blk_level<NB, 64>(X, W, warp, lane);
       stamp();
     }
     // 4. store nb x nb (X = J X' J for the upper case): lower full blocks with 16-byte
     //    aligned rows as one bulk copy per row; otherwise column pairs as 16-byte stores
     //    where the destination is aligned
-    double* dst = a.X + b * a.sX;
-    if (!UPPER && nb == NB && (a.ldx & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-      fence_proxy_async_smem();
-      __syncthreads();
-      for (int i = tid; i < NB; i += T) bulk_s2g(dst + (int64_t)i * a.ldx, X + i * S, NB * 8);
-      bulk_commit();
+    if (bulk_out) {
+      store_rows(NB == 64 ? 0 : NB / 2, NB);
       bulk_wait_read<0>();  // X is reused by the next matrix
     } else {
 #pragma unroll 4

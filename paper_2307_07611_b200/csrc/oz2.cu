@@ -193,6 +193,7 @@ struct Oz2Params {
   int triA, triB;
   uint8_t* R;  // residues [16][M][N]
   int tiles_n;
+  int msplit;  // CTAs per output tile, each running OZ2_NMOD / msplit consecutive moduli
 };
 
 __global__ void __launch_bounds__(OZ2_THREADS, 1)
@@ -208,7 +209,8 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = p.M / OZ2_TM;
-  const int t = blockIdx.x;
+  const int t = blockIdx.x / p.msplit;
+  const int nmod = OZ2_NMOD / p.msplit, mod0 = (blockIdx.x % p.msplit) * nmod;
   const int per_group = OZ2_GROUP_M * p.tiles_n;
   const int first_m = (t / per_group) * OZ2_GROUP_M;
   const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
     tma_prefetch_desc(&ma);
     tma_prefetch_desc(&mb);
     int it = 0;
-    for (int i = 0; i < OZ2_NMOD; ++i)
+    for (int i = mod0; i < mod0 + nmod; ++i)
       for (int kk = 0; kk < nkb; ++kk, ++it) {
         const int st = it % OZ2_STAGES, use = it / OZ2_STAGES;
         if (use > 0) mbar_wait(&empty[st], (uint32_t)((use - 1) & 1));
@@ -253,8 +255,8 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
     const uint32_t idesc =
         (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(OZ2_TM >> 4) << 24);
     int it = 0;
-    for (int i = 0; i < OZ2_NMOD; ++i) {
-      const int buf = i & 1, use = i >> 1;
+    for (int i = mod0; i < mod0 + nmod; ++i) {
+      const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
       if (use > 0) {
         mbar_wait(&acc_empty[buf], (uint32_t)((use - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -287,8 +289,8 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   if (warp >= 2) {  // epilogue: residues C'_i = (A'_i B'_i) mod m_i as uint8
     const int q4 = warp & 3;
     const int row = I * OZ2_TM + q4 * 32 + lane;
-    for (int i = 0; i < OZ2_NMOD; ++i) {
-      const int buf = i & 1, use = i >> 1;
+    for (int i = mod0; i < mod0 + nmod; ++i) {
+      const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
       mbar_wait(&acc_full[buf], (uint32_t)(use & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int m = oz2_mod(i);
@@ -508,10 +510,14 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   Oz2Params p{};
   p.M = (int)M; p.N = (int)N; p.K = (int)K; p.triA = triA; p.triB = triB; p.R = Rs;
   p.tiles_n = (int)(N / OZ2_TN);
+  // below ~6 waves of tiles, each tile's moduli are split over 2 or 4 CTAs so the last
+  // partial wave is a small fraction (the level-4096 products: 512 tiles on 148 SMs)
+  const int64_t tiles = (M / OZ2_TM) * (N / OZ2_TN), waves6 = 6 * (int64_t)device_sms();
+  p.msplit = tiles >= waves6 ? 1 : (2 * tiles >= waves6 ? 2 : 4);
   set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
   {
     ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
-    oz2_gemm_kernel<<<(unsigned)((M / OZ2_TM) * (N / OZ2_TN)), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+    oz2_gemm_kernel<<<(unsigned)(tiles * p.msplit), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
   }
   const int64_t total4 = M * N / 4;
   static const Oz2Crt crt = oz2_crt_constants();

@@ -211,10 +211,23 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   const int tiles_m = p.M / OZ2_TM;
   const int t = blockIdx.x / p.msplit;
   const int nmod = OZ2_NMOD / p.msplit, mod0 = (blockIdx.x % p.msplit) * nmod;
-  const int per_group = OZ2_GROUP_M * p.tiles_n;
-  const int first_m = (t / per_group) * OZ2_GROUP_M;
-  const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
-  int I = first_m + (t % per_group) % gsz, J = (t % per_group) / gsz;
+  // grouped rasterisation: groups of OZ2_GROUP_M row tiles (dense, or B triangular), or
+  // of OZ2_GROUP_M column tiles when only A is triangular (its K-range varies along the
+  // rows; measured DRAM reads at n = 32768, profiles/r01_oz2_raster.txt)
+  int I, J;
+  if (p.triA != TRI_NONE && p.triB == TRI_NONE) {
+    const int per_group = OZ2_GROUP_M * tiles_m;
+    const int first_n = (t / per_group) * OZ2_GROUP_M;
+    const int gsz = min(p.tiles_n - first_n, OZ2_GROUP_M);
+    J = first_n + (t % per_group) % gsz;
+    I = (t % per_group) / gsz;
+  } else {
+    const int per_group = OZ2_GROUP_M * p.tiles_n;
+    const int first_m = (t / per_group) * OZ2_GROUP_M;
+    const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
+    I = first_m + (t % per_group) % gsz;
+    J = (t % per_group) / gsz;
+  }
   if (p.triA == TRI_LOWER) I = tiles_m - 1 - I;
   if (p.triB == TRI_UPPER) J = p.tiles_n - 1 - J;
   int kb = 0, ke = p.K;

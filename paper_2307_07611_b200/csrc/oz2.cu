@@ -34,7 +34,10 @@
 namespace trinv {
 
 constexpr int OZ2_NMOD = 16;
-constexpr int OZ2_TM = 128, OZ2_TN = 256, OZ2_TK = 128, OZ2_STAGES = 4, OZ2_GROUP_M = 8;
+#ifndef OZ2_GROUP
+#define OZ2_GROUP 8
+#endif
+constexpr int OZ2_TM = 128, OZ2_TN = 256, OZ2_TK = 128, OZ2_STAGES = 4, OZ2_GROUP_M = OZ2_GROUP;
 constexpr int OZ2_A_BYTES = OZ2_TM * OZ2_TK, OZ2_B_BYTES = OZ2_TN * OZ2_TK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
 constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + 1024 + 256;
 constexpr int OZ2_THREADS = 192;

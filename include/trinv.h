@@ -243,7 +243,8 @@ void trinv_reset_launch_count(void);
  * kind 0 (leaf / batched kernels), 1 (DMMA product kernels), 2 (INT8 product
  * engine: the tensor-core GEMM kernel of the CRT engine, the whole product of the
  * digit engine; bytes = int8 operations) or 3 (the CRT engine's scaling, residue
- * and reconstruction kernels; flops = 0), the summed device milliseconds, the
+ * and reconstruction kernels; flops = 0), the device milliseconds covered by those
+ * launches (the union of their intervals: launches on two streams may overlap), the
  * number of timed scopes and the ALGORITHMIC flops and bytes of those launches
  * (n^3/3 per leaf; triangular-aware products; leaf bytes
  * = referenced triangle in + full matrix out).

@@ -996,16 +996,34 @@ void trinv_profile_end(void) {
 }
 
 int trinv_profile_read(int kind, double* ms, int64_t* launches, double* flops, double* bytes) {
+  // device time = length of the union of this kind's [start, end] intervals (launches of
+  // one kind may overlap on two streams), measured from the session's first event
   double t = 0, f = 0, b = 0;
   int64_t c = 0;
-  if (g_prof) {
+  if (g_prof && !g_prof->empty()) {
+    const cudaEvent_t base = g_prof->front().e0;
+    if (cudaEventSynchronize(base) != cudaSuccess) return (int)TRINV_CUDA_ERROR;
+    std::vector<std::pair<double, double>> iv;
     for (auto& r : *g_prof) {
       if (r.kind != kind) continue;
       if (cudaEventSynchronize(r.e1) != cudaSuccess) return (int)TRINV_CUDA_ERROR;
-      float e = 0.f;
-      cudaEventElapsedTime(&e, r.e0, r.e1);
-      t += e; f += r.flops; b += r.bytes; ++c;
+      float a = 0.f, e = 0.f;
+      cudaEventElapsedTime(&a, base, r.e0);
+      cudaEventElapsedTime(&e, base, r.e1);
+      iv.emplace_back((double)a, (double)e);
+      f += r.flops; b += r.bytes; ++c;
     }
+    std::sort(iv.begin(), iv.end());
+    double lo = 0, hi = -1;
+    for (const auto& x : iv) {
+      if (x.first > hi) {
+        if (hi > lo) t += hi - lo;
+        lo = x.first; hi = x.second;
+      } else if (x.second > hi) {
+        hi = x.second;
+      }
+    }
+    if (hi > lo) t += hi - lo;
   }
   if (ms) *ms = t;
   if (launches) *launches = c;

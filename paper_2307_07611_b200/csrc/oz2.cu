@@ -41,6 +41,7 @@ constexpr int OZ2_TM = 128, OZ2_TN = 256, OZ2_TK = 128, OZ2_STAGES = 4, OZ2_GROU
 constexpr int OZ2_A_BYTES = OZ2_TM * OZ2_TK, OZ2_B_BYTES = OZ2_TN * OZ2_TK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
 constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + 1024 + 256;
 constexpr int OZ2_THREADS = 192;
+constexpr int OZ2_CMAX_ROWS = 128;  // rows per block of the column-maximum kernel
 
 // pairwise coprime, <= 256 (symmetric residues fit int8)
 __host__ __device__ constexpr int oz2_mod(int i) {
@@ -145,7 +146,7 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
   if (j >= cols) return;
   int kb, ke;
   oz2_k_range(tri, false, j, K, kb, ke);
-  const int k0 = max(kb, (int)blockIdx.y * 512), k1 = min(ke, (int)blockIdx.y * 512 + 512);
+  const int k0 = max(kb, (int)blockIdx.y * OZ2_CMAX_ROWS), k1 = min(ke, (int)(blockIdx.y + 1) * OZ2_CMAX_ROWS);
   double m = 0.0;
   const int kz = strict ? j : -1;
   for (int k = k0; k < k1; ++k) m = k == kz ? m : fmax(m, fabs(B[(int64_t)k * ldb + j]));
@@ -514,7 +515,8 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
                                                                                P, As, ea);
     cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
     if (e != cudaSuccess) return e;
-    oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + 511) / 512)), 256, 0, st>>>(
+    oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + OZ2_CMAX_ROWS - 1) / OZ2_CMAX_ROWS)), 256, 0,
+                        st>>>(
         B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, maxbits);
     oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
         B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, P, maxbits, eb, Bs);

@@ -377,7 +377,7 @@ __device__ __forceinline__ double oz2_crt_value(const uint32_t (&c)[OZ2_NMOD], c
   for (int q = 0; q < OZ2_NMOD; ++q) {
     a0 += (uint64_t)crt.w[q][0] * c[q];
     a1 += (uint64_t)crt.w[q][1] * c[q];
-    const double cd = __hiloint2double(0x43300000, (int)c[q]) - 4503599627370496.0;  // (double)c, exact
+    const double cd = (double)c[q];  // I2F (the hi/lo-word construction cost two extra instructions)
     s2 = fma(cd, crt.wd[q][0], s2);
     s3 = fma(cd, crt.wd[q][1], s3);
   }

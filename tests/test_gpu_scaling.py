@@ -1,0 +1,69 @@
+"""Power-of-two diagonal scaling: inv(D1 T D2) = D2^-1 inv(T) D1^-1 for D1, D2 = diag(2^k).
+With FP64 DMMA products it holds exactly in floating point (every product term and every
+diagonal reciprocal moves by the same power of two): bit-for-bit agreement at |k| <= 60,
+which pins the exponent handling of the leaves, the block kernel and the DMMA engine.  The
+INT8 CRT engine truncates its operands to P-bit integers relative to row / column maxima,
+so scalings that differ along the product's K dimension change which entries survive: its
+error grows with the spread of the scaling (tools/scaling_probe.py: 2.9e-15 at |k| <= 8,
+1.2e-10 at |k| <= 16, 9e-4 at |k| >= 30); the test holds it to 1e-12 at
+|k| <= 8."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import synth  # noqa: E402
+import paper_2307_07611_b200 as P  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.mark.parametrize("engine,R", [("dmma", 60), ("int8crt", 8)])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_pow2_scaling_invariance(engine, R, uplo):
+    n = 1024
+    P.set_product_engine(engine, min_block=256)
+    try:
+        rng = np.random.default_rng(11)
+        k1 = rng.integers(-R, R + 1, n)
+        k2 = rng.integers(-R, R + 1, n)
+        T = synth.host(n, seed=9, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+        S = np.ldexp(np.ldexp(T, k1[:, None]), k2[None, :])  # D1 T D2
+        f = P.trinv_lower if uplo == "L" else P.trinv_upper
+        Y = f(torch.from_numpy(T).to(DEV)).cpu().numpy()
+        X = f(torch.from_numpy(S).to(DEV)).cpu().numpy()
+        Z = np.ldexp(np.ldexp(Y, -k2[:, None]), -k1[None, :])  # D2^-1 Y D1^-1
+        if engine == "dmma":
+            assert np.array_equal(X, Z)
+        else:  # error of each entry relative to |Y| rescaled: the unscaled problem's yardstick
+            E = np.ldexp(np.ldexp(np.abs(X - Z), k2[:, None]), k1[None, :])
+            assert np.max(E) <= 1e-12 * max(1.0, np.max(np.abs(Y))), np.max(E)
+    finally:
+        P.set_product_engine()
+
+
+@pytest.mark.parametrize("engine,R", [("dmma", 40), ("int8crt", 8)])
+def test_pow2_scaling_invariance_inv_from_lu(engine, R):
+    n = 1024
+    P.set_product_engine(engine, min_block=256)
+    try:
+        rng = np.random.default_rng(12)
+        k = rng.integers(-R, R + 1, n)
+        L = synth.host(n, tag="L", diag="one")
+        U = synth.host(n, tag="U", uplo="U", diag="pos")
+        # A = L U; (D L)(U D') with D' = D^-1 keeps L's unit diagonal: scale rows of L and
+        # compensate in the columns of U: X' = D'^-1 X D^-1
+        Ls = np.ldexp(L, k[:, None]); Ls = np.ldexp(Ls, -k[None, :])      # D L D^-1 (unit diagonal kept)
+        Us = np.ldexp(U, k[:, None])                                      # D U
+        f = lambda a, b: P.inv_from_lu(torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV),  # noqa: E731
+                                       unit_l=True).cpu().numpy()
+        Y = f(L, U)
+        X = f(Ls, Us)  # (D L D^-1)(D U) = D L U: X = (L U)^-1 D^-1
+        Z = np.ldexp(Y, -k[None, :])
+        if engine == "dmma":
+            assert np.array_equal(X, Z)
+        else:
+            E = np.ldexp(np.abs(X - Z), k[None, :])
+            assert np.max(E) <= 1e-12 * max(1.0, np.max(np.abs(Y))), np.max(E)
+    finally:
+        P.set_product_engine()

@@ -126,6 +126,147 @@ static int product_engine() {
   return e;
 }
 
+// ---- scaling guard of the INT8 engines ---------------------------------------------------
+// The INT8 engines truncate their operands relative to row / column maxima, so inputs whose
+// rows or columns span many binades lose accuracy there (1.2e-10 at a
+// 2^+-16 row / column scaling, 9e-4 beyond 2^+-30) while the DMMA path is exactly scaling
+// invariant.  Before a call that would use them, the spread of the row-maximum exponents
+// and of the column-maximum exponents of the input is estimated on every 16th row; above
+// OZ_MAX_SPREAD binades the call runs every product on DMMA.  Skipped under stream
+// capture (it needs one 16-byte device-to-host read).
+constexpr int OZ_MAX_SPREAD = 20;
+constexpr int SPREAD_STRIDE = 16;   // rows sampled
+constexpr int SPREAD_GROUPS = 8;    // row groups of the column pass
+// Per call: the check kernels run first on the call's stream and copy their 4 exponents
+// per checked matrix to pinned host memory behind an event; the decision is taken (event
+// synchronize) only when the first INT8-eligible product is reached, so the host waits
+// while the GPU works through the leaves and the small DMMA levels: no pipeline bubble.
+struct ScaleCheck {
+  int* dev = nullptr;        // [2 matrices][4] exponents + [n] column maxima bits follow
+  int* host = nullptr;       // pinned [8]
+  cudaEvent_t ev = nullptr;
+  int nmat = 0;              // matrices checked in this call
+  bool pending = false;
+};
+static thread_local ScaleCheck g_check[64];
+static thread_local bool g_int8_veto = false;
+static thread_local ScaleCheck* g_pending = nullptr;
+// RAII scope of one public call (active = true): fresh veto / pending-check state, the
+// caller's restored at exit.  Internal calls (active = false) share their caller's state.
+struct Int8Scope {
+  bool active, prev_veto = false;
+  ScaleCheck* prev_pending = nullptr;
+  explicit Int8Scope(bool a) : active(a) {
+    if (!active) return;
+    prev_veto = g_int8_veto;
+    prev_pending = g_pending;
+    g_int8_veto = false;
+    g_pending = nullptr;
+  }
+  ~Int8Scope() {
+    if (!active) return;
+    if (g_pending) g_pending->pending = false;
+    g_int8_veto = prev_veto;
+    g_pending = prev_pending;
+  }
+};
+__device__ __forceinline__ int spread_exp(double m) {
+  int e;
+  frexp(m, &e);
+  return e;
+}
+__global__ void spread_init_kernel(int* r, unsigned long long* cmax, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) cmax[j] = 0ull;
+  if (j == 0) { r[0] = r[2] = 1 << 30; r[1] = r[3] = -(1 << 30); }
+}
+// row maxima of rows 0, 16, 32, ... over their referenced part (uplo 'L' / 'U' / 'N')
+__global__ void spread_rows_kernel(const double* A, int64_t lda, int n, char uplo, int* r) {
+  __shared__ double red[8];
+  const int i = blockIdx.x * SPREAD_STRIDE;
+  const int j0 = uplo == 'U' ? i : 0, j1 = uplo == 'L' ? i + 1 : n;
+  double m = 0.0;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) m = fmax(m, fabs(A[(int64_t)i * lda + j]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    if (m > 0.0 && m <= 1.7976931348623157e308) {
+      const int e = spread_exp(m);
+      atomicMin(&r[0], e);
+      atomicMax(&r[1], e);
+    }
+  }
+}
+// column maxima over the sampled rows: thread per column, SPREAD_GROUPS row groups
+__global__ void spread_cols_kernel(const double* A, int64_t lda, int n, char uplo, unsigned long long* cmax) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double m = 0.0;
+#pragma unroll 4
+  for (int i = blockIdx.y * SPREAD_STRIDE; i < n; i += SPREAD_GROUPS * SPREAD_STRIDE)
+    if ((uplo == 'L' && j <= i) || (uplo == 'U' && j >= i) || uplo == 'N') m = fmax(m, fabs(A[(int64_t)i * lda + j]));
+  if (m > 0.0) atomicMax(&cmax[j], (unsigned long long)__double_as_longlong(m));
+}
+__global__ void spread_colred_kernel(const unsigned long long* cmax, int n, int* r) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double m = __longlong_as_double((long long)cmax[j]);
+  if (m > 0.0 && m <= 1.7976931348623157e308) {
+    const int e = spread_exp(m);
+    atomicMin(&r[2], e);
+    atomicMax(&r[3], e);
+  }
+}
+// launch the check of one input matrix of the current call (no-op under stream capture)
+static void int8_check_begin(const double* A, int64_t lda, int64_t n, char uplo, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  ScaleCheck& c = g_check[dev];
+  static thread_local int64_t cap[64] = {};
+  if (!c.host) {
+    if (cudaMallocHost(&c.host, 8 * sizeof(int)) != cudaSuccess) { c.host = nullptr; return; }
+    if (cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming) != cudaSuccess) return;
+  }
+  if (cap[dev] < n) {  // [8 ints | 2 x n column maxima]
+    if (c.dev) cudaFree(c.dev);
+    if (cudaMalloc(&c.dev, 256 + 2 * (size_t)n * 8) != cudaSuccess) { c.dev = nullptr; cap[dev] = 0; return; }
+    cap[dev] = n;
+  }
+  if (g_pending != &c) { c.nmat = 0; c.pending = true; g_pending = &c; }
+  if (c.nmat >= 2) return;
+  int* r = c.dev + 4 * c.nmat;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c.dev) + 256) + c.nmat * n;
+  spread_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(r, cmax, (int)n);
+  spread_rows_kernel<<<(unsigned)((n + SPREAD_STRIDE - 1) / SPREAD_STRIDE), 256, 0, s>>>(A, lda, (int)n, uplo, r);
+  spread_cols_kernel<<<dim3((unsigned)((n + 255) / 256), SPREAD_GROUPS), 256, 0, s>>>(A, lda, (int)n, uplo, cmax);
+  spread_colred_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cmax, (int)n, r);
+  g_launches += 4;
+  ++c.nmat;
+  cudaMemcpyAsync(c.host, c.dev, 4 * c.nmat * sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaEventRecord(c.ev, s);
+}
+// the veto for the current call: resolves a pending check (waits for its event only)
+static bool int8_veto() {
+  if (g_pending && g_pending->pending) {
+    ScaleCheck& c = *g_pending;
+    c.pending = false;
+    if (cudaEventSynchronize(c.ev) == cudaSuccess) {
+      for (int m = 0; m < c.nmat; ++m) {
+        const int* h = c.host + 4 * m;
+        const int sr = h[1] >= h[0] ? h[1] - h[0] : 0, sc = h[3] >= h[2] ? h[3] - h[2] : 0;
+        if (std::max(sr, sc) > OZ_MAX_SPREAD) g_int8_veto = true;
+      }
+    }
+  }
+  return g_int8_veto;
+}
+// whether a call of order n would run any product on an INT8 engine (sizes only)
+static bool int8_would_run(int64_t n) { return product_engine() != 0 && n >= g_oz_min.load(); }
+
 // Number of merges at level b: g with 2gb + b < n.
 static int64_t merges_at(int64_t n, int64_t b) { return (n - b + 2 * b - 1) / (2 * b); }
 
@@ -264,7 +405,7 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       l1.mode = MODE_UPPER_1; l1.opA = xr; l1.opB = in;
       l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
     }
-    if (oz_level_ok(n, b)) {  // opt-in: both products of every merge on the INT8 tensor cores
+    if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
       void* ozws = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
       for (int64_t g = 0; g < merges; ++g) {
         const int64_t s0 = 2 * g * b, r = std::min(b, n - s0 - b);
@@ -307,6 +448,9 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   if (st != TRINV_OK || n == 0) return st;
   const size_t need = tri_ws(n, A, lda, X, ldx);
   if (ws_bytes < need || (need > 0 && ws == nullptr)) return TRINV_WORKSPACE_TOO_SMALL;
+  // public entries check the input's scaling for the INT8 engines; internal calls inherit
+  Int8Scope scope(init_info);
+  if (init_info && int8_would_run(n)) int8_check_begin(A, lda, n, uplo, s);
   if (init_info && info) TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (n <= BLK_MAX) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
 
@@ -561,7 +705,7 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
   auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                   int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
-    if (ozws && lu_gemm_on_int8(M, N, K))
+    if (ozws && lu_gemm_on_int8(M, N, K) && !int8_veto())
       return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, st,
                                        &g_launches));
     GemmArgs g{};
@@ -617,6 +761,11 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0) +
                       (ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : 0);
   if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
+  Int8Scope scope(true);
+  if (int8_would_run(n)) {
+    int8_check_begin(Lf, ldl, n, 'L', s);
+    int8_check_begin(Uf, ldu, n, 'U', s);
+  }
   char* p = static_cast<char*>(ws);
   double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
   double* Li = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
@@ -630,7 +779,7 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   double* Xuse = X;
   int64_t ldx_use = ldx;
   if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; p += align_up(mat_bytes(n)); }
-  if (ul_on_int8(n)) {  // S K on the INT8 tensor cores (k >= max(i, j))
+  if (ul_on_int8(n) && !int8_veto()) {  // S K on the INT8 tensor cores (k >= max(i, j))
     TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, p, s, &g_launches));
   } else {
     LevelArgs ul{};
@@ -781,6 +930,8 @@ trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int
   if (ws_bytes < beta4_ws(n) || !ws) return TRINV_WORKSPACE_TOO_SMALL;
   cudaStream_t s = (cudaStream_t)stream;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
+  Int8Scope scope(true);
+  if (int8_would_run(n)) int8_check_begin(A, lda, n, uplo, s);
   return run_tri_beta4(uplo, n, A, lda, X, ldx, (int)diag, static_cast<char*>(ws), d_info, s);
 }
 
@@ -891,6 +1042,8 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   if (overlap(A, lda, X, ldx, n)) return TRINV_ALIASING;
   const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
   if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
+  Int8Scope scope(true);
+  if (int8_would_run(n)) int8_check_begin(A, lda, n, 'N', s);
   const int64_t lde = even_up(n);
   // workspace: [F packed factors | W working copy of A | K = L^{-1} | S = U^{-1} | T | X staging]
   char* p = static_cast<char*>(ws);
@@ -911,7 +1064,7 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, ozws);
   if (st != TRINV_OK) return st;
   // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
-  if (ul_on_int8(n)) {
+  if (ul_on_int8(n) && !int8_veto()) {
     TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, ozws, s, &g_launches));
   } else {
     LevelArgs ul{};

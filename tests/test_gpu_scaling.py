@@ -6,7 +6,9 @@ INT8 CRT engine truncates its operands to P-bit integers relative to row / colum
 so scalings that differ along the product's K dimension change which entries survive: its
 error grows with the spread of the scaling (tools/scaling_probe.py: 2.9e-15 at |k| <= 8,
 1.2e-10 at |k| <= 16, 9e-4 at |k| >= 30); the test holds it to 1e-12 at
-|k| <= 8."""
+|k| <= 8.  Above a 2^20 spread of the input's row / column maxima the library runs every
+product on DMMA (the scaling guard), which makes the default engine exactly invariant
+there too."""
 import numpy as np
 import pytest
 
@@ -67,3 +69,39 @@ def test_pow2_scaling_invariance_inv_from_lu(engine, R):
             assert np.max(E) <= 1e-12 * max(1.0, np.max(np.abs(Y))), np.max(E)
     finally:
         P.set_product_engine()
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_scaling_guard_falls_back_to_dmma(uplo):
+    """Default engine on a 2^+-60 scaled input: the guard sends every product to DMMA, so
+    the result is bit-for-bit the DMMA result (and scaling invariant)."""
+    n = 1024
+    rng = np.random.default_rng(13)
+    k1 = rng.integers(-60, 61, n); k2 = rng.integers(-60, 61, n)
+    T = synth.host(n, seed=9, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    S = torch.from_numpy(np.ldexp(np.ldexp(T, k1[:, None]), k2[None, :])).to(DEV)
+    f = P.trinv_lower if uplo == "L" else P.trinv_upper
+    try:
+        P.set_product_engine("int8crt", min_block=256)
+        X8 = f(S).cpu().numpy()
+        P.set_product_engine("dmma")
+        Xd = f(S).cpu().numpy()
+    finally:
+        P.set_product_engine()
+    assert np.array_equal(X8, Xd)
+
+
+def test_scaling_guard_keeps_int8_on_well_scaled_input():
+    """The BASELINE distribution (row / column maxima within a few binades) keeps the INT8
+    engine: its result differs from the DMMA one in the last bits."""
+    n = 1024
+    T = torch.from_numpy(synth.host(n, seed=9, diag="signed")).to(DEV)
+    try:
+        P.set_product_engine("int8crt", min_block=256)
+        X8 = P.trinv_lower(T).cpu().numpy()
+        P.set_product_engine("dmma")
+        Xd = P.trinv_lower(T).cpu().numpy()
+    finally:
+        P.set_product_engine()
+    assert not np.array_equal(X8, Xd)
+    assert np.max(np.abs(X8 - Xd)) <= 1e-12 * np.max(np.abs(Xd))

@@ -204,7 +204,8 @@ trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, cons
  * digits * K * 127^2 < 2^31 (K <= 16384 at 8 digits), else TRINV_NOT_SUPPORTED.
  * digits <= 0 selects the modular variant instead: operands scaled to P-bit integers
  * (P = 55 at K = 16384), 16 int8 products modulo 16 pairwise coprime moduli <= 256 and
- * an exact CRT reconstruction (Garner, 128-bit) of the integer product (K <= 65536).
+ * an exact CRT reconstruction (rounded quotient, 128-bit limbs) of the integer product
+ * (K <= 65536).
  * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, digits) bytes. */
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits);
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
@@ -212,13 +213,18 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
                              int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream);
 
 /* Product engine for the level products of trinv_lower / trinv_upper (and the
- * triangular inverses inside inv_from_lu / lu_crout): engine 0 = FP64 DMMA
- * (mma.sync), 1 = the INT8 tensor-core engine above with `digits` digits, 2 (default)
- * = its modular (CRT) variant; engines 1 and 2 take every level whose block size is
- * >= min_block (>= 256; default 4096) and whose shapes fit their envelope, all other
- * levels stay on DMMA.  Process-wide; the environment variable
+ * triangular inverses inside inv_from_lu, its U^-1 L^-1 product and the LU products of
+ * inv_general): engine 0 = FP64 DMMA (mma.sync), 1 = the INT8 tensor-core engine above
+ * with `digits` digits, 2 (default) = its modular (CRT) variant; engines 1 and 2 take
+ * every product whose blocks are >= min_block (>= 256; default 4096) and whose shapes
+ * fit their envelope, all other products stay on DMMA.  Scaling guard: when the input's
+ * row- or column-maximum exponents (every 16th row sampled) span more than 20 binades,
+ * the call runs every product on DMMA (the INT8 engines' truncation is relative to row /
+ * column maxima); the check costs one 16-byte device-to-host read per
+ * call, resolved by an event when the first INT8 product is reached, and is skipped
+ * under stream capture.  Process-wide; the environment variable
  * TRINV_PRODUCTS=dmma|int8|int8crt selects the engine before the first call.  Changing
- * it changes trinv_workspace_bytes ('L', 'U', 'G', 'F'): query the workspace after. */
+ * it changes trinv_workspace_bytes ('L', 'U', 'G', 'A', 'F'): query the workspace after. */
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
 int trinv_get_product_engine(void);
 

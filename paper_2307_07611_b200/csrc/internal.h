@@ -143,6 +143,8 @@ cudaError_t launch_geam(int64_t rows, int64_t cols, double alpha, const double* 
                         const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s, int64_t* launches);
 // p[i*ld + j] = +0.0 for i < rows, j < cols.
 cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches);
+cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                           cudaStream_t s, int64_t* launches);
 
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.

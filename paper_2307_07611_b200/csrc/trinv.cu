@@ -463,7 +463,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
     double* As = reinterpret_cast<double*>(p);
     p += align_up(mat_bytes(n));
     lda_use = even_up(n);
-    TRY(cudaMemcpy2DAsync(As, lda_use * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+    TRY(launch_copy_2d(A, lda, As, lda_use, n, n, s, &g_launches));
     Ause = As;
   }
   double* Xuse = X;
@@ -475,7 +475,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   }
   st = run_tri(uplo, n, Ause, lda_use, Xuse, ldx_use, diag, W, info, info_off, s);
   if (st != TRINV_OK) return st;
-  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  if (stage_x) TRY(launch_copy_2d(Xuse, ldx_use, X, ldx, n, n, s, &g_launches));
   return TRINV_OK;
 }
 
@@ -605,7 +605,7 @@ static trinv_status_t lu_rec(int64_t n, double* W, int64_t ldw, double* F, int64
   g.C = inplace ? T : F12; g.ldc = inplace ? ldr : ldf;
   g.alpha = 1.0; g.beta = 0.0; g.triA = TRI_LOWER; g.triB = TRI_NONE;
   TRY(launch_gemm(g, s, &g_launches));
-  if (inplace) TRY(cudaMemcpy2DAsync(F12, ldf * 8, T, ldr * 8, r * 8, h, cudaMemcpyDeviceToDevice, s));
+  if (inplace) TRY(launch_copy_2d(T, ldr, F12, ldf, h, r, s, &g_launches));
   // L21 = A21 U11^{-1}  (r x h; U11^{-1} upper: K-range k <= column)
   GemmArgs g2{};
   g2.M = r; g2.N = h; g2.K = h; g2.batch = 1;
@@ -613,7 +613,7 @@ static trinv_status_t lu_rec(int64_t n, double* W, int64_t ldw, double* F, int64
   g2.C = inplace ? T : F21; g2.ldc = inplace ? ldh : ldf;
   g2.alpha = 1.0; g2.beta = 0.0; g2.triA = TRI_NONE; g2.triB = TRI_UPPER;
   TRY(launch_gemm(g2, s, &g_launches));
-  if (inplace) TRY(cudaMemcpy2DAsync(F21, ldf * 8, T, ldh * 8, h * 8, r, cudaMemcpyDeviceToDevice, s));
+  if (inplace) TRY(launch_copy_2d(T, ldh, F21, ldf, r, h, s, &g_launches));
   // Schur complement W22 <- A22 - L21 U12
   GemmArgs g3{};
   g3.M = r; g3.N = r; g3.K = h; g3.batch = 1;
@@ -788,7 +788,7 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
     ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
     TRY(launch_level(ul, s, &g_launches));
   }
-  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  if (stage_x) TRY(launch_copy_2d(Xuse, ldx_use, X, ldx, n, n, s, &g_launches));
   return TRINV_OK;
 }
 
@@ -1059,7 +1059,7 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const size_t oz_bytes = std::max(lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
   void* ozws = oz_bytes ? static_cast<void*>(take(oz_bytes)) : nullptr;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
-  TRY(cudaMemcpy2DAsync(Wk, lde * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  TRY(launch_copy_2d(A, lda, Wk, lde, n, n, s, &g_launches));
   // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
   trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, ozws);
   if (st != TRINV_OK) return st;
@@ -1073,7 +1073,7 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
     ul.out = Xuse; ul.ldo = ldx_use; ul.out_rows = n; ul.out_cols = n; ul.alpha = 1.0;
     TRY(launch_level(ul, s, &g_launches));
   }
-  if (stage_x) TRY(cudaMemcpy2DAsync(X, ldx * 8, Xuse, ldx_use * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+  if (stage_x) TRY(launch_copy_2d(Xuse, ldx_use, X, ldx, n, n, s, &g_launches));
   return TRINV_OK;
 }
 

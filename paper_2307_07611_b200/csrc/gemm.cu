@@ -529,7 +529,7 @@ cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t 
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const bool vec = ((lds | ldd) & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
   const int64_t per_row = vec ? (cols / 2 + 255) / 256 : (cols + 255) / 256;
-  const unsigned gx = (unsigned)(per_row < 8 ? per_row : 8);
+  const unsigned gx = (unsigned)(per_row < 1 ? 1 : (per_row < 8 ? per_row : 8));
   const unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
   copy_2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, vec);
   if (launches) ++*launches;

@@ -480,7 +480,9 @@ def main():
                      else "oz2_gemm_kernel (INT8 tcgen05, 16 moduli + CRT)")
             line["roofline"] = {"bound": "tensor", "kernel": kname,
                                 "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
-                                "traffic": None,
+                                "traffic": ncu_traffic("oz2_gemm_kernel") if args.products == "int8crt" else None,
+                                "traffic_note": "DRAM bytes of one top-level product launch of config 3 (ncu --set "
+                                                "full); a tensor-bound kernel: for comparison with its operand bytes",
                                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8 / bf16)",
                                 "int8_share_of_step": ms_o / (args.steps * ms_per_step),
                                 "int8_fp64_equivalent_tflops": fl_o / (ms_o / 1e3) / 1e12,

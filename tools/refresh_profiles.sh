@@ -27,8 +27,10 @@ ncu --set full --clock-control none --import-source on -k regex:leaf32_tma -s 3 
 ncu --set full --clock-control none --import-source on -k regex:blk_kernel -s 3 -c 1 -o gpurun_out/full_blk $CMD0 > gpurun_out/ncu_f0.log 2>&1
 TRINV_PRODUCTS=dmma ncu --set full --clock-control none --import-source on -k regex:dmma_level -s 10 -c 2 -o gpurun_out/full_dmma_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:oz2_gemm -c 2 -o gpurun_out/full_oz2_c2 python tools/prof_one.py L 8192 > gpurun_out/ncu_f2oz.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:oz2_gemm -s 12 -c 2 -o gpurun_out/full_oz2_c3 python tools/prof_one.py U 32768 > gpurun_out/ncu_f3oz.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"oz2_split|oz2_recon|oz2_colmax" -s 6 -c 4 -o gpurun_out/full_oz2aux_c3 python tools/prof_one.py U 32768 > gpurun_out/ncu_f3aux.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:leaf64_tma -c 1 -o gpurun_out/full_leaf64 python tools/sweep_batched.py 64 > gpurun_out/ncu_f64.log 2>&1
-for f in full_leaf32 full_blk full_dmma_c2 full_oz2_c2 full_leaf64; do
+for f in full_leaf32 full_blk full_dmma_c2 full_oz2_c2 full_oz2_c3 full_oz2aux_c3 full_leaf64; do
   [ -f gpurun_out/$f.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$f.ncu-rep > gpurun_out/$f.txt 2>&1
 done
 ls -la gpurun_out >> gpurun_out/steps.log

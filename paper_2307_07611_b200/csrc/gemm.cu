@@ -30,6 +30,8 @@
 // zero-filled by TMA and clipped at the store.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -468,8 +470,12 @@ double gemm_flops(const GemmArgs& a) {
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.M <= 0 || a.N <= 0 || a.batch <= 0) return cudaSuccess;
   ProfileScope prof(KIND_DMMA, gemm_flops(a), 0.0, s);
+  // tiles per SM required before a larger tile is taken (experiments: TRINV_GEMM_WAVES)
+  static const double waves = [] { const char* e = std::getenv("TRINV_GEMM_WAVES"); return e ? std::atof(e) : 2.0; }();
   auto tiles = [&](int64_t T) { return a.batch * ((a.M + T - 1) / T) * ((a.N + T - 1) / T); };
-  const int64_t t = pick_tile(tiles, 128);
+  int64_t t = 32;
+  for (int64_t T : {128, 64})
+    if (tiles(T) >= (int64_t)(waves * device_sms())) { t = T; break; }
   if (t >= 128) return launch_gemm_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_gemm_cfg<64, 64, 2, 2, 4>(a, s, launches);
   return launch_gemm_cfg<32, 32, 2, 2, 4>(a, s, launches);

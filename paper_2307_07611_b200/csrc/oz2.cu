@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 
 #include "internal.h"
@@ -109,8 +110,8 @@ __device__ __forceinline__ void oz2_residues4(const int64_t (&v)[4], uint32_t* o
 // The K range the GEMM reads for row i of a triangular A (tile rows of OZ2_TM) or column
 // j of a triangular B (tile columns of OZ2_TN), oz2_gemm_kernel's kb..ke: only that range
 // is scaled and split (the rest of a triangular operand is zero and never read).
-__device__ __forceinline__ void oz2_k_range(int tri, bool is_a, int idx, int K, int& kb, int& ke) {
-  const int tile = is_a ? OZ2_TM : OZ2_TN;
+__device__ __forceinline__ void oz2_k_range(int tri, bool is_a, int idx, int K, int& kb, int& ke, int tma = OZ2_TM) {
+  const int tile = is_a ? tma : OZ2_TN;
   const bool upto = is_a ? tri == TRI_LOWER : tri == TRI_UPPER;  // k < end of idx's tile
   const bool from = is_a ? tri == TRI_UPPER : tri == TRI_LOWER;  // k >= start of idx's tile
   kb = from ? (idx / tile) * tile : 0;
@@ -119,11 +120,11 @@ __device__ __forceinline__ void oz2_k_range(int tri, bool is_a, int idx, int K, 
 // A operand (rows x K, row-major): one warp per row; exponent e_i of the row maximum;
 // each lane converts 4 consecutive entries per step (K % 4 == 0).
 __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, int K, int tri, bool strict, int P,
-                                      int8_t* out, int* expo) {
+                                      int tma, int8_t* out, int* expo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   int kb, ke;
-  oz2_k_range(tri, true, warp, K, kb, ke);
+  oz2_k_range(tri, true, warp, K, kb, ke, tma);  // the K range of the GEMM's row tile (tma rows)
   const double* a = A + (int64_t)warp * lda;
   double m = 0.0;
   const int kz = strict ? warp : -1;  // a diagonal read as zero
@@ -353,6 +354,203 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * OZ2_TN));
 }
 
+// ---- CTA-pair variant (cta_group::2): one 256 x 256 tile per cluster of two CTAs ------
+// Each CTA of the pair stages its 128 rows of A and its 128 columns of B per K block
+// (32 KB per stage instead of 48: 6 stages in the same shared memory, i.e. twice the
+// bytes in flight per output row), the leader CTA issues tcgen05.mma.cta_group::2
+// (M 256, N 256, K 32) over both CTAs' shared memory, each CTA's TMEM holds its 128
+// rows x 256 columns.  Protocol: both producers' TMA complete on the leader's full
+// barrier (which the leader arms with both halves' bytes); the leader's commits arrive
+// on the empty / acc_full barriers of both CTAs (multicast); both CTAs' epilogue warps
+// arrive on the leader's acc_empty barrier (8 arrivals).
+constexpr int OZ2P_STAGES = 6;
+constexpr int OZ2P_A_BYTES = 128 * OZ2_TK, OZ2P_B_BYTES = 128 * OZ2_TK, OZ2P_STAGE = OZ2P_A_BYTES + OZ2P_B_BYTES;
+constexpr size_t OZ2P_SMEM = (size_t)OZ2P_STAGES * OZ2P_STAGE + 1024 + 256;
+
+__device__ __forceinline__ uint32_t oz2_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t oz2_leader_addr(const void* p) {  // same smem offset in cluster CTA 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void oz2_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ2_THREADS, 1)
+    oz2_gemm_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
+                         const Oz2Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* sA = base;
+  unsigned char* sB = base + OZ2P_STAGES * OZ2P_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + OZ2P_STAGES * OZ2P_STAGE);
+  uint64_t* empty = full + OZ2P_STAGES;
+  uint64_t* acc_full = empty + OZ2P_STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2], leader's used
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = oz2_cluster_rank();
+  const int tiles_m = p.M / 256;  // row-pair tiles
+  const int t = (blockIdx.x >> 1) / p.msplit;
+  const int nmod = OZ2_NMOD / p.msplit, mod0 = ((blockIdx.x >> 1) % p.msplit) * nmod;
+  int I, J;
+  if (p.triA != TRI_NONE && p.triB == TRI_NONE) {
+    const int per_group = OZ2_GROUP_M * tiles_m;
+    const int first_n = (t / per_group) * OZ2_GROUP_M;
+    const int gsz = min(p.tiles_n - first_n, OZ2_GROUP_M);
+    J = first_n + (t % per_group) % gsz;
+    I = (t % per_group) / gsz;
+  } else {
+    const int per_group = OZ2_GROUP_M * p.tiles_n;
+    const int first_m = (t / per_group) * OZ2_GROUP_M;
+    const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
+    I = first_m + (t % per_group) % gsz;
+    J = (t % per_group) / gsz;
+  }
+  if (p.triA == TRI_LOWER) I = tiles_m - 1 - I;
+  if (p.triB == TRI_UPPER) J = p.tiles_n - 1 - J;
+  int kb = 0, ke = p.K;  // K range of the 256-row pair tile
+  if (p.triA == TRI_LOWER) ke = min(ke, (I + 1) * 256);
+  if (p.triA == TRI_UPPER) kb = I * 256;
+  if (p.triB == TRI_LOWER) kb = max(kb, J * OZ2_TN);
+  if (p.triB == TRI_UPPER) ke = min(ke, (J + 1) * OZ2_TN);
+  const int nkb = ke > kb ? (ke - kb) / OZ2_TK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ2P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 8); }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * OZ2_TN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  oz2_cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {  // TMA producer (both CTAs): this CTA's A rows and B columns
+    tma_prefetch_desc(&ma);
+    tma_prefetch_desc(&mb);
+    int it = 0;
+    for (int i = mod0; i < mod0 + nmod; ++i)
+      for (int kk = 0; kk < nkb; ++kk, ++it) {
+        const int st = it % OZ2P_STAGES, use = it / OZ2P_STAGES;
+        if (use > 0) mbar_wait(&empty[st], (uint32_t)((use - 1) & 1));
+        if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * OZ2P_STAGE);
+        const uint32_t fb = oz2_leader_addr(&full[st]);
+        const int k = kb + kk * OZ2_TK;
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+            "%3}], [%4];\n" ::"r"(smem_u32(sA + st * OZ2P_A_BYTES)),
+            "l"(reinterpret_cast<uint64_t>(&ma)), "r"(k), "r"(i * p.M + I * 256 + (int)rank * 128), "r"(fb)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+            "%3}], [%4];\n" ::"r"(smem_u32(sB + st * OZ2P_B_BYTES)),
+            "l"(reinterpret_cast<uint64_t>(&mb)), "r"(k), "r"(i * p.N + J * OZ2_TN + (int)rank * 128), "r"(fb)
+            : "memory");
+      }
+  } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer (leader CTA)
+    const uint32_t idesc =
+        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    int it = 0;
+    for (int i = mod0; i < mod0 + nmod; ++i) {
+      const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
+      if (use > 0) {
+        mbar_wait(&acc_empty[buf], (uint32_t)((use - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      }
+      const uint32_t tacc = tmem + (uint32_t)(buf * OZ2_TN);
+      bool first = true;
+      for (int kk = 0; kk < nkb; ++kk, ++it) {
+        const int st = it % OZ2P_STAGES;
+        mbar_wait(&full[st], (uint32_t)((it / OZ2P_STAGES) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint64_t da = oz2_smem_desc(sA + st * OZ2P_A_BYTES), db = oz2_smem_desc(sB + st * OZ2P_B_BYTES);
+#pragma unroll
+        for (int k = 0; k < OZ2_TK / 32; ++k) {
+          const uint32_t acc = first ? 0u : 1u;
+          first = false;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tacc),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(idesc), "r"(acc));
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                smem_u32(&empty[st])),
+            "h"((uint16_t)3)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+              smem_u32(&acc_full[buf])),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+  }
+  if (warp >= 2) {  // epilogue (both CTAs): this CTA's 128 rows of the pair tile
+    const int q4 = warp & 3;
+    const int row = I * 256 + (int)rank * 128 + q4 * 32 + lane;
+    for (int i = mod0; i < mod0 + nmod; ++i) {
+      const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
+      mbar_wait(&acc_full[buf], (uint32_t)(use & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int m = oz2_mod(i);
+      const double rm = 1.0 / m;
+      uint8_t* dst = p.R + ((size_t)i * p.M + row) * p.N + J * OZ2_TN;
+#pragma unroll 1
+      for (int c = 0; c < OZ2_TN; c += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * OZ2_TN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        uint32_t packed[8];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int x = nkb ? (int)v[j + b] : 0;
+            int r = x - (int)floor((double)x * rm) * m;
+            r += (r < 0) ? m : 0;
+            r -= (r >= m) ? m : 0;
+            w |= (uint32_t)r << (8 * b);
+          }
+          packed[j / 4] = w;
+        }
+        *reinterpret_cast<uint4*>(dst + c) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                         oz2_leader_addr(&acc_empty[buf]))
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  oz2_cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * OZ2_TN));
+}
+
 // ---- reconstruction: C' = sum_i c_i w_i - q M -------------------------------------------
 // w_i = M_i (M_i^-1 mod m_i) mod M (so sum_i c_i w_i == C' mod M) in 32-bit limbs
 // w_i = sum_l w_il 2^(32 l).  S = sum_i c_i w_i < 2^138; as |C'| < M/2 by a margin (P from
@@ -509,10 +707,20 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   };
   const double ea_n = range_sum(M, OZ2_TM, triA == TRI_LOWER, triA == TRI_UPPER);
   const double eb_n = range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER);
+  // CTA-pair GEMM (cta_group::2) for products with M % 256 == 0 and all dimensions >=
+  // pair_min (TRINV_OZ2_PAIR = 0 disables, = <n> sets pair_min; default 8192: the pair
+  // kernel won at the 8192 and 16384 levels, not at 4096, profiles/r01_oz2_pair.txt)
+  static const int64_t pair_min = [] {
+    const char* e = std::getenv("TRINV_OZ2_PAIR");
+    if (!e) return (int64_t)8192;
+    const long long v = std::atoll(e);
+    return v <= 0 ? (int64_t)1 << 62 : (int64_t)v;
+  }();
+  const bool pair = M % 256 == 0 && std::min(M, std::min(N, K)) >= pair_min;
   {
     ProfileScope aux(KIND_OZAUX, 0.0, 24.0 * ea_n + 32.0 * eb_n, st);
     oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, (strict & 1) != 0,
-                                                                               P, As, ea);
+                                                                               P, pair ? 256 : OZ2_TM, As, ea);
     cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
     if (e != cudaSuccess) return e;
     oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + OZ2_CMAX_ROWS - 1) / OZ2_CMAX_ROWS)), 256, 0,
@@ -523,19 +731,25 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   }
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
-      !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, OZ2_TN))
+      !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, pair ? 128 : OZ2_TN))
     return cudaErrorInvalidValue;
   Oz2Params p{};
   p.M = (int)M; p.N = (int)N; p.K = (int)K; p.triA = triA; p.triB = triB; p.R = Rs;
   p.tiles_n = (int)(N / OZ2_TN);
   // below ~6 waves of tiles, each tile's moduli are split over 2 or 4 CTAs so the last
   // partial wave is a small fraction (the level-4096 products: 512 tiles on 148 SMs)
-  const int64_t tiles = (M / OZ2_TM) * (N / OZ2_TN), waves6 = 6 * (int64_t)device_sms();
-  p.msplit = tiles >= waves6 ? 1 : (2 * tiles >= waves6 ? 2 : 4);
-  set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
+  const int64_t ctas = pair ? 2 * (M / 256) * (N / OZ2_TN) : (M / OZ2_TM) * (N / OZ2_TN);
+  const int64_t waves6 = 6 * (int64_t)device_sms();
+  p.msplit = ctas >= waves6 ? 1 : (2 * ctas >= waves6 ? 2 : 4);
   {
     ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
-    oz2_gemm_kernel<<<(unsigned)(tiles * p.msplit), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+    if (pair) {
+      set_smem_once<oz2_gemm_pair_kernel>((int)OZ2P_SMEM);
+      oz2_gemm_pair_kernel<<<(unsigned)(ctas * p.msplit), OZ2_THREADS, OZ2P_SMEM, st>>>(ma, mb, p);
+    } else {
+      set_smem_once<oz2_gemm_kernel>((int)OZ2_SMEM);
+      oz2_gemm_kernel<<<(unsigned)(ctas * p.msplit), OZ2_THREADS, OZ2_SMEM, st>>>(ma, mb, p);
+    }
   }
   const int64_t total4 = M * N / 4;
   static const Oz2Crt crt = oz2_crt_constants();

@@ -363,7 +363,10 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
 // barrier (which the leader arms with both halves' bytes); the leader's commits arrive
 // on the empty / acc_full barriers of both CTAs (multicast); both CTAs' epilogue warps
 // arrive on the leader's acc_empty barrier (8 arrivals).
-constexpr int OZ2P_STAGES = 6;
+#ifndef OZ2P_NSTAGES
+#define OZ2P_NSTAGES 6
+#endif
+constexpr int OZ2P_STAGES = OZ2P_NSTAGES;
 constexpr int OZ2P_A_BYTES = 128 * OZ2_TK, OZ2P_B_BYTES = 128 * OZ2_TK, OZ2P_STAGE = OZ2P_A_BYTES + OZ2P_B_BYTES;
 constexpr size_t OZ2P_SMEM = (size_t)OZ2P_STAGES * OZ2P_STAGE + 1024 + 256;
 

@@ -367,6 +367,9 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
 #define OZ2P_NSTAGES 6
 #endif
 constexpr int OZ2P_STAGES = OZ2P_NSTAGES;
+#ifndef OZ2P_GROUP
+#define OZ2P_GROUP 8  // raster group of the pair kernel (in 256-row / 256-column pair tiles)
+#endif
 constexpr int OZ2P_A_BYTES = 128 * OZ2_TK, OZ2P_B_BYTES = 128 * OZ2_TK, OZ2P_STAGE = OZ2P_A_BYTES + OZ2P_B_BYTES;
 constexpr size_t OZ2P_SMEM = (size_t)OZ2P_STAGES * OZ2P_STAGE + 1024 + 256;
 
@@ -401,17 +404,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ2_THREADS, 1)
   const int tiles_m = p.M / 256;  // row-pair tiles
   const int t = (blockIdx.x >> 1) / p.msplit;
   const int nmod = OZ2_NMOD / p.msplit, mod0 = ((blockIdx.x >> 1) % p.msplit) * nmod;
+  // raster group: 4 pair tiles for dense products, 8 with a triangular operand (r01_oz2_pair.txt)
+  const int G = (p.triA == TRI_NONE && p.triB == TRI_NONE) ? 4 : OZ2P_GROUP;
   int I, J;
   if (p.triA != TRI_NONE && p.triB == TRI_NONE) {
-    const int per_group = OZ2_GROUP_M * tiles_m;
-    const int first_n = (t / per_group) * OZ2_GROUP_M;
-    const int gsz = min(p.tiles_n - first_n, OZ2_GROUP_M);
+    const int per_group = G * tiles_m;
+    const int first_n = (t / per_group) * G;
+    const int gsz = min(p.tiles_n - first_n, G);
     J = first_n + (t % per_group) % gsz;
     I = (t % per_group) / gsz;
   } else {
-    const int per_group = OZ2_GROUP_M * p.tiles_n;
-    const int first_m = (t / per_group) * OZ2_GROUP_M;
-    const int gsz = min(tiles_m - first_m, OZ2_GROUP_M);
+    const int per_group = G * p.tiles_n;
+    const int first_m = (t / per_group) * G;
+    const int gsz = min(tiles_m - first_m, G);
     I = first_m + (t % per_group) % gsz;
     J = (t % per_group) / gsz;
   }

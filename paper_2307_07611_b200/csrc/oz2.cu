@@ -1,7 +1,7 @@
 // oz2.cu — FP64 products on the INT8 tensor cores by modular arithmetic (a
-// CRT-based Ozaki-type scheme, "Ozaki scheme II"): the second opt-in product
-// engine (DESIGN.md §8 "oz2_gemm_kernel"), 16 int8 GEMMs per FP64 product instead
-// of the 36 digit products of oz.cu.
+// CRT-based Ozaki-type scheme, "Ozaki scheme II"): the default product engine for
+// blocks >= 4096 (DESIGN.md §8 "oz2_gemm_kernel", §11), 16 int8 GEMMs per FP64
+// product instead of the 36 digit products of oz.cu.
 //
 // Scaling.  Row i of A is scaled by 2^(P - e_i), 2^e_i > max_k |a_ik|, and truncated:
 // A'_ik = trunc(a_ik 2^(P - e_i)), an exact integer with |A'| < 2^P (a_ik has 53
@@ -19,7 +19,10 @@
 //
 // The GEMM kernel is the engine of oz.cu (TMA 128B-swizzled K blocks, tcgen05.mma
 // kind::i8, two TMEM accumulators) looping over the 16 moduli instead of digit pairs;
-// its epilogue writes uint8 residues, and a separate kernel reconstructs C.
+// its epilogue writes uint8 residues, and a separate kernel reconstructs C.  Products
+// with all dimensions >= 8192 use the CTA-pair variant (tcgen05.mma.cta_group::2 over
+// two SMs, M 256 x N 256 tiles).  The scaling and residue kernels split only the K
+// range each tile reads of a triangular operand.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

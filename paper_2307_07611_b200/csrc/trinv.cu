@@ -165,7 +165,10 @@ struct Int8Scope {
   }
   ~Int8Scope() {
     if (!active) return;
-    if (g_pending) g_pending->pending = false;
+    if (g_pending && g_pending->pending) {  // never resolved: let its copy land before reuse
+      cudaEventSynchronize(g_pending->ev);
+      g_pending->pending = false;
+    }
     g_int8_veto = prev_veto;
     g_pending = prev_pending;
   }
@@ -265,7 +268,7 @@ static bool int8_veto() {
   return g_int8_veto;
 }
 // whether a call of order n would run any product on an INT8 engine (sizes only)
-static bool int8_would_run(int64_t n) { return product_engine() != 0 && n >= g_oz_min.load(); }
+static bool int8_would_run(int64_t n);  // defined below with the level predicates
 
 // Number of merges at level b: g with 2gb + b < n.
 static int64_t merges_at(int64_t n, int64_t b) { return (n - b + 2 * b - 1) / (2 * b); }
@@ -314,6 +317,14 @@ static size_t oz_scratch(int64_t n) {
     }
   }
   return align_up(best);
+}
+
+// whether a triangular inverse of order n runs any level product on an INT8 engine
+static bool int8_would_run(int64_t n) {
+  if (product_engine() == 0) return false;
+  for (int64_t b = BLK_MAX; b < n; b *= 2)
+    if (oz_level_ok(n, b)) return true;
+  return false;
 }
 
 // The U^{-1} L^{-1} product on the INT8 CRT engine: the diagonals of both factors are split
@@ -762,7 +773,7 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
                       (ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : 0);
   if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
   Int8Scope scope(true);
-  if (int8_would_run(n)) {
+  if (int8_would_run(n) || ul_on_int8(n)) {
     int8_check_begin(Lf, ldl, n, 'L', s);
     int8_check_begin(Uf, ldu, n, 'U', s);
   }
@@ -1043,7 +1054,7 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
   if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
   Int8Scope scope(true);
-  if (int8_would_run(n)) int8_check_begin(A, lda, n, 'N', s);
+  if (lu_oz_ws(n) > 0 || ul_on_int8(n)) int8_check_begin(A, lda, n, 'N', s);
   const int64_t lde = even_up(n);
   // workspace: [F packed factors | W working copy of A | K = L^{-1} | S = U^{-1} | T | X staging]
   char* p = static_cast<char*>(ws);

@@ -751,7 +751,9 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   // partial wave is a small fraction (the level-4096 products: 512 tiles on 148 SMs)
   const int64_t ctas = pair ? 2 * (M / 256) * (N / OZ2_TN) : (M / OZ2_TM) * (N / OZ2_TN);
   const int64_t waves6 = 6 * (int64_t)device_sms();
+  static const int msplit_env = [] { const char* e = std::getenv("TRINV_OZ2_MSPLIT"); return e ? std::atoi(e) : 0; }();
   p.msplit = ctas >= waves6 ? 1 : (2 * ctas >= waves6 ? 2 : 4);
+  if (msplit_env == 1 || msplit_env == 2 || msplit_env == 4 || msplit_env == 8) p.msplit = msplit_env;  // experiments
   {
     ProfileScope prof(KIND_OZ, f64, f64 * OZ2_NMOD, st);  // bytes slot: int8 ops
     if (pair) {

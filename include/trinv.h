@@ -124,7 +124,9 @@ trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const dou
 /* General inverse from triangular factors, X = (L U)^{-1} = U^{-1} L^{-1}
  * (SKUL, "S K = A^{-1}" with S = U^{-1}, K = L^{-1}): L^{-1} and
  * U^{-1} by the two calls above, then the upper x lower product
- * X_ij = sum_{k >= max(i,j)} (U^{-1})_ik (L^{-1})_kj  (P_UL)
+ * X_ij = sum_{k >= max(i,j)} (U^{-1})_ik (L^{-1})_kj  (P_UL):
+ * with the INT8 CRT engine (default, n >= its block threshold) the diagonal terms in
+ * one elementwise pass and the strictly triangular product on the tensor cores, else
  * on the DMMA engine.  Lf (lower, ldl) and Uf (upper, ldu) are read-only; X
  * (ldx) must not overlap either (TRINV_ALIASING).  diagL / diagU select unit
  * factors (the paper's Crout makes U unit; BASELINE config 4 makes L
@@ -142,7 +144,8 @@ trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const doubl
  * strict upper triangle holds U.  Blocked right-looking recursion: diagonal blocks
  * <= 128 in registers of one CTA, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
  * through the triangular inverses above and the DMMA engine, Schur complement on
- * the DMMA engine.  As in the paper there is no pivoting: the leading principal
+ * the DMMA engine (inv_general's own recursion routes its products of blocks >=
+ * 4096 through the INT8 engine).  As in the paper there is no pivoting: the leading principal
  * minors must be non-zero; an exact zero pivot k sets d_info = 1 + k (output then
  * unspecified).  A: device, 16-byte aligned with even lda when n > 128
  * (TRINV_NOT_SUPPORTED otherwise).  ws_bytes >= trinv_workspace_bytes('F', n, ...). */
@@ -150,8 +153,11 @@ trinv_status_t lu_crout(int64_t n, double* A, int64_t lda, void* ws, size_t ws_b
                         void* stream);
 
 /* X = A^{-1} for a general non-singular A with non-zero leading principal minors:
- * lu_crout on a copy of A, then inv_from_lu(L, U unit) — SKUL's S K = A^{-1}
- * (P:799-803).  A is read-only (any layout); X must not overlap A.  2 n^3 flops.
+ * a Crout recursion on a copy of A that builds K = L^{-1} and S = U^{-1} alongside the
+ * factors (the merges of the recursive split reuse the diagonal-block inverses), then
+ * X = S K — SKUL's S K = A^{-1}.  Independent product pairs run on a second
+ * stream forked from and joined to `stream`.  A is read-only (any layout); X must not
+ * overlap A.  2 n^3 flops.
  * ws_bytes >= trinv_workspace_bytes('A', n, A, lda, X, ldx). */
 trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, int64_t ldx, void* ws,
                            size_t ws_bytes, int32_t* d_info, void* stream);

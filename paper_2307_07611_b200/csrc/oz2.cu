@@ -45,7 +45,8 @@ constexpr int OZ2_TM = 128, OZ2_TN = 256, OZ2_TK = 128, OZ2_STAGES = 4, OZ2_GROU
 constexpr int OZ2_A_BYTES = OZ2_TM * OZ2_TK, OZ2_B_BYTES = OZ2_TN * OZ2_TK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
 constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + 1024 + 256;
 constexpr int OZ2_THREADS = 192;
-constexpr int OZ2_CMAX_ROWS = 128;  // rows per block of the column-maximum kernel
+constexpr int OZ2_CMAX_ROWS = 128;
+  // rows per block of the column-maximum kernel
 
 // pairwise coprime, <= 256 (symmetric residues fit int8)
 __host__ __device__ constexpr int oz2_mod(int i) {
@@ -160,7 +161,7 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
 // 32 (k) x 32 (j) tile of scaled integers; thread t converts k0 + 4 (t % 8) .. +3 of
 // column j0 + t / 8 and stores one 32-bit word per modulus plane.  Tiles outside the
 // GEMM's K range (a 32-column tile lies in one OZ2_TN column tile) are skipped.
-__global__ void __launch_bounds__(256) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
+__global__ void __launch_bounds__(256, 8) oz2_split_cols_kernel(const double* B, int64_t ldb, int K, int cols, int tri,
                                                              bool strict, int P, const unsigned long long* maxbits,
                                                              int* expo, int8_t* out) {
   __shared__ long long tile[32][33];

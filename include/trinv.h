@@ -224,7 +224,7 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
  * with `digits` digits, 2 (default) = its modular (CRT) variant; engines 1 and 2 take
  * every product whose blocks are >= min_block (>= 256; default 4096) and whose shapes
  * fit their envelope, all other products stay on DMMA.  Scaling guard: when the input's
- * row- or column-maximum exponents (every 16th row sampled) span more than 20 binades,
+ * row- or column-maximum exponents (every 17th row sampled) span more than 20 binades,
  * the call runs every product on DMMA (the INT8 engines' truncation is relative to row /
  * column maxima); the check costs one 16-byte device-to-host read per
  * call, resolved by an event when the first INT8 product is reached, and is skipped
@@ -233,6 +233,14 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
  * it changes trinv_workspace_bytes ('L', 'U', 'G', 'A', 'F'): query the workspace after. */
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
 int trinv_get_product_engine(void);
+
+/* The scaling guard of the INT8 engines on its own (for callers composing products
+ * themselves, e.g. the multi-rank split): 1 when the row- and column-maximum exponents
+ * of the n x n matrix A (device, ld lda; uplo 'L' / 'U' = only that triangle is read,
+ * 'N' = all of it; every 17th row sampled) span at most 20 binades, or when `stream` is
+ * capturing (check skipped); 0 otherwise; -TRINV_INVALID_ARG / -TRINV_CUDA_ERROR on
+ * error.  Waits for the check on `stream` (one 16-byte device-to-host read). */
+int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, void* stream);
 
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);

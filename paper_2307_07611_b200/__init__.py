@@ -19,7 +19,8 @@ from ._lib import (TRINV_OK, TRINV_UNIT, TRINV_NON_UNIT, TrinvError, SingularMat
                    lib, so_path, status_string, launch_count, reset_launch_count)
 
 __all__ = ["trinv_lower", "trinv_upper", "trinv_batched", "trinv_batched_host", "inv_from_lu", "inv_general",
-           "lu_crout", "gemm", "gemm_oz", "gemm_strassen", "set_product_engine", "product_engine", "trinv_beta", "workspace_bytes",
+           "lu_crout", "gemm", "gemm_oz", "gemm_strassen", "set_product_engine", "product_engine", "product_min_block",
+           "int8_scaling_ok", "trinv_beta", "workspace_bytes",
            "TrinvError", "SingularMatrixError", "lib", "so_path", "launch_count", "reset_launch_count"]
 
 
@@ -215,12 +216,31 @@ def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", di
     return C
 
 
+_MIN_BLOCK = 4096  # the engines' block threshold as last set through set_product_engine
+
+
 def set_product_engine(engine="int8crt", digits=8, min_block=4096):
     """Engine of the level products: "int8crt" (default: INT8 tensor cores, 16 moduli + CRT,
     for the levels with block size >= min_block), "int8" (INT8 tensor cores, exact splitting
     into `digits` 7-bit digits) or "dmma" (FP64 mma.sync for every level)."""
+    global _MIN_BLOCK
     e = {"dmma": 0, "int8": 1, "int8crt": 2}[engine]
     _check(lib().trinv_set_product_engine(e, digits, min_block))
+    _MIN_BLOCK = int(min_block)
+
+
+def product_min_block():
+    return _MIN_BLOCK
+
+
+def int8_scaling_ok(A, uplo="N", stream=None):
+    """The INT8 engines' scaling guard (trinv_int8_scaling_ok): True when A's row / column
+    maxima span at most 20 binades (only the `uplo` triangle read for "L" / "U")."""
+    n = A.shape[-1]
+    r = lib().trinv_int8_scaling_ok(n, ctypes.c_void_p(A.data_ptr()), _ld(A), uplo.encode(), _stream(stream))
+    if r < 0:
+        _check(-r)
+    return r == 1
 
 
 def product_engine():

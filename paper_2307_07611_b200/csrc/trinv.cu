@@ -131,11 +131,11 @@ static int product_engine() {
 // rows or columns span many binades lose accuracy there (1.2e-10 at a
 // 2^+-16 row / column scaling, 9e-4 beyond 2^+-30) while the DMMA path is exactly scaling
 // invariant.  Before a call that would use them, the spread of the row-maximum exponents
-// and of the column-maximum exponents of the input is estimated on every 16th row; above
+// and of the column-maximum exponents of the input is estimated on every 17th row; above
 // OZ_MAX_SPREAD binades the call runs every product on DMMA.  Skipped under stream
 // capture (it needs one 16-byte device-to-host read).
 constexpr int OZ_MAX_SPREAD = 20;
-constexpr int SPREAD_STRIDE = 16;   // rows sampled
+constexpr int SPREAD_STRIDE = 17;   // rows sampled (odd: periodic row scalings with even period are seen)
 constexpr int SPREAD_GROUPS = 8;    // row groups of the column pass
 // Per call: the check kernels run first on the call's stream and copy their 4 exponents
 // per checked matrix to pinned host memory behind an event; the decision is taken (event
@@ -202,11 +202,13 @@ __global__ void spread_rows_kernel(const double* A, int64_t lda, int n, char upl
     }
   }
 }
-// column maxima over the sampled rows: thread per column, SPREAD_GROUPS row groups
+// column maxima over the sampled rows and the column's diagonal entry (a triangular
+// column near the triangle's edge has few sampled rows; its diagonal, non-zero for an
+// invertible factor, anchors the estimate): thread per column, SPREAD_GROUPS row groups
 __global__ void spread_cols_kernel(const double* A, int64_t lda, int n, char uplo, unsigned long long* cmax) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  double m = 0.0;
+  double m = blockIdx.y == 0 ? fabs(A[(int64_t)j * lda + j]) : 0.0;
 #pragma unroll 4
   for (int i = blockIdx.y * SPREAD_STRIDE; i < n; i += SPREAD_GROUPS * SPREAD_STRIDE)
     if ((uplo == 'L' && j <= i) || (uplo == 'U' && j >= i) || uplo == 'N') m = fmax(m, fabs(A[(int64_t)i * lda + j]));
@@ -1126,6 +1128,17 @@ trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_bloc
 }
 
 int trinv_get_product_engine(void) { return product_engine(); }
+
+int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, void* stream) {
+  if (n <= 0 || !A || lda < n || (uplo != 'L' && uplo != 'U' && uplo != 'N')) return -(int)TRINV_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  Int8Scope scope(true);
+  int8_check_begin(A, lda, n, uplo, s);
+  const bool veto = int8_veto();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_last_cuda_error = (int)e; return -(int)TRINV_CUDA_ERROR; }
+  return veto ? 0 : 1;
+}
 
 const char* trinv_status_string(trinv_status_t st) {
   switch (st) {

@@ -104,6 +104,26 @@ def panel_owner_map(world):
     return {r: (r, 2 * world - 1 - r) for r in range(world)}
 
 
+def _int8_panels(T, uplo):
+    """Whether the panel products may use the INT8 CRT engine: the library's default
+    engine is in use and the input passes its scaling guard (same decision on every rank:
+    every rank holds T)."""
+    from . import int8_scaling_ok, product_engine
+    return product_engine() == "int8crt" and int8_scaling_ok(T, uplo)
+
+
+def _panel_gemm(A, B, *, C=None, alpha=1.0, struct_a="N", struct_b="N", int8=False):
+    """C = alpha A B through the INT8 CRT engine when allowed and the shape fits its
+    envelope (M % 128, N % 256, K % 128, every dimension >= the engine's block threshold),
+    else through the DMMA engine."""
+    from . import gemm, gemm_oz, product_min_block
+    M, K = A.shape
+    N = B.shape[1]
+    if int8 and M % 128 == 0 and N % 256 == 0 and K % 128 == 0 and min(M, N, K) >= product_min_block():
+        return gemm_oz(A, B, C=C, alpha=alpha, struct_a=struct_a, struct_b=struct_b, digits=0)
+    return gemm(A, B, C=C, alpha=alpha, struct_a=struct_a, struct_b=struct_b)
+
+
 def trinv_split(T, uplo="L", group=None, dst=0, inv=None, gemm=None):
     """Invert one n x n triangular matrix across the ranks of `group` (see above).
 
@@ -112,14 +132,16 @@ def trinv_split(T, uplo="L", group=None, dst=0, inv=None, gemm=None):
     struct_a, struct_b)` default to this package's kernels; tests may pass CPU
     stand-ins to exercise the partition and communication logic without a GPU.
     """
-    from . import gemm as _gemm, trinv_lower, trinv_upper
+    from . import trinv_lower, trinv_upper
     if inv is None:
         def inv(M, u):
             M = M.contiguous()
             return trinv_lower(M) if u == "L" else trinv_upper(M)
     if gemm is None:
+        int8 = T.is_cuda and _int8_panels(T, uplo)
+
         def gemm(A, B, alpha, sa, sb):
-            return _gemm(A, B, alpha=alpha, struct_a=sa, struct_b=sb)
+            return _panel_gemm(A, B, alpha=alpha, struct_a=sa, struct_b=sb, int8=int8)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     n = T.shape[0]
@@ -199,7 +221,7 @@ def _share_from(t, src, group):
 
 def trinv_split_p2p(T, uplo="L", group=None, dst=0):
     """trinv_split with the data exchange done by the kernels over peer memory (see above)."""
-    from . import gemm as _gemm, trinv_lower, trinv_upper
+    from . import trinv_lower, trinv_upper
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     n = T.shape[0]
@@ -219,6 +241,10 @@ def trinv_split_p2p(T, uplo="L", group=None, dst=0):
     torch.cuda.synchronize()
     dist.barrier(group=group)
     # phase 3: 2G balanced panels; operands read from X on dst, results stored there
+    int8 = _int8_panels(T, uplo)
+
+    def _gemm(A, B, C=None, alpha=1.0, struct_a="N", struct_b="N"):
+        return _panel_gemm(A, B, C=C, alpha=alpha, struct_a=struct_a, struct_b=struct_b, int8=int8)
     P = 2 * world
     w = (h + P - 1) // P
     w += w % 2

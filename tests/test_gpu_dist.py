@@ -74,3 +74,52 @@ def test_split_single_process():
     T = torch.from_numpy(synth.host(n, seed=8)).cuda()
     X = trinv_split(T, "L").cpu().numpy()
     assert oracle.floored_rel_err(X, oracle.crit_lower(T.cpu().numpy())) <= 1e-10
+
+
+def _worker_large(rank, world, port, n, uplo, q, transport):
+    """As _worker at a size whose panel products take the INT8 CRT engine; 64 sampled
+    columns against the oracle."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        from gpu_common import REL_TOL, RES_TOL, sample_columns
+        from paper_2307_07611_b200.dist import trinv_split, trinv_split_p2p
+        T = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
+        synth.device_fill(T, n, seed=6, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+        X = trinv_split(T, uplo) if transport == "nccl" else trinv_split_p2p(T, uplo)
+        torch.cuda.synchronize()
+        if rank == 0:
+            cols = sample_columns(n, 2)
+            Xs = X[:, torch.from_numpy(cols).to("cuda:0")].T.contiguous().cpu().numpy()
+            Th = T.cpu().numpy()
+            R = oracle.columns(Th, uplo, cols)
+            Tt = np.tril(Th) if uplo == "L" else np.triu(Th)
+            ok = (oracle.floored_rel_err(Xs, R, axis_cols=0) <= REL_TOL and
+                  oracle.column_residual_ratio(Tt, Xs, cols) <= RES_TOL)
+            q.put(bool(ok))
+        else:
+            q.put(X is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_split_int8_panels(uplo, transport):
+    """n = 16384 over two ranks: the 4096-wide panel products run on the INT8 CRT engine
+    (the library default; the input passes the scaling guard)."""
+    world, n = 2, 16384
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_large, args=(r, world, port, n, uplo, q, transport)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    results = [q.get(timeout=5) for _ in range(world)]
+    assert all(results), results
+    assert all(p.exitcode == 0 for p in procs)

@@ -105,3 +105,30 @@ def test_scaling_guard_keeps_int8_on_well_scaled_input():
         P.set_product_engine()
     assert not np.array_equal(X8, Xd)
     assert np.max(np.abs(X8 - Xd)) <= 1e-12 * np.max(np.abs(Xd))
+
+
+def test_scaling_guard_sees_alternating_rows():
+    """Rows scaled by 2^40 in alternation (a period-2 pattern) are seen by the sampled
+    check (odd sampling stride)."""
+    n = 4096
+    T = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    synth.device_fill(T, n, diag="signed")
+    assert P.int8_scaling_ok(T, "L")
+    T[::2] *= 2.0 ** 40
+    assert not P.int8_scaling_ok(T, "L")
+    U = torch.triu(torch.ones((n, n), dtype=torch.float64, device=DEV))
+    U[:, ::3] *= 2.0 ** -30  # column scaling
+    assert not P.int8_scaling_ok(U, "U")
+
+
+@pytest.mark.parametrize("n,uplo,seed", [(8192, "L", 0), (16384, "L", 3), (16384, "U", 7), (32768, "U", 0)])
+def test_scaling_guard_no_veto_on_baseline_inputs(n, uplo, seed):
+    """BASELINE distributions (diagonal in [1,2], off-diagonal ~1/n) and their diagonal
+    blocks pass the guard: the column estimate is anchored by the diagonal, so columns at
+    the triangle's edge with few sampled rows of ~1/n entries do not fake a spread."""
+    T = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    synth.device_fill(T, n, seed=seed, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    assert P.int8_scaling_ok(T, uplo)
+    h = n // 2
+    assert P.int8_scaling_ok(T[:h, :h].contiguous(), uplo)
+    assert P.int8_scaling_ok(T[h:, h:].contiguous(), uplo)

@@ -86,7 +86,9 @@ def _worker_large(rank, world, port, n, uplo, q, transport):
         import oracle
         import synth
         from gpu_common import REL_TOL, RES_TOL, sample_columns
+        import paper_2307_07611_b200 as P
         from paper_2307_07611_b200.dist import trinv_split, trinv_split_p2p
+        P.set_product_engine("int8crt", min_block=2048)  # the 2048-wide panels of n = 16384 over 2 ranks
         T = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
         synth.device_fill(T, n, seed=6, uplo=uplo, diag="signed" if uplo == "L" else "pos")
         X = trinv_split(T, uplo) if transport == "nccl" else trinv_split_p2p(T, uplo)
@@ -109,8 +111,8 @@ def _worker_large(rank, world, port, n, uplo, q, transport):
 @pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_split_int8_panels(uplo, transport):
-    """n = 16384 over two ranks: the 4096-wide panel products run on the INT8 CRT engine
-    (the library default; the input passes the scaling guard)."""
+    """n = 16384 over two ranks: the 2048-wide panel products run on the INT8 CRT engine
+    (block threshold lowered to 2048 in the workers; the input passes the scaling guard)."""
     world, n = 2, 16384
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -123,3 +125,21 @@ def test_split_int8_panels(uplo, transport):
     results = [q.get(timeout=5) for _ in range(world)]
     assert all(results), results
     assert all(p.exitcode == 0 for p in procs)
+
+
+def test_split_int8_panels_single_process():
+    """One process (no process group), n = 16384: two 8192-wide panels on the INT8 engine
+    at the default threshold."""
+    import oracle
+    import synth
+    from gpu_common import REL_TOL, RES_TOL, sample_columns
+    from paper_2307_07611_b200.dist import trinv_split
+    n = 16384
+    T = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
+    synth.device_fill(T, n, seed=8, diag="signed")
+    X = trinv_split(T, "L")
+    cols = sample_columns(n, 2)
+    Xs = X[:, torch.from_numpy(cols).to("cuda:0")].T.contiguous().cpu().numpy()
+    Th = T.cpu().numpy()
+    assert oracle.floored_rel_err(Xs, oracle.columns(Th, "L", cols), axis_cols=0) <= REL_TOL
+    assert oracle.column_residual_ratio(np.tril(Th), Xs, cols) <= RES_TOL

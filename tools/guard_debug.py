@@ -1,3 +1,5 @@
+"""Scaling-guard check on a BASELINE-style input and its diagonal halves, with the true row /
+column maxima for comparison (python tools/guard_debug.py)."""
 import sys, torch
 sys.path.insert(0, ".")
 import synth, paper_2307_07611_b200 as P

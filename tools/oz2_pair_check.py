@@ -1,3 +1,5 @@
+"""Normwise error of gemm_oz(digits=0) on shapes the CTA-pair kernel takes (run with
+TRINV_OZ2_PAIR=256 to route them through it)."""
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_2307_07611_b200 as P

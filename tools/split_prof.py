@@ -1,3 +1,4 @@
+"""Kernel breakdown and gaps of one dist.trinv_split call on one process (n = 32768)."""
 import sys, torch
 sys.path.insert(0, ".")
 import synth, paper_2307_07611_b200 as P

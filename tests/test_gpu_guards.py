@@ -95,3 +95,39 @@ def test_gemm_writes_stay_inside(M, N, K):
     torch.cuda.synchronize()
     assert np.max(np.abs(C.cpu().numpy() - Ga @ Gb)) <= 1e-12 * K
     _assert_guards(buf, _inside_mask(M, N, ld, buf.numel()))
+
+
+@pytest.mark.parametrize("engine", ["int8crt", "int8"])
+@pytest.mark.parametrize("n,uplo", [(1024, "L"), (1536, "U"), (2048, "L")])
+def test_int8_engine_writes_stay_inside(engine, n, uplo):
+    """The INT8 engines' kernels (residue splits into the workspace, the tensor-core GEMM,
+    the reconstruction into X) inside the recursion, with the block threshold lowered so
+    they carry the 512 / 1024 levels: X in a padded, guarded buffer."""
+    P.set_product_engine(engine, min_block=256)
+    try:
+        T = synth.host(n, seed=n + 1, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+        ld = n + 8
+        buf, X = _guarded(n, n, ld)
+        f = P.trinv_lower if uplo == "L" else P.trinv_upper
+        f(torch.from_numpy(T).to(DEV), out=X)
+        torch.cuda.synchronize()
+        assert oracle.floored_rel_err(X.cpu().numpy(), oracle.trinv(T, uplo)) <= REL_TOL
+        _assert_guards(buf, _inside_mask(n, n, ld, buf.numel()))
+    finally:
+        P.set_product_engine()
+
+
+@pytest.mark.parametrize("M,N,K,sa,sb", [(512, 768, 384, "N", "N"), (1024, 512, 1024, "L", "N"),
+                                         (768, 1024, 1024, "N", "U")])
+def test_gemm_oz_writes_stay_inside(M, N, K, sa, sb):
+    rng = np.random.default_rng(M + N)
+    Ga, Gb = rng.uniform(-1, 1, (M, K)), rng.uniform(-1, 1, (K, N))
+    if sa == "L": Ga = np.tril(Ga)
+    if sb == "U": Gb = np.triu(Gb)
+    ld = N + 4
+    buf, C = _guarded(M, N, ld)
+    P.gemm_oz(torch.from_numpy(Ga).to(DEV), torch.from_numpy(Gb).to(DEV), C=C, struct_a=sa, struct_b=sb, digits=0)
+    torch.cuda.synchronize()
+    sc = np.abs(Ga).max(1, keepdims=True) * np.abs(Gb).max(0, keepdims=True) * K
+    assert np.max(np.abs(C.cpu().numpy() - Ga @ Gb) / sc) <= 1e-15
+    _assert_guards(buf, _inside_mask(M, N, ld, buf.numel()))

@@ -132,16 +132,37 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
   const double* a = A + (int64_t)warp * lda;
   double m = 0.0;
   const int kz = strict ? warp : -1;  // a diagonal read as zero
-  for (int k = kb + lane; k < ke; k += 32) m = k == kz ? m : fmax(m, fabs(a[k]));
+  const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0;  // kb is a multiple of 128
+  if (vec) {
+    double m1 = 0.0;
+#pragma unroll 4
+    for (int k = kb + 2 * lane; k < ke; k += 64) {
+      const double2 x = *reinterpret_cast<const double2*>(a + k);
+      m = k == kz ? m : fmax(m, fabs(x.x));
+      m1 = k + 1 == kz ? m1 : fmax(m1, fabs(x.y));
+    }
+    m = fmax(m, m1);
+  } else {
+#pragma unroll 4
+    for (int k = kb + lane; k < ke; k += 32) m = k == kz ? m : fmax(m, fabs(a[k]));
+  }
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = oz2_exp_above(m);
   if (lane == 0) expo[warp] = e;
   const size_t sw = (size_t)rows * K / 4;  // plane stride in 32-bit words
   uint32_t* o = reinterpret_cast<uint32_t*>(out) + (size_t)warp * K / 4;
   for (int k = kb + 4 * lane; k < ke; k += 128) {
+    double x[4];
+    if (vec) {
+      const double2 x01 = *reinterpret_cast<const double2*>(a + k), x23 = *reinterpret_cast<const double2*>(a + k + 2);
+      x[0] = x01.x; x[1] = x01.y; x[2] = x23.x; x[3] = x23.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = a[k + q];
+    }
     int64_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = k + q == kz ? 0 : (int64_t)oz2_ldexp(a[k + q], P - e);  // exact, truncated
+    for (int q = 0; q < 4; ++q) v[q] = k + q == kz ? 0 : (int64_t)oz2_ldexp(x[q], P - e);  // exact, truncated
     oz2_residues4(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }

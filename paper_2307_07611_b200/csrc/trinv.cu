@@ -307,18 +307,57 @@ static bool oz_level_ok(int64_t n, int64_t b) {
   }
   return true;
 }
+// A second stream per device for the independent product pairs of lu_inv_rec (U12 / L21,
+// the K21 / S12 chains, the two leaf inversions): forked from and joined back to the
+// caller's stream by events, so ordering with the caller's work is unchanged and the pair
+// is captured as two graph branches under stream capture.
+struct ForkCtx {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static cudaError_t fork_ctx(ForkCtx** out) {
+  static thread_local ForkCtx ctx[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  ForkCtx& c = ctx[dev];
+  if (!c.aux) {
+    if ((e = cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  *out = &c;
+  return cudaSuccess;
+}
+static cudaError_t fork_to(ForkCtx* c, cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(c->fork, s);
+  return e != cudaSuccess ? e : cudaStreamWaitEvent(c->aux, c->fork, 0);
+}
+static cudaError_t join_from(ForkCtx* c, cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(c->join, c->aux);
+  return e != cudaSuccess ? e : cudaStreamWaitEvent(s, c->join, 0);
+}
+
+// Scratch of one INT8 product of level b (the largest of its merges' products).
+static size_t oz_level_scratch(int64_t n, int64_t b) {
+  size_t best = 0;
+  for (int64_t s = 0; s + b < n; s += 2 * b) {
+    const int64_t r = std::min(b, n - s - b);
+    for (size_t v : {oz_shape_ws(r, b, b), oz_shape_ws(r, b, r), oz_shape_ws(b, r, b), oz_shape_ws(b, r, r)})
+      best = std::max(best, v);
+  }
+  return align_up(best);
+}
+// Levels with two or more merges run their merges alternately on two streams, each with
+// its own product scratch (run_tri): the residue / reconstruction kernels of one merge
+// overlap the tensor-core GEMM of the other.
 static size_t oz_scratch(int64_t n) {
   if (product_engine() == 0 || n <= BLK_MAX) return 0;
   size_t best = 0;
-  for (int64_t b = BLK_MAX; b < n; b *= 2) {
-    if (!oz_level_ok(n, b)) continue;
-    for (int64_t s = 0; s + b < n; s += 2 * b) {
-      const int64_t r = std::min(b, n - s - b);
-      for (size_t v : {oz_shape_ws(r, b, b), oz_shape_ws(r, b, r), oz_shape_ws(b, r, b), oz_shape_ws(b, r, r)})
-        best = std::max(best, v);
-    }
-  }
-  return align_up(best);
+  for (int64_t b = BLK_MAX; b < n; b *= 2)
+    if (oz_level_ok(n, b)) best = std::max(best, (merges_at(n, b) > 1 ? 2 : 1) * oz_level_scratch(n, b));
+  return best;
 }
 
 // whether a triangular inverse of order n runs any level product on an INT8 engine
@@ -419,8 +458,18 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
     }
     if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
-      void* ozws = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
+      void* ozws0 = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
+      const bool two = merges > 1;
+      ForkCtx* fc = nullptr;
+      if (two) {
+        TRY(fork_ctx(&fc));
+        TRY(fork_to(fc, s));
+      }
+      const cudaStream_t s_main = s;
       for (int64_t g = 0; g < merges; ++g) {
+        const bool odd = two && (g & 1);
+        const cudaStream_t s = odd ? fc->aux : s_main;  // merges alternate between the two streams
+        void* ozws = reinterpret_cast<char*>(ozws0) + (odd ? oz_level_scratch(n, b) : 0);
         const int64_t s0 = 2 * g * b, r = std::min(b, n - s0 - b);
         double* Wg = W + g * b * b;
         const double* Ai = X + s0 * ldx + s0;                // A^{-1}
@@ -435,6 +484,7 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
           TRY(launch_zero_2d(X + (s0 + b) * ldx + s0, ldx, r, b, s, &g_launches));
         }
       }
+      if (two) TRY(join_from(fc, s_main));
       continue;
     }
     TRY(launch_level(l1, s, &g_launches));
@@ -653,37 +703,6 @@ static size_t lu_inv_half_scratch(int64_t n) {
 }
 static size_t lu_inv_scratch(int64_t n) { return 2 * lu_inv_half_scratch(n); }
 
-// A second stream per device for the independent product pairs of lu_inv_rec (U12 / L21,
-// the K21 / S12 chains, the two leaf inversions): forked from and joined back to the
-// caller's stream by events, so ordering with the caller's work is unchanged and the pair
-// is captured as two graph branches under stream capture.
-struct ForkCtx {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static cudaError_t fork_ctx(ForkCtx** out) {
-  static thread_local ForkCtx ctx[64];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  ForkCtx& c = ctx[dev];
-  if (!c.aux) {
-    if ((e = cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess) return e;
-  }
-  *out = &c;
-  return cudaSuccess;
-}
-static cudaError_t fork_to(ForkCtx* c, cudaStream_t s) {
-  cudaError_t e = cudaEventRecord(c->fork, s);
-  return e != cudaSuccess ? e : cudaStreamWaitEvent(c->aux, c->fork, 0);
-}
-static cudaError_t join_from(ForkCtx* c, cudaStream_t s) {
-  cudaError_t e = cudaEventRecord(c->join, c->aux);
-  return e != cudaSuccess ? e : cudaStreamWaitEvent(s, c->join, 0);
-}
 // INT8 CRT scratch for the products of lu_inv_rec that run on the modular engine (all of
 // them with min(M, N, K) >= the engine's block threshold): the largest over the recursion.
 static bool lu_gemm_on_int8(int64_t M, int64_t N, int64_t K) {

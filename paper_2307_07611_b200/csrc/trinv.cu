@@ -717,8 +717,9 @@ static size_t lu_oz_ws(int64_t n) {
     if (lu_gemm_on_int8(m[0], m[1], m[2])) best = std::max(best, align_up(oz2_workspace_bytes(m[0], m[1], m[2])));
   return best;
 }
+// ozws: two CRT scratches of ozhalf bytes each, one per stream (nullptr: DMMA only)
 static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
-                                 int32_t* info, int64_t info_off, cudaStream_t s, void* ozws) {
+                                 int32_t* info, int64_t info_off, cudaStream_t s, void* ozws, size_t ozhalf) {
   ForkCtx* fc = nullptr;
   TRY(fork_ctx(&fc));
   if (n <= LU_MAX) {
@@ -737,21 +738,22 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   auto blk = [&](double* M, int64_t i, int64_t j) { return M + i * ld + j; };
   auto gemm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                   int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
-    if (ozws && lu_gemm_on_int8(M, N, K) && !int8_veto())
-      return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, ozws, st,
+    if (ozws && lu_gemm_on_int8(M, N, K) && !int8_veto()) {  // one CRT scratch per stream
+      void* w = st == fc->aux ? static_cast<void*>(static_cast<char*>(ozws) + ozhalf) : ozws;
+      return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, w, st,
                                        &g_launches));
+    }
     GemmArgs g{};
     g.M = M; g.N = N; g.K = K; g.batch = 1;
     g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
     g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
     return cuda_fail(launch_gemm(g, st, &g_launches));
   };
-  // the two products of a pair run concurrently unless one uses the (single) INT8 scratch
+  // the two products of a pair run concurrently (each stream has its own CRT scratch)
   static const bool fork_on = [] { const char* e = std::getenv("TRINV_LU_FORK"); return !(e && e[0] == '0'); }();
-  const bool par = fork_on && !(ozws && (lu_gemm_on_int8(h, r, h) || lu_gemm_on_int8(r, h, r) ||
-                                         lu_gemm_on_int8(h, r, r)));
+  const bool par = fork_on;
   cudaStream_t s2 = par ? fc->aux : s;
-  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws);  // A11 = L11 U11, K11, S11
+  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws, ozhalf);  // A11 = L11 U11, K11, S11
   if (st != TRINV_OK) return st;
   // U12 = K11 A12 (K11 lower) || L21 = A21 S11 (S11 upper); Schur W22 <- A22 - L21 U12
   if (par) TRY(fork_to(fc, s));
@@ -760,7 +762,8 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   if (par) TRY(join_from(fc, s));
   if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0, s)))
     return st;
-  st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s, ozws);
+  st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s, ozws,
+                  ozhalf);
   if (st != TRINV_OK) return st;
   const int64_t lth = even_up(h), ltr = even_up(r);
   if (par) TRY(fork_to(fc, s));
@@ -837,7 +840,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
   if (op == 'A') {  // inv_general: F, W, K, S (n x even(n) each), the product scratch, X staging, INT8 scratch
     size_t bytes = 4 * align_up(mat_bytes(n)) + align_up(lu_inv_scratch(n));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
-    bytes += std::max(lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
+    bytes += std::max(2 * lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
     (void)A; (void)lda;
     return bytes;
   }
@@ -1088,12 +1091,12 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const bool stage_x = !tma_ok(X, ldx);
   double* Xuse = stage_x ? take(mat_bytes(n)) : X;
   const int64_t ldx_use = stage_x ? lde : ldx;
-  const size_t oz_bytes = std::max(lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
+  const size_t oz_bytes = std::max(2 * lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
   void* ozws = oz_bytes ? static_cast<void*>(take(oz_bytes)) : nullptr;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   TRY(launch_copy_2d(A, lda, Wk, lde, n, n, s, &g_launches));
   // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
-  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, ozws);
+  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, lu_oz_ws(n) ? ozws : nullptr, lu_oz_ws(n));
   if (st != TRINV_OK) return st;
   // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
   if (ul_on_int8(n) && !int8_veto()) {

@@ -123,9 +123,14 @@ cudaError_t launch_oz_gemm(int64_t M, int64_t N, int64_t K, const double* A, int
 bool oz2_supported(int64_t M, int64_t N, int64_t K);
 size_t oz2_workspace_bytes(int64_t M, int64_t N, int64_t K);
 // strict: bit 0 / bit 1 = the diagonal (k == i of A, k == j of B) is read as zero.
+// skip: bit 0 / bit 1 = A / B already split into ws by launch_oz2_prepare.
 cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                             int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
-                            cudaStream_t st, int64_t* launches, int strict = 0);
+                            cudaStream_t st, int64_t* launches, int strict = 0, int skip = 0);
+// The operand splits of launch_oz2_gemm alone (which: 1 = A, 2 = B), same workspace layout.
+cudaError_t launch_oz2_prepare(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA,
+                               const double* B, int64_t ldb, int triB, void* ws, cudaStream_t st, int which,
+                               int64_t* launches, int strict = 0);
 // X = S K (S upper, K lower, order n) on the modular engine with the diagonals split off:
 // X = D_S D_K + D_S N_K + N_S D_K (one elementwise pass, exact up to one rounding) plus the
 // product of the strictly triangular parts N_S N_K (row / column scales set by the

@@ -706,9 +706,55 @@ static bool oz2_encode(CUtensorMap* m, const void* base, uint64_t cols, uint64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// CTA-pair GEMM (cta_group::2) for products with M % 256 == 0 and all dimensions >=
+// pair_min (TRINV_OZ2_PAIR = 0 disables, = <n> sets pair_min; default 8192: the pair
+// kernel won at the 8192 and 16384 levels, not at 4096, profiles/r01_oz2_pair.txt)
+static bool oz2_use_pair(int64_t M, int64_t N, int64_t K) {
+  static const int64_t pair_min = [] {
+    const char* e = std::getenv("TRINV_OZ2_PAIR");
+    if (!e) return (int64_t)8192;
+    const long long v = std::atoll(e);
+    return v <= 0 ? (int64_t)1 << 62 : (int64_t)v;
+  }();
+  return M % 256 == 0 && std::min(M, std::min(N, K)) >= pair_min;
+}
+
+// Operand splits on their own (which: 1 = A, 2 = B), into the same workspace layout as
+// launch_oz2_gemm, which then skips them (skip = which): lets a caller split an operand
+// on another stream while an earlier product runs.
+cudaError_t launch_oz2_prepare(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA,
+                               const double* B, int64_t ldb, int triB, void* ws, cudaStream_t st, int which,
+                               int64_t* launches, int strict) {
+  if (!oz2_supported(M, N, K)) return cudaErrorInvalidValue;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* w = static_cast<char*>(ws);
+  int8_t* As = reinterpret_cast<int8_t*>(w); w += al((size_t)OZ2_NMOD * M * K);
+  int8_t* Bs = reinterpret_cast<int8_t*>(w); w += al((size_t)OZ2_NMOD * N * K);
+  w += al((size_t)OZ2_NMOD * M * N);
+  int* ea = reinterpret_cast<int*>(w); w += al((size_t)M * 4);
+  int* eb = reinterpret_cast<int*>(w); w += al((size_t)N * 4);
+  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(w);
+  const int P = oz2_scale_bits(K);
+  if (which & 1) {
+    oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(
+        A, lda, (int)M, (int)K, triA, (strict & 1) != 0, P, oz2_use_pair(M, N, K) ? 256 : OZ2_TM, As, ea);
+    if (launches) ++*launches;
+  }
+  if (which & 2) {
+    cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
+    if (e != cudaSuccess) return e;
+    oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + OZ2_CMAX_ROWS - 1) / OZ2_CMAX_ROWS)), 256, 0,
+                        st>>>(B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, maxbits);
+    oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
+        B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, P, maxbits, eb, Bs);
+    if (launches) *launches += 2;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                             int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, void* ws,
-                            cudaStream_t st, int64_t* launches, int strict) {
+                            cudaStream_t st, int64_t* launches, int strict, int skip) {
   if (!oz2_supported(M, N, K)) return cudaErrorInvalidValue;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* w = static_cast<char*>(ws);
@@ -740,28 +786,13 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   };
   const double ea_n = range_sum(M, OZ2_TM, triA == TRI_LOWER, triA == TRI_UPPER);
   const double eb_n = range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER);
-  // CTA-pair GEMM (cta_group::2) for products with M % 256 == 0 and all dimensions >=
-  // pair_min (TRINV_OZ2_PAIR = 0 disables, = <n> sets pair_min; default 8192: the pair
-  // kernel won at the 8192 and 16384 levels, not at 4096, profiles/r01_oz2_pair.txt)
-  static const int64_t pair_min = [] {
-    const char* e = std::getenv("TRINV_OZ2_PAIR");
-    if (!e) return (int64_t)8192;
-    const long long v = std::atoll(e);
-    return v <= 0 ? (int64_t)1 << 62 : (int64_t)v;
-  }();
-  const bool pair = M % 256 == 0 && std::min(M, std::min(N, K)) >= pair_min;
-  {
-    ProfileScope aux(KIND_OZAUX, 0.0, 24.0 * ea_n + 32.0 * eb_n, st);
-    oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(A, lda, (int)M, (int)K, triA, (strict & 1) != 0,
-                                                                               P, pair ? 256 : OZ2_TM, As, ea);
-    cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
+  const bool pair = oz2_use_pair(M, N, K);
+  if ((skip & 3) != 3) {
+    ProfileScope aux(KIND_OZAUX, 0.0, ((skip & 1) ? 0.0 : 24.0 * ea_n) + ((skip & 2) ? 0.0 : 32.0 * eb_n), st);
+    const cudaError_t e = launch_oz2_prepare(M, N, K, A, lda, triA, B, ldb, triB, ws, st, 3 & ~skip, nullptr, strict);
     if (e != cudaSuccess) return e;
-    oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + OZ2_CMAX_ROWS - 1) / OZ2_CMAX_ROWS)), 256, 0,
-                        st>>>(
-        B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, maxbits);
-    oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
-        B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, P, maxbits, eb, Bs);
   }
+  (void)maxbits;
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||
       !oz2_encode(&mb, Bs, (uint64_t)K, (uint64_t)OZ2_NMOD * N, pair ? 128 : OZ2_TN))
@@ -793,7 +824,7 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
     oz2_reconstruct_kernel<<<(unsigned)((total4 + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha,
                                                                             beta, C, ldc, crt);
   }
-  if (launches) *launches += 5;
+  if (launches) *launches += 2 + ((skip & 1) ? 0 : 1) + ((skip & 2) ? 0 : 2);
   return cudaGetLastError();
 }
 

@@ -352,11 +352,14 @@ static size_t oz_level_scratch(int64_t n, int64_t b) {
 // Levels with two or more merges run their merges alternately on two streams, each with
 // its own product scratch (run_tri): the residue / reconstruction kernels of one merge
 // overlap the tensor-core GEMM of the other.
+// With the CRT engine a single-merge level (the top level) splits its second product's
+// inverse-block operand on the second stream while the first product runs: two scratches.
 static size_t oz_scratch(int64_t n) {
   if (product_engine() == 0 || n <= BLK_MAX) return 0;
   size_t best = 0;
   for (int64_t b = BLK_MAX; b < n; b *= 2)
-    if (oz_level_ok(n, b)) best = std::max(best, (merges_at(n, b) > 1 ? 2 : 1) * oz_level_scratch(n, b));
+    if (oz_level_ok(n, b))
+      best = std::max(best, (merges_at(n, b) > 1 || product_engine() == 2 ? 2 : 1) * oz_level_scratch(n, b));
   return best;
 }
 
@@ -464,6 +467,37 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       if (two) {
         TRY(fork_ctx(&fc));
         TRY(fork_to(fc, s));
+      }
+      if (!two && product_engine() == 2) {
+        // one merge: the second product's inverse-block operand (B^-1 rows for the lower
+        // case, C^-1 columns for the upper) is split on the second stream during the first
+        // product; the second product then runs in the second scratch with that split done
+        TRY(fork_ctx(&fc));
+        const int64_t s0 = 0, r = std::min(b, n - b);
+        double* Wg = W;
+        const double* Ai = X;
+        const double* Bi = X + b * ldx + b;
+        void* ws2 = reinterpret_cast<char*>(ozws0) + oz_level_scratch(n, b);
+        TRY(fork_to(fc, s));
+        if (uplo == 'L')
+          TRY(launch_oz2_prepare(r, b, r, Bi, ldx, TRI_LOWER, Wg, b, TRI_NONE, ws2, fc->aux, 1, &g_launches));
+        else
+          TRY(launch_oz2_prepare(b, r, r, Wg, b, TRI_NONE, Bi, ldx, TRI_UPPER, ws2, fc->aux, 2, &g_launches));
+        if (uplo == 'L') {
+          TRY(oz_product(r, b, b, A + b * lda, lda, TRI_NONE, Ai, ldx, TRI_LOWER, Wg, b, 1.0, ozws0, s));
+          TRY(join_from(fc, s));
+          TRY(launch_oz2_gemm(r, b, r, Bi, ldx, TRI_LOWER, Wg, b, TRI_NONE, X + b * ldx, ldx, -1.0, 0.0, ws2, s,
+                              &g_launches, 0, 1));
+          TRY(launch_zero_2d(X + b, ldx, b, r, s, &g_launches));
+        } else {
+          TRY(oz_product(b, r, b, Ai, ldx, TRI_UPPER, A + b, lda, TRI_NONE, Wg, b, 1.0, ozws0, s));
+          TRY(join_from(fc, s));
+          TRY(launch_oz2_gemm(b, r, r, Wg, b, TRI_NONE, Bi, ldx, TRI_UPPER, X + b, ldx, -1.0, 0.0, ws2, s,
+                              &g_launches, 0, 2));
+          TRY(launch_zero_2d(X + b * ldx, ldx, r, b, s, &g_launches));
+        }
+        (void)s0;
+        continue;
       }
       const cudaStream_t s_main = s;
       for (int64_t g = 0; g < merges; ++g) {

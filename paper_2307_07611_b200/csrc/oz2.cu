@@ -735,6 +735,19 @@ cudaError_t launch_oz2_prepare(int64_t M, int64_t N, int64_t K, const double* A,
   int* eb = reinterpret_cast<int*>(w); w += al((size_t)N * 4);
   unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(w);
   const int P = oz2_scale_bits(K);
+  // algorithmic bytes: the K ranges split (8 B read, 16 B of residues written per entry)
+  auto range_sum = [&](int64_t rows, int tile, bool upto, bool from) {
+    double sum = 0.0;
+    for (int64_t t0 = 0; t0 < rows; t0 += tile) {
+      const int64_t r = std::min<int64_t>(tile, rows - t0);
+      const int64_t b = from ? t0 : 0, e = upto ? std::min<int64_t>(K, t0 + tile) : K;
+      sum += (double)r * (double)std::max<int64_t>(0, e - b);
+    }
+    return sum;
+  };
+  const double bytes = ((which & 1) ? 24.0 * range_sum(M, OZ2_TM, triA == TRI_LOWER, triA == TRI_UPPER) : 0.0) +
+                       ((which & 2) ? 32.0 * range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER) : 0.0);
+  ProfileScope aux(KIND_OZAUX, 0.0, bytes, st);
   if (which & 1) {
     oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(
         A, lda, (int)M, (int)K, triA, (strict & 1) != 0, P, oz2_use_pair(M, N, K) ? 256 : OZ2_TM, As, ea);
@@ -788,10 +801,10 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   const double eb_n = range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER);
   const bool pair = oz2_use_pair(M, N, K);
   if ((skip & 3) != 3) {
-    ProfileScope aux(KIND_OZAUX, 0.0, ((skip & 1) ? 0.0 : 24.0 * ea_n) + ((skip & 2) ? 0.0 : 32.0 * eb_n), st);
     const cudaError_t e = launch_oz2_prepare(M, N, K, A, lda, triA, B, ldb, triB, ws, st, 3 & ~skip, nullptr, strict);
     if (e != cudaSuccess) return e;
   }
+  (void)ea_n; (void)eb_n;
   (void)maxbits;
   CUtensorMap ma, mb;
   if (!oz2_encode(&ma, As, (uint64_t)K, (uint64_t)OZ2_NMOD * M, OZ2_TM) ||

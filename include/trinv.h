@@ -210,8 +210,8 @@ trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, cons
  * digits * K * 127^2 < 2^31 (K <= 16384 at 8 digits), else TRINV_NOT_SUPPORTED.
  * digits <= 0 selects the modular variant instead: operands scaled to P-bit integers
  * (P = 55 at K = 16384), 16 int8 products modulo 16 pairwise coprime moduli <= 256 and
- * an exact CRT reconstruction (rounded quotient, 128-bit limbs) of the integer product
- * (K <= 65536).
+ * a CRT reconstruction of the integer product as the centred fraction C' / M in 96-bit
+ * fixed point (error < 2^-85 M, then FP64 roundings of 2^-53 relative) (K <= 65536).
  * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, digits) bytes. */
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits);
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,

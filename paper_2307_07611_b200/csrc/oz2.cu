@@ -10,9 +10,10 @@
 // Residues.  With 16 pairwise coprime moduli m_i <= 256 (M = prod m_i ~ 2^125.4),
 // A'_i = A' mod m_i and B'_i in the symmetric range (int8), the tensor cores give
 // C'_i = A'_i B'_i exactly in int32 (|.| <= K 2^14), reduced mod m_i by the epilogue.
-// Reconstruction.  The CRT sum S = sum_i C'_i w_i (w_i the CRT basis of M) is congruent
-// to C' mod M; as |C'| < M/2 by a margin (P chosen from K: 2P + log2 K < log2 M - 1),
-// q = round(S / M) from an FP64 estimate is exact and C' = S - q M in 128-bit integers:
+// Reconstruction.  The CRT sum sum_i C'_i w_i (w_i the CRT basis of M) is congruent to
+// C' mod M, i.e. C' / M == sum_i C'_i y_i / m_i (mod 1); as |C'| < M/2 by a margin (P
+// chosen from K: 2P + log2 K < log2 M - 1), C' / M is that fraction's representative in
+// [-1/2, 1/2), evaluated in 96-bit fixed point (error 2^-85, far below the truncation):
 //     (A B)_ij ~= 2^(e_i - P) 2^(f_j - P) C'_ij,
 // the only errors being the truncation of the scaled operands (2^-P relative to the
 // row / column maxima) and the final rounding to FP64.
@@ -584,46 +585,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ2_THREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * OZ2_TN));
 }
 
-// ---- reconstruction: C' = sum_i c_i w_i - q M -------------------------------------------
-// w_i = M_i (M_i^-1 mod m_i) mod M (so sum_i c_i w_i == C' mod M) in 32-bit limbs
-// w_i = sum_l w_il 2^(32 l).  S = sum_i c_i w_i < 2^138; as |C'| < M/2 by a margin (P from
-// K, oz2_scale_bits), q = round(S / M) and C' = S - q M exactly.  q comes from the two top
-// limb sums in FP64 (error < 2^-40, far inside the margin); S - q M is then evaluated
-// mod 2^128, which is exact because |C'| < 2^124.
+// ---- reconstruction: C' / M = frac(sum_i c_i y_i / m_i) ----------------------------------
+// With M_i = M / m_i and y_i = M_i^-1 mod m_i, sum_i c_i M_i y_i == C' (mod M), so
+//     C' / M == sum_i c_i (y_i / m_i)   (mod 1),
+// and as |C'| < M/2 by a margin (P from K, oz2_scale_bits) C' / M is the representative of
+// that sum in [-1/2, 1/2).  F_i = round(2^96 y_i / m_i) in three 32-bit limbs; the limb sums
+// A_l = sum_i c_i F_il (< 2^44, 64-bit IMAD.WIDE accumulators) give the fraction mod 1 as a
+// signed 96-bit fixed-point number (the integer part carried out of the top limb is dropped)
+// with absolute error < 16 * 255 * 2^-97 < 2^-85, i.e. < 2^41 on C' against the 2^P-sized
+// truncation error of the scaled operands.  C' = fraction * M in FP64 (relative 2^-52).
 struct Oz2Crt {
-  uint32_t w[OZ2_NMOD][2];   // limbs 0, 1 of w_i
-  double wd[OZ2_NMOD][2];    // limbs 2, 3 of w_i (exact in FP64)
-  uint32_t Ml[2];            // M in 32-bit limbs 0, 1
-  double Md[2];              // limbs 2, 3 of M
-  double r64, r96;           // 2^64 / M, 2^96 / M
+  uint32_t f[OZ2_NMOD][3];  // limbs of F_i = round(2^96 y_i / m_i)
+  double Md96;              // M 2^-96
 };
 
-// The four limb sums (each < 2^44, exact) are split between the integer multiply-add pipe
-// (limbs 0, 1: IMAD.WIDE) and the FP64 pipe (limbs 2, 3: exact DFMA on integers < 2^53),
-// which run concurrently.
-__device__ __forceinline__ double oz2_crt_value(const uint32_t (&c)[OZ2_NMOD], const Oz2Crt& crt) {
-  uint64_t a0 = 0, a1 = 0;
-  double s2 = 0.0, s3 = 0.0;
-#pragma unroll
-  for (int q = 0; q < OZ2_NMOD; ++q) {
-    a0 += (uint64_t)crt.w[q][0] * c[q];
-    a1 += (uint64_t)crt.w[q][1] * c[q];
-    const double cd = (double)c[q];  // I2F (the hi/lo-word construction cost two extra instructions)
-    s2 = fma(cd, crt.wd[q][0], s2);
-    s3 = fma(cd, crt.wd[q][1], s3);
-  }
-  const double qd = rint(fma(s3, crt.r96, s2 * crt.r64));  // round(S / M)
-  const uint64_t q = (uint64_t)qd;
-  const int64_t d0 = (int64_t)(a0 - q * crt.Ml[0]), d1 = (int64_t)(a1 - q * crt.Ml[1]);
-  const int64_t d2 = (int64_t)fma(-qd, crt.Md[0], s2), d3 = (int64_t)fma(-qd, crt.Md[1], s3);  // exact, |d| < 2^45
-  const __int128 x = (__int128)d0 + ((__int128)d1 << 32) + ((__int128)d2 << 64) + ((__int128)d3 << 96);
-  const bool neg = x < 0;
-  const unsigned __int128 mag = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
-  const double v = fma((double)(uint64_t)(mag >> 64), 18446744073709551616.0, (double)(uint64_t)mag);
-  return neg ? -v : v;
-}
-
-// 4 consecutive entries of one row per thread (N % 4 == 0): one 32-bit word per plane.
+// 4 consecutive entries of one row per thread (N % 4 == 0): one 32-bit word per plane; the
+// moduli are the outer loop so each constant is loaded once for the four entries.
 __global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int* ea, const int* eb, int P,
                                        double alpha, double beta, double* C, int64_t ldc, const Oz2Crt crt) {
   const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // index of 4 entries
@@ -635,14 +612,26 @@ __global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int
   uint32_t w[OZ2_NMOD];
 #pragma unroll
   for (int q = 0; q < OZ2_NMOD; ++q) w[q] = Rw[q * plane_w];
+  uint64_t a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < OZ2_NMOD; ++q) {
+    const uint32_t f0 = crt.f[q][0], f1 = crt.f[q][1], f2 = crt.f[q][2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t c = __byte_perm(w[q], 0u, 0x4440 + b);
+      a0[b] += (uint64_t)c * f0;
+      a1[b] += (uint64_t)c * f1;
+      a2[b] += (uint64_t)c * f2;
+    }
+  }
   double* out = C + (int64_t)i * ldc + j;
   const int ei = ea[i] - 2 * P;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    uint32_t c[OZ2_NMOD];
-#pragma unroll
-    for (int q = 0; q < OZ2_NMOD; ++q) c[q] = __byte_perm(w[q], 0u, 0x4440 + b);
-    const double val = oz2_ldexp(oz2_crt_value(c, crt), ei + eb[j + b]);
+    const uint64_t b1 = a1[b] + (a0[b] >> 32), b2 = a2[b] + (b1 >> 32);
+    const int64_t hi = (int64_t)(((uint64_t)(uint32_t)b2 << 32) | (uint32_t)b1);  // top 64 of 96 bits, signed
+    const double frac96 = fma((double)hi, 4294967296.0, (double)(uint32_t)a0[b]);  // fraction * 2^96
+    const double val = oz2_ldexp(frac96 * crt.Md96, ei + eb[j + b]);
     out[b] = beta == 0.0 ? alpha * val : fma(alpha, val, beta * out[b]);
   }
 }
@@ -653,23 +642,18 @@ static Oz2Crt oz2_crt_constants() {
   for (int q = 0; q < OZ2_NMOD; ++q) Mall *= (unsigned)oz2_mod(q);
   for (int q = 0; q < OZ2_NMOD; ++q) {
     const unsigned m = (unsigned)oz2_mod(q);
-    const unsigned __int128 Mi = Mall / m;
-    const unsigned y = (unsigned)oz2_inv((int)(Mi % m), (int)m);
-    const unsigned __int128 w = (Mi * y) % Mall;  // Mi y < M 2^8 / m: no overflow (M < 2^126)
-    for (int l = 0; l < 2; ++l) c.w[q][l] = (uint32_t)(w >> (32 * l));
-    for (int l = 0; l < 2; ++l) c.wd[q][l] = (double)(uint32_t)(w >> (32 * (l + 2)));
+    const unsigned y = (unsigned)oz2_inv((int)((Mall / m) % m), (int)m);
+    const unsigned __int128 F = (((unsigned __int128)y << 96) + m / 2) / m;  // < 2^96 (y < m)
+    for (int l = 0; l < 3; ++l) c.f[q][l] = (uint32_t)(F >> (32 * l));
   }
-  for (int l = 0; l < 2; ++l) c.Ml[l] = (uint32_t)(Mall >> (32 * l));
-  for (int l = 0; l < 2; ++l) c.Md[l] = (double)(uint32_t)(Mall >> (32 * (l + 2)));
   const double Md = (double)(unsigned long long)(Mall >> 64) * 18446744073709551616.0 + (double)(unsigned long long)Mall;
-  c.r64 = std::ldexp(1.0, 64) / Md;
-  c.r96 = std::ldexp(1.0, 96) / Md;
+  c.Md96 = std::ldexp(Md, -96);
   return c;
 }
 
 // ---- host -------------------------------------------------------------------------------
-// P with K 2^(2P) <= (1 - 2^-10) M / 2: |C'| < K 2^(2P) keeps round(S / M) unambiguous
-// (oz2_crt_value); at most 58 (the residue chunks of oz2_chunks).
+// P with K 2^(2P) <= (1 - 2^-10) M / 2: |C'| < K 2^(2P) keeps the centred fraction C' / M
+// unambiguous (oz2_reconstruct_kernel); at most 58 (the residue chunks of oz2_chunks).
 static int oz2_scale_bits(int64_t K) {
   double lm = 0.0;
   for (int q = 0; q < OZ2_NMOD; ++q) lm += std::log2((double)oz2_mod(q));

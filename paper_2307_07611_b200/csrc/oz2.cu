@@ -8,8 +8,9 @@
 // significant bits, the scaling is a power of two); columns of B likewise (f_j).
 // Then C' = A' B' is an exact integer matrix with |C'| < K 2^(2P).
 // Residues.  With 16 pairwise coprime moduli m_i <= 256 (M = prod m_i ~ 2^125.4),
-// A'_i = A' mod m_i and B'_i in the symmetric range (int8), the tensor cores give
-// C'_i = A'_i B'_i exactly in int32 (|.| <= K 2^14), reduced mod m_i by the epilogue.
+// A'_i = A' mod m_i in [0, m_i) (uint8) and B'_i in the symmetric range (int8), the tensor
+// cores give C'_i = A'_i B'_i exactly in int32 (|.| <= 255 * 128 K < 2^31 for K <= 65536),
+// reduced mod m_i by the epilogue.
 // Reconstruction.  The CRT sum sum_i C'_i w_i (w_i the CRT basis of M) is congruent to
 // C' mod M, i.e. C' / M == sum_i C'_i y_i / m_i (mod 1); as |C'| < M/2 by a margin (P
 // chosen from K: 2P + log2 K < log2 M - 1), C' / M is that fraction's representative in
@@ -82,6 +83,8 @@ __device__ __forceinline__ double oz2_ldexp(double x, int k) {
 // c2 = 2^40 mod m, s = lo + c1 mid + c2 hi + D < 2^29 is congruent to v + h (h = floor(m/2),
 // D = (h - 2^59) mod m), and (s mod m) - h is the residue of v in [-h, m - 1 - h]:
 // [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m; its low byte is the int8 residue.
+// The A operand takes the plain residue in [0, m - 1] (uint8, h = 0: one instruction less
+// per residue): |sum_k a_k b_k| <= 255 * 128 * K < 2^31 for K <= 65536.
 struct Oz2Chunks {
   uint32_t lo, mid, hi;
 };
@@ -89,9 +92,9 @@ __device__ __forceinline__ Oz2Chunks oz2_chunks(int64_t v) {
   const uint64_t u = (uint64_t)(v + (1ll << 59));
   return {(uint32_t)u & 0xFFFFFu, (uint32_t)(u >> 20) & 0xFFFFFu, (uint32_t)(u >> 40)};
 }
-template <int I>
-__device__ __forceinline__ uint32_t oz2_sym_residue(const Oz2Chunks& x) {
-  constexpr uint32_t m = (uint32_t)oz2_mod(I), h = m / 2;
+template <int I, bool Sym>
+__device__ __forceinline__ uint32_t oz2_residue(const Oz2Chunks& x) {
+  constexpr uint32_t m = (uint32_t)oz2_mod(I), h = Sym ? m / 2 : 0;
   constexpr uint32_t c1 = (uint32_t)((1ull << 20) % m), c2 = (uint32_t)((1ull << 40) % m);
   constexpr uint32_t D = (uint32_t)((h + m - (uint32_t)((1ull << 59) % m)) % m);
   const uint32_t s = x.lo + x.mid * c1 + x.hi * c2 + D;
@@ -101,14 +104,14 @@ __device__ __forceinline__ uint32_t oz2_pack4(uint32_t a, uint32_t b, uint32_t c
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 // residues of 4 consecutive values, packed one 32-bit word per modulus plane
-template <int... I>
+template <bool Sym, int... I>
 __device__ __forceinline__ void oz2_residues4(const int64_t (&v)[4], uint32_t* out, size_t stride_words,
                                               std::integer_sequence<int, I...>) {
   Oz2Chunks x[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) x[q] = oz2_chunks(v[q]);
-  ((out[I * stride_words] = oz2_pack4(oz2_sym_residue<I>(x[0]), oz2_sym_residue<I>(x[1]),
-                                      oz2_sym_residue<I>(x[2]), oz2_sym_residue<I>(x[3]))),
+  ((out[I * stride_words] = oz2_pack4(oz2_residue<I, Sym>(x[0]), oz2_residue<I, Sym>(x[1]),
+                                      oz2_residue<I, Sym>(x[2]), oz2_residue<I, Sym>(x[3]))),
    ...);
 }
 
@@ -164,7 +167,7 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
     int64_t v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) v[q] = k + q == kz ? 0 : (int64_t)oz2_ldexp(x[q], P - e);  // exact, truncated
-    oz2_residues4(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});
+    oz2_residues4<false>(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});  // uint8 residues
   }
 }
 __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols, int tri, bool strict,
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(256, 8) oz2_split_cols_kernel(const double* B,
   const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
   if (j < cols && k < K) {
     const int64_t v[4] = {tile[kq][j - j0], tile[kq + 1][j - j0], tile[kq + 2][j - j0], tile[kq + 3][j - j0]};
-    oz2_residues4(v, reinterpret_cast<uint32_t*>(out) + ((size_t)j * K + k) / 4, (size_t)cols * K / 4,
+    oz2_residues4<true>(v, reinterpret_cast<uint32_t*>(out) + ((size_t)j * K + k) / 4, (size_t)cols * K / 4,
                   std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
       }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
     const uint32_t idesc =
-        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(OZ2_TM >> 4) << 24);
+        (2u << 4) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(OZ2_TM >> 4) << 24);  // u8 x s8 -> s32
     int it = 0;
     for (int i = mod0; i < mod0 + nmod; ++i) {
       const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
@@ -494,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ2_THREADS, 1)
       }
   } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer (leader CTA)
     const uint32_t idesc =
-        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+        (2u << 4) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // u8 x s8 -> s32
     int it = 0;
     for (int i = mod0; i < mod0 + nmod; ++i) {
       const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;

@@ -8,9 +8,9 @@
 // significant bits, the scaling is a power of two); columns of B likewise (f_j).
 // Then C' = A' B' is an exact integer matrix with |C'| < K 2^(2P).
 // Residues.  With 16 pairwise coprime moduli m_i <= 256 (M = prod m_i ~ 2^125.4),
-// A'_i = A' mod m_i in [0, m_i) (uint8) and B'_i in the symmetric range (int8), the tensor
-// cores give C'_i = A'_i B'_i exactly in int32 (|.| <= 255 * 128 K < 2^31 for K <= 65536),
-// reduced mod m_i by the epilogue.
+// A'_i = A' mod m_i in [0, m_i) (uint8) and B'_i likewise (K <= 32768) or in the symmetric
+// range (int8, larger K), the tensor cores give C'_i = A'_i B'_i exactly in int32 (|.| <=
+// 255^2 K or 255 * 128 K, < 2^31), reduced mod m_i by the epilogue.
 // Reconstruction.  The CRT sum sum_i C'_i w_i (w_i the CRT basis of M) is congruent to
 // C' mod M, i.e. C' / M == sum_i C'_i y_i / m_i (mod 1); as |C'| < M/2 by a margin (P
 // chosen from K: 2P + log2 K < log2 M - 1), C' / M is that fraction's representative in
@@ -48,6 +48,7 @@ constexpr int OZ2_A_BYTES = OZ2_TM * OZ2_TK, OZ2_B_BYTES = OZ2_TN * OZ2_TK, OZ2_
 constexpr size_t OZ2_SMEM = (size_t)OZ2_STAGES * OZ2_STAGE + 1024 + 256;
 constexpr int OZ2_THREADS = 192;
 constexpr int OZ2_CMAX_ROWS = 128;
+constexpr int OZ2_U8_MAXK = 32768;  // u8 x u8 products up to this K (255^2 K < 2^31), else u8 x s8
   // rows per block of the column-maximum kernel
 
 // pairwise coprime, <= 256 (symmetric residues fit int8)
@@ -84,7 +85,8 @@ __device__ __forceinline__ double oz2_ldexp(double x, int k) {
 // D = (h - 2^59) mod m), and (s mod m) - h is the residue of v in [-h, m - 1 - h]:
 // [-128, 127] for m = 256, [-(m-1)/2, (m-1)/2] for odd m; its low byte is the int8 residue.
 // The A operand takes the plain residue in [0, m - 1] (uint8, h = 0: one instruction less
-// per residue): |sum_k a_k b_k| <= 255 * 128 * K < 2^31 for K <= 65536.
+// per residue): |sum_k a_k b_k| <= 255 * 128 * K < 2^31 for K <= 65536; so does the B
+// operand when K <= OZ2_U8_MAXK (255^2 K < 2^31).
 struct Oz2Chunks {
   uint32_t lo, mid, hi;
 };
@@ -207,8 +209,11 @@ __global__ void __launch_bounds__(256, 8) oz2_split_cols_kernel(const double* B,
   const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
   if (j < cols && k < K) {
     const int64_t v[4] = {tile[kq][j - j0], tile[kq + 1][j - j0], tile[kq + 2][j - j0], tile[kq + 3][j - j0]};
-    oz2_residues4<true>(v, reinterpret_cast<uint32_t*>(out) + ((size_t)j * K + k) / 4, (size_t)cols * K / 4,
-                  std::make_integer_sequence<int, OZ2_NMOD>{});
+    uint32_t* o = reinterpret_cast<uint32_t*>(out) + ((size_t)j * K + k) / 4;
+    if (K > OZ2_U8_MAXK)
+      oz2_residues4<true>(v, o, (size_t)cols * K / 4, std::make_integer_sequence<int, OZ2_NMOD>{});
+    else
+      oz2_residues4<false>(v, o, (size_t)cols * K / 4, std::make_integer_sequence<int, OZ2_NMOD>{});
   }
 }
 
@@ -300,7 +305,8 @@ __global__ void __launch_bounds__(OZ2_THREADS, 1)
       }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
     const uint32_t idesc =
-        (2u << 4) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(OZ2_TM >> 4) << 24);  // u8 x s8 -> s32
+        (2u << 4) | (p.K > OZ2_U8_MAXK ? 1u << 10 : 0u) | ((uint32_t)(OZ2_TN >> 3) << 17) |
+        ((uint32_t)(OZ2_TM >> 4) << 24);  // u8 x u8 (u8 x s8 above OZ2_U8_MAXK) -> s32
     int it = 0;
     for (int i = mod0; i < mod0 + nmod; ++i) {
       const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;
@@ -497,7 +503,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ2_THREADS, 1)
       }
   } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer (leader CTA)
     const uint32_t idesc =
-        (2u << 4) | (1u << 10) | ((uint32_t)(OZ2_TN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // u8 x s8 -> s32
+        (2u << 4) | (p.K > OZ2_U8_MAXK ? 1u << 10 : 0u) | ((uint32_t)(OZ2_TN >> 3) << 17) |
+        ((uint32_t)(256 >> 4) << 24);  // u8 x u8 (u8 x s8 above OZ2_U8_MAXK) -> s32
     int it = 0;
     for (int i = mod0; i < mod0 + nmod; ++i) {
       const int buf = (i - mod0) & 1, use = (i - mod0) >> 1;

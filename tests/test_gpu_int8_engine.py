@@ -60,6 +60,20 @@ def test_gemm_oz_vs_dmma(struct, digits):
     assert np.max(np.abs(C1 - (-2.0 * R + 0.5 * C0.cpu().numpy()))) <= 1e-12
 
 
+@pytest.mark.parametrize("K", [32768, 40960])
+def test_gemm_oz_crt_long_k(K):
+    """The CRT variant takes u8 x u8 residue products up to K = 32768 (255^2 K < 2^31) and
+    u8 x s8 (symmetric B residues) above: both sides of the switch, at the same bound as
+    test_gemm_oz_vs_dmma."""
+    rng = np.random.default_rng(K)
+    M, N = 128, 256
+    A = rng.uniform(-1, 1, (M, K)); B = rng.uniform(-1, 1, (K, N))
+    R = (A.astype(np.longdouble) @ B.astype(np.longdouble)).astype(np.float64)
+    C = P.gemm_oz(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), digits=0).cpu().numpy()
+    scale = np.abs(A).max(1, keepdims=True) * np.abs(B).max(0, keepdims=True) * K
+    assert np.max(np.abs(C - R) / scale) <= 1e-16
+
+
 @pytest.mark.parametrize("n", [512, 1024, 2048, 3072])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_trinv_int8_engine_parity(int8_engine, n, uplo):

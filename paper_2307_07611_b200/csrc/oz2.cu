@@ -181,7 +181,16 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
   const int k0 = max(kb, (int)blockIdx.y * OZ2_CMAX_ROWS), k1 = min(ke, (int)(blockIdx.y + 1) * OZ2_CMAX_ROWS);
   double m = 0.0;
   const int kz = strict ? j : -1;
-  for (int k = k0; k < k1; ++k) m = k == kz ? m : fmax(m, fabs(B[(int64_t)k * ldb + j]));
+  const double* b = B + j;
+  int k = k0;
+  for (; k + 8 <= k1; k += 8) {  // 8 independent loads in flight per thread
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = b[(int64_t)(k + u) * ldb];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m = k + u == kz ? m : fmax(m, fabs(x[u]));
+  }
+  for (; k < k1; ++k) m = k == kz ? m : fmax(m, fabs(b[(int64_t)k * ldb]));
   if (k0 < k1) atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
 }
 // B operand (K x cols): residues written transposed (cols x K, K-major) through a

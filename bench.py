@@ -276,9 +276,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true", help="never replay steps from a CUDA graph")
     ap.add_argument("--products", default="int8crt", choices=["dmma", "int8", "int8crt"],
-                    help="engine for the level products: INT8 tensor cores by 16 moduli + CRT for blocks >= 4096 "
+                    help="engine for the level products: INT8 tensor cores by 16 moduli + CRT for blocks >= 2048 "
                          "(int8crt, default), by 8-digit splitting (int8), or FP64 DMMA for every level (dmma)")
-    ap.add_argument("--min-block", type=int, default=0, help="INT8 engines: smallest level block (0: 4096)")
+    ap.add_argument("--min-block", type=int, default=0, help="INT8 engines: smallest level block (0: 2048)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -305,7 +305,7 @@ def main():
     stream = torch.cuda.current_stream()
     cfg = CONFIGS[args.config]
     hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
-    mb = args.min_block or 4096
+    mb = args.min_block or 2048
     P.set_product_engine(args.products, min_block=mb)
     if cfg["kind"] not in ("B",) and n_of(cfg) > 128:
         if args.products == "dmma":

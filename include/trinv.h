@@ -145,7 +145,7 @@ trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const doubl
  * <= 128 in registers of one CTA, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
  * through the triangular inverses above and the DMMA engine, Schur complement on
  * the DMMA engine (inv_general's own recursion routes its products of blocks >=
- * 4096 through the INT8 engine).  As in the paper there is no pivoting: the leading principal
+ * 2048 through the INT8 engine).  As in the paper there is no pivoting: the leading principal
  * minors must be non-zero; an exact zero pivot k sets d_info = 1 + k (output then
  * unspecified).  A: device, 16-byte aligned with even lda when n > 128
  * (TRINV_NOT_SUPPORTED otherwise).  ws_bytes >= trinv_workspace_bytes('F', n, ...). */
@@ -222,7 +222,7 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
  * triangular inverses inside inv_from_lu, its U^-1 L^-1 product and the LU products of
  * inv_general): engine 0 = FP64 DMMA (mma.sync), 1 = the INT8 tensor-core engine above
  * with `digits` digits, 2 (default) = its modular (CRT) variant; engines 1 and 2 take
- * every product whose blocks are >= min_block (>= 256; default 4096) and whose shapes
+ * every product whose blocks are >= min_block (>= 256; default 2048) and whose shapes
  * fit their envelope, all other products stay on DMMA.  Scaling guard: when the input's
  * row- or column-maximum exponents (every 17th row sampled) span more than 20 binades,
  * the call runs every product on DMMA (the INT8 engines' truncation is relative to row /

@@ -216,10 +216,10 @@ def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", di
     return C
 
 
-_MIN_BLOCK = 4096  # the engines' block threshold as last set through set_product_engine
+_MIN_BLOCK = 2048  # the engines' block threshold as last set through set_product_engine
 
 
-def set_product_engine(engine="int8crt", digits=8, min_block=4096):
+def set_product_engine(engine="int8crt", digits=8, min_block=2048):
     """Engine of the level products: "int8crt" (default: INT8 tensor cores, 16 moduli + CRT,
     for the levels with block size >= min_block), "int8" (INT8 tensor cores, exact splitting
     into `digits` 7-bit digits) or "dmma" (FP64 mma.sync for every level)."""

@@ -113,7 +113,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // overrides the default before the first call.
 static std::atomic<int> g_engine{-1};
 static std::atomic<int> g_digits{8};
-static std::atomic<int64_t> g_oz_min{4096};
+static std::atomic<int64_t> g_oz_min{2048};  // tools/minblock_probe.py: 2048 beats 1024 / 4096
 static int product_engine() {
   int e = g_engine.load(std::memory_order_relaxed);
   if (e < 0) {

@@ -63,7 +63,7 @@ def general_case(n):
 
 def main():
     for engine in ("dmma", "int8", "int8crt"):
-        P.set_product_engine(engine, min_block=4096 if engine == "int8crt" else 8192)
+        P.set_product_engine(engine, min_block=2048 if engine == "int8crt" else 8192)
         for name, fn in (("config2 n=8192 L", lambda: tri_case(8192, "L", 2)),
                          ("config3 n=32768 U", lambda: tri_case(32768, "U", 3)),
                          ("config4 inv_from_lu n=16384", lambda: lu_case(16384)),

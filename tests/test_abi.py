@@ -63,7 +63,7 @@ def test_workspace_sizes():
     P.set_product_engine("dmma")
     try:
         assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
-        P.set_product_engine()  # default: INT8 CRT engine for blocks >= 4096 adds its residue scratch
+        P.set_product_engine()  # default: INT8 CRT engine for blocks >= 2048 adds its residue scratch
         h = n // 2
         assert ws(b"L", n, None, n, None, n) >= h * h * 8 + 16 * 3 * h * h
         assert P.product_engine() == "int8crt"

@@ -1,6 +1,6 @@
 // oz2.cu — FP64 products on the INT8 tensor cores by modular arithmetic (a
 // CRT-based Ozaki-type scheme, "Ozaki scheme II"): the default product engine for
-// blocks >= 4096 (DESIGN.md §8 "oz2_gemm_kernel", §11), 16 int8 GEMMs per FP64
+// blocks >= 2048 (DESIGN.md §8 "oz2_gemm_kernel", §11), 16 int8 GEMMs per FP64
 // product instead of the 36 digit products of oz.cu.
 //
 // Scaling.  Row i of A is scaled by 2^(P - e_i), 2^e_i > max_k |a_ik|, and truncated:

@@ -482,11 +482,12 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
 }
 
 // ---------------------------------------------------------------------------
+// rows over blockIdx.y (grid-strided), columns over blockIdx.x / threads: no division per entry
 __global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols) {
-  const int64_t total = rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
-    p[i * ld + j] = 0.0;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    double* r = p + i * ld;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols; j += (int64_t)gridDim.x * blockDim.x)
+      r[j] = 0.0;
   }
 }
 
@@ -544,10 +545,9 @@ cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t 
 
 cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cudaStream_t s, int64_t* launches) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
-  const int64_t total = rows * cols;
-  const int64_t blocks = (total + 255) / 256;
-  const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
-  zero_2d_kernel<<<grid, 256, 0, s>>>(p, ld, rows, cols);
+  const int64_t gx = std::min<int64_t>((cols + 255) / 256, 64);
+  const int64_t gy = std::min<int64_t>(rows, std::max<int64_t>(1, (int64_t)device_sms() * 16 / gx));
+  zero_2d_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(p, ld, rows, cols);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -14,13 +14,15 @@ def floored_rel_err(X, R, axis_cols=-1, floor=FLOOR):
     (col_axis=-1 means columns are X[..., :, j]); for column-sample arrays pass
     arrays shaped [ncols, n] with axis_cols=0 meaning each row is one column."""
     X = np.asarray(X, dtype=np.float64); R = np.asarray(R, dtype=np.float64)
+    if X.size == 0:
+        return 0.0
     if axis_cols == 0:
         colmax = np.max(np.abs(R), axis=-1, keepdims=True)
     else:
         colmax = np.max(np.abs(R), axis=-2, keepdims=True)
     den = np.maximum(np.abs(R), floor * colmax)
     den = np.where(den == 0, 1.0, den)
-    return float(np.max(np.abs(X - R) / den)) if X.size else 0.0
+    return float(np.max(np.abs(X - R) / den))
 
 
 def residual_ratio(T, X):

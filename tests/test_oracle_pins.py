@@ -287,6 +287,50 @@ def test_metrics():
     assert oracle.column_residual_ratio(T, Xc, [1]) == 0.0
 
 
+# Hand-computed non-zero values for the metric code (reading C7/C8; the residual is the
+# definition L X = I of the bordering inverse, and S K = A^-1).
+# Each case is chosen so that a dropped sqrt, a swapped product order (X T for T X), a
+# mean instead of a max over a batch, a mis-indexed identity column or the wrong column
+# axis gives a different number.
+def test_residual_ratio_hand_values():
+    # T = diag(2, 1), X = diag(0.5, 1.1): T X - I = diag(0, 0.1)
+    T = np.diag([2.0, 1.0]); X = np.diag([0.5, 1.1])
+    assert oracle.residual_ratio(T, X) == pytest.approx(0.1 / (np.sqrt(5.0) * np.sqrt(1.46)), rel=1e-12)
+    # T = [[2,0],[1,1]], X = [[.5,0],[-.4,1]]: T X = [[1,0],[.1,1]] (X T would give .2)
+    T = np.array([[2.0, 0.0], [1.0, 1.0]]); X = np.array([[0.5, 0.0], [-0.4, 1.0]])
+    want = 0.1 / np.sqrt(6.0 * 1.41)
+    assert oracle.residual_ratio(T, X) == pytest.approx(want, rel=1e-12)
+    # batch: max over the batch, not the mean (the identity pair contributes 0)
+    Tb = np.stack([np.eye(2), T]); Xb = np.stack([np.eye(2), X])
+    assert oracle.residual_ratio(Tb, Xb) == pytest.approx(want, rel=1e-12)
+
+
+def test_column_residual_ratio_hand_values():
+    T = np.array([[2.0, 0.0], [1.0, 1.0]])  # inverse [[.5, 0], [-.5, 1]]
+    # column 0 given as [.5, -.4]: T x - e_0 = [0, .1]; ||T||_F = sqrt 6, ||x|| = sqrt .41
+    assert oracle.column_residual_ratio(T, np.array([[0.5, -0.4]]), [0]) == pytest.approx(
+        0.1 / np.sqrt(6.0 * 0.41), rel=1e-12)
+    # columns (1, 0) in that order: column 1 given as [0, 1.2] (T x - e_1 = [0, .2]),
+    # column 0 exact; the identity must be subtracted at rows cols[c]
+    Xc = np.array([[0.0, 1.2], [0.5, -0.5]])
+    assert oracle.column_residual_ratio(T, Xc, [1, 0]) == pytest.approx(
+        0.2 / np.sqrt(6.0 * (1.44 + 0.25 + 0.25)), rel=1e-12)
+
+
+def test_floored_rel_err_hand_values():
+    # axis_cols=0: each ROW of the arrays is one column of the inverse, floor from its own max
+    R = np.array([[1e-9, 2.0], [4.0, 1e-3]])
+    X = R + np.array([[1e-12, 0.0], [0.0, 1e-12]])
+    # row 0: den = max(1e-9, 1e-6 * 2) = 2e-6 -> 5e-7; row 1: den = max(1e-3, 4e-6) = 1e-3
+    # -> 1e-9.  Max 5e-7 (flooring along the other axis would give 2.5e-7)
+    assert oracle.floored_rel_err(X, R, axis_cols=0) == pytest.approx(5e-7, rel=1e-9)
+    # default axis: columns are X[:, j]; col 0 = (1e-9, 4) floor 4e-6, col 1 = (2, 1e-3) floor 2e-6
+    assert oracle.floored_rel_err(X, R) == pytest.approx(max(1e-12 / 4e-6, 1e-12 / 1e-3), rel=1e-9)
+    # an all-zero reference column divides by 1 (absolute error)
+    assert oracle.floored_rel_err(np.array([[0.0, 0.0], [3e-3, 0.0]]), np.zeros((2, 2))) == pytest.approx(3e-3)
+    assert oracle.floored_rel_err(np.zeros((0, 3)), np.zeros((0, 3))) == 0.0
+
+
 # --- NEXT row f2: SKUL (Alg. 5) ------------------------------------------
 def test_skul_paper_5x5_printed(golden):
     g = golden("paper_5x5_factors.txt")

@@ -2,19 +2,26 @@
 """bench.py — throughput of the FP64 triangular-inverse hot path on B200.
 
 Default workload (BASELINE.json configs[1], the metric's batched case):
-131072 independent lower-triangular 32x32 fp64 matrices per GPU, matrix b
-seeded by its global index b, row-major contiguous, inverted by trinv_batched
-(one launch per step).  `value` = matrices inverted by all ranks / max-over-
-ranks device time, inverses/s.  --config 0|2|3|4 runs the single-matrix
-configurations (GFLOP/s at n^3/3 per triangular inverse, 4n^3/3 for config 4)
-as separate lines.
+131072 independent lower-triangular 32x32 fp64 matrices, matrix b seeded by
+its global index b, row-major contiguous, inverted by trinv_batched (one
+launch per step).  `value` = matrices inverted by all ranks / max-over-ranks
+device time, inverses/s.  At N = 1 the same line carries an "fp64" block:
+BASELINE configs 2, 3 and 4 (the metric's FP64 half) timed in the same run on
+the DMMA engine, with their fraction of the FP64 tensor-core peak measured
+live (trinv_probe_dmma_tflops).  --config 0|2|3|4 runs a single-matrix
+configuration as the main line instead.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-Multi-GPU: launched by torchrun, one rank per GPU; config 1 is partitioned by
-batch (weak scaling: every rank inverts its own 131072 matrices, global
-indices rank*131072 + b); no collective touches the data path (the barrier
-and the max-over-ranks timing reduction only).
+Multi-GPU: launched by torchrun, one rank per GPU; config 1 is sharded by
+batch as BASELINE states ("sharded by batch over 1/2/4/8 GPUs", strong
+scaling: rank r inverts dist.shard_range(131072, N, r), 131072/N matrices,
+generated locally from their global indices); no collective touches the
+timed data path.  After the timed region the shards are gathered on rank 0
+(NCCL gather, timed apart with its NVLink roofline) and rank 0 checks that the
+gathered batch equals, bit for bit, its own single-GPU inversion of all 131072
+matrices (sharding invariance, SURVEY P-l).  --scaling weak gives every rank
+its own 131072 matrices instead.
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on the
 host cores on a bounded sample of the same workload; it is the tier's
@@ -102,7 +109,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index, period=0.005):
+    def __init__(self, index, period=0.0005):
         self.index, self.period = index, period
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
@@ -213,6 +220,20 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- CPU baseline leg
+def one_thread(fn):
+    """Seconds of fn() with the oracle's OpenMP loops on one thread (restored after)."""
+    import oracle
+    prev = oracle.max_threads()
+    oracle.set_threads(1)
+    try:
+        fn()
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+    finally:
+        oracle.set_threads(prev)
+
+
 def cpu_baseline(cfg):
     import numpy as np
     import oracle
@@ -228,8 +249,10 @@ def cpu_baseline(cfg):
             if time.perf_counter() - t0 > 2.0:
                 break
         dt = (time.perf_counter() - t0) / reps
+        t1 = one_thread(lambda: oracle.crit_batched(A[:4096]))
         return {"value": sample / dt, "unit": "inverses/s", "cores": cores, "kind": "oracle",
-                "sample": f"{sample} of the 131072 config-1 matrices x {reps} reps, OpenMP over matrices"}
+                "sample": f"{sample} of the 131072 config-1 matrices x {reps} reps, OpenMP over matrices",
+                "value_1thread": 4096 / t1, "sample_1thread": "4096 of the config-1 matrices, 1 OpenMP thread"}
     n = cfg["n"]
     if cfg["kind"] == "A":  # SKUL oracle (O(n^3)) on a smaller order, GFLOP/s at 2n^3
         m = 1024
@@ -240,11 +263,17 @@ def cpu_baseline(cfg):
         return {"value": 2 * m ** 3 / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                 "sample": f"SKUL + S K at n={m} (the n={n} workload would take hours on the host)"}
     if n <= 2048:
-        T = synth.host(n, uplo="L" if cfg["kind"] != "U" else "U", diag=cfg.get("diag", "signed"))
-        t0 = time.perf_counter(); oracle.trinv(T, "L" if cfg["kind"] != "U" else "U")
-        dt = time.perf_counter() - t0
+        uplo = "L" if cfg["kind"] != "U" else "U"
+        T = synth.host(n, uplo=uplo, diag=cfg.get("diag", "signed"))
+        reps = 200 if n <= 128 else 1
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.trinv(T, uplo)
+        dt = (time.perf_counter() - t0) / reps
+        t1 = one_thread(lambda: [oracle.trinv(T, uplo) for _ in range(reps)]) / reps
         return {"value": n ** 3 / 3 / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-                "sample": f"full inverse n={n}"}
+                "sample": f"full inverse n={n} x {reps}", "value_1thread": n ** 3 / 3 / t1 / 1e9,
+                "us_per_call": dt * 1e6, "us_per_call_1thread": t1 * 1e6}
     cols = np.arange(0, n, n // 16)[:16]
     if cfg["kind"] == "G":
         L = synth.host(n, tag="L", diag="one"); U = synth.host(n, tag="U", uplo="U", diag="pos")
@@ -264,6 +293,118 @@ def cpu_baseline(cfg):
             "sample": f"{len(cols)} sampled columns, extrapolated to the full inverse by the column cost model"}
 
 
+# ----------------------------------------------------------------------------- config 1 at N > 1
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def gather_and_check(X, count, strong, world, rank, dev, stream, backend, n, barrier, max_over_ranks, P, torch,
+                     dist):
+    """Gather every rank's shard on rank 0 (NCCL gather = one send per rank into rank 0), timed
+    apart from the throughput with its NVLink roofline (rank 0's ingress bytes / the measured
+    peer-copy bandwidth), then rank 0 inverts the whole 131072-matrix batch itself and compares
+    the gathered result bit for bit (sharding invariance, SURVEY P-l)."""
+    import hashlib
+    import synth
+    nccl = backend == "nccl"
+    send = X if nccl else X.cpu()
+    recv = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    for _ in range(2):  # warm the communicator
+        dist.gather(send, recv, dst=0)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    dist.gather(send, recv, dst=0)
+    e1.record(stream)
+    barrier()
+    wall = time.perf_counter() - t0
+    g_ms = max_over_ranks(e0.elapsed_time(e1) if nccl else wall * 1e3)
+    ingress = (world - 1) * count * n * n * 8
+    out = {"op": "dist.gather to rank 0" + (" (NCCL)" if nccl else f" ({backend}, host-staged)"),
+           "ms": g_ms, "rank0_ingress_bytes": ingress,
+           "achieved_gbs": ingress / (g_ms / 1e3) / 1e9 if g_ms > 0 else None,
+           "peak_gbs": NVLINK_PEER_GBS, "peak_source": "B200_PROFILING.md measured peer copy per direction",
+           "frac": ingress / (g_ms / 1e3) / 1e9 / NVLINK_PEER_GBS if g_ms > 0 else None,
+           "in_throughput": False}
+    if rank == 0 and strong:
+        G = torch.cat([r.to(dev) for r in recv], dim=0)
+        Af = torch.empty((BATCH, n, n), dtype=torch.float64, device=dev)
+        synth.device_fill(Af, n, b0=0)
+        Xf = P.trinv_batched(Af, "L")
+        torch.cuda.synchronize()
+        h = lambda t: hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()[:16]  # noqa: E731
+        hg, h1 = h(G), h(Xf)
+        out.update({"hash_gathered": hg, "hash_g1": h1, "hash_equal_g1": hg == h1,
+                    "hash_note": "sha256 of the 131072 x 32 x 32 fp64 result: gathered shards vs one rank "
+                                 "inverting the whole batch"})
+        del G, Af, Xf
+    return out
+
+
+# ----------------------------------------------------------------------------- fp64 block (N = 1)
+def fp64_block(args, dev, stream, P, synth, torch, barrier):
+    """BASELINE configs 2, 3, 4 on the default DMMA engine in the same run: GFLOP/s (n^3/3 per
+    triangular inverse, 4n^3/3 for inv_from_lu) and the fraction of the FP64 tensor-core peak
+    measured live (register-only DMMA loop) before and after the block."""
+    peak0 = P.lib().trinv_probe_dmma_tflops(200.0, ctypes_stream(stream))
+    out = {"engine": P.product_engine(), "configs": {}}
+    W = max(3, args.warmup)
+    for c in (2, 3, 4):
+        cfg = CONFIGS[c]
+        n = cfg["n"]
+        if cfg["kind"] == "G":
+            Lm = torch.empty((n, n), dtype=torch.float64, device=dev)
+            Um = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(Lm, n, tag="L", diag="one")
+            synth.device_fill(Um, n, tag="U", uplo="U", diag="pos")
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            step = lambda: P.inv_from_lu(Lm, Um, unit_l=True, out=X)  # noqa: E731
+            flops = 4 * n ** 3 / 3
+        else:
+            A = torch.empty((n, n), dtype=torch.float64, device=dev)
+            synth.device_fill(A, n, uplo=cfg["kind"], diag=cfg["diag"])
+            X = torch.empty((n, n), dtype=torch.float64, device=dev)
+            f = P.trinv_lower if cfg["kind"] == "L" else P.trinv_upper
+            step = lambda: f(A, out=X)  # noqa: E731
+            flops = n ** 3 / 3
+        for _ in range(W):
+            step()
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.fp64_steps + 1)]
+        with ClockSampler(dev.index) as clk:
+            ev[0].record(stream)
+            for i in range(args.fp64_steps):
+                step()
+                ev[i + 1].record(stream)
+            barrier()
+        ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.fp64_steps)]
+        med = statistics.median(ms)
+        tf = flops / (med / 1e3) / 1e12
+        out["configs"][f"config{c}"] = {
+            "workload": cfg["workload"], "n": n, "flops_per_call": flops,
+            "ms": {"median": med, "min": min(ms), "max": max(ms)}, "steps": args.fp64_steps, "warmup": W,
+            "gflops": tf * 1e3, "clocks": clk.summary()}
+        del X
+        if cfg["kind"] == "G":
+            del Lm, Um
+        else:
+            del A
+        torch.cuda.empty_cache()
+    peak1 = P.lib().trinv_probe_dmma_tflops(200.0, ctypes_stream(stream))
+    peak = max(peak0, peak1)
+    out["fp64_tc_peak"] = {"tflops": peak, "before": peak0, "after": peak1,
+                           "source": "trinv_probe_dmma_tflops: register-only mma.sync m8n8k4 f64 (DMMA.8x8x4) "
+                                     "loop on all SMs, measured in this run (max of before / after the block)"}
+    for v in out["configs"].values():
+        v["frac_of_fp64_tc_peak"] = v["gflops"] / 1e3 / peak if peak > 0 else None
+    return out
+
+
+def ctypes_stream(stream):
+    import ctypes
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -275,10 +416,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true", help="never replay steps from a CUDA graph")
-    ap.add_argument("--products", default="int8crt", choices=["dmma", "int8", "int8crt"],
-                    help="engine for the level products: INT8 tensor cores by 16 moduli + CRT for blocks >= 2048 "
-                         "(int8crt, default), by 8-digit splitting (int8), or FP64 DMMA for every level (dmma)")
+    ap.add_argument("--products", default="dmma", choices=["dmma", "int8crt"],
+                    help="engine for the level products: FP64 DMMA for every level (dmma, default) or the opt-in "
+                         "FP64-emulated (Ozaki-II) INT8 tensor-core engine, 16 moduli + CRT, for blocks >= 2048")
     ap.add_argument("--min-block", type=int, default=0, help="INT8 engines: smallest level block (0: 2048)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="config 1 at N > 1: shard the 131072-matrix batch over the ranks (strong, BASELINE) "
+                         "or give every rank its own 131072 matrices (weak)")
+    ap.add_argument("--no-fp64", action="store_true", help="config 1 at N = 1: skip the FP64 configs 2-4 block")
+    ap.add_argument("--fp64-steps", type=int, default=3, help="timed steps per FP64 config of the fp64 block")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -311,7 +457,7 @@ def main():
         if args.products == "dmma":
             cfg = dict(cfg, workload=cfg["workload"] + " [FP64 DMMA products]")
         else:
-            desc = "8-digit splitting" if args.products == "int8" else "16 moduli + CRT"
+            desc = "16 moduli + CRT"
             cfg = dict(cfg, workload=cfg["workload"] + f" [products of blocks >= {mb} on the INT8 tensor cores "
                                                        f"({desc}), smaller ones on FP64 DMMA]")
 
@@ -328,14 +474,17 @@ def main():
         return float(t.item())
 
     n = cfg["n"]
+    strong = cfg["kind"] == "B" and args.scaling == "strong"
     if cfg["kind"] == "B":
-        B = BATCH
+        from paper_2307_07611_b200.dist import shard_range
+        b0, B = shard_range(BATCH, world, rank) if strong else (rank * BATCH, BATCH)
         A = torch.empty((B, n, n), dtype=torch.float64, device=dev)
-        synth.device_fill(A, n, b0=rank * B)
+        synth.device_fill(A, n, b0=b0)  # matrix b seeded by its global index (shard-invariant)
         X = torch.empty_like(A)
         def step():
             P.trinv_batched(A, "L", out=X)
         units_per_rank, unit = B, "inverses/s"
+        total_units = BATCH if strong else BATCH * world
         algo_bytes_per_launch = B * (n * (n + 1) / 2 + n * n) * 8  # triangle in + full matrix out
         flops_per_step = B * n ** 3 / 3
     else:
@@ -429,23 +578,32 @@ def main():
     total_ms = ev[0].elapsed_time(ev[-1])
     total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
-    value = units_per_rank * world * args.steps / (total_ms / 1e3)
+    if cfg["kind"] == "B":
+        value = total_units * args.steps / (total_ms / 1e3)
+    else:
+        value = units_per_rank * world * args.steps / (total_ms / 1e3)
 
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if cfg["kind"] == "S" else "weak",
+            "scaling": "strong" if (cfg["kind"] == "S" or strong) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based SplitMix64, synth/)"}
     conf = {"workload": cfg["workload"], "n": n, "per_rank_units": units_per_rank,
             "l2_policy": "inputs larger than L2 (126 MB)" if (cfg["kind"] == "B" or n >= 4096)
             else "input smaller than L2, not flushed (latency config)",
             "parallelism": f"batch partition x{world}" if cfg["kind"] == "B" else "replicas (single matrix per GPU)"}
+    if step_ms:
+        line["step_ms_stats"] = {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms),
+                                 "rank": rank}
     if cfg["kind"] == "B":
-        conf["batch_per_rank"] = BATCH
+        conf["batch_per_rank"] = B
+        conf["batch_total"] = total_units
+        conf["parallelism"] = (f"batch shards of {B} over {world} rank(s) (dist.shard_range)" if strong
+                               else f"batch partition x{world}, {BATCH} matrices per rank (weak)")
     elif n > 128:
         conf["arithmetic"] = ("FP64 (DMMA mma.sync) for every level product" if args.products == "dmma" else
                               "FP64 results; level products of blocks >= %d computed exactly in int8 x int8 -> int32 "
                               "on the tcgen05 tensor cores (%s) and reconstructed in FP64, smaller ones on FP64 DMMA"
-                              % (mb, "8-digit splitting" if args.products == "int8" else "16 moduli + CRT"))
+                              % (mb, "16 moduli + CRT"))
         if cfg["kind"] in ("G", "A") and args.products == "int8crt":
             conf["arithmetic"] += ("; U^-1 L^-1 as its diagonal terms (one elementwise pass) plus the strictly "
                                    "triangular product on the INT8 engine" +
@@ -456,9 +614,9 @@ def main():
     if cfg["kind"] == "B":
         avg_ms = statistics.mean(step_ms)  # one launch per step: the leaf kernel
         achieved = algo_bytes_per_launch / (avg_ms / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": "leaf32_tma_kernel (trinv_batched)", "achieved": achieved,
+        line["roofline"] = {"bound": "hbm", "kernel": "leaf32_mma_kernel (trinv_batched)", "achieved": achieved,
                             "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                            "traffic": ncu_traffic("leaf32_tma_kernel"), "peak_source": hbm_src,
+                            "traffic": ncu_traffic("leaf32_mma_kernel"), "peak_source": hbm_src,
                             "algorithmic_bytes_per_launch": algo_bytes_per_launch,
                             "launch_ms": avg_ms, "fp64_gflops": flops_per_step / (avg_ms / 1e3) / 1e9}
     else:
@@ -476,8 +634,7 @@ def main():
         if n_o > 0 and ms_o + ms_x >= ms_d:  # the INT8 engine carries the dominant products
             i8_peak = 2.0 * I8_PER_BF16_SUSTAINED
             ach = ops_o / (ms_o / 1e3) / 1e12
-            kname = ("oz_gemm_kernel (INT8 tcgen05, exact 8-digit splitting)" if args.products == "int8"
-                     else "oz2_gemm_kernel (INT8 tcgen05, 16 moduli + CRT)")
+            kname = "oz2_gemm_kernel (INT8 tcgen05, 16 moduli + CRT; FP64-emulated, Ozaki-II)"
             line["roofline"] = {"bound": "tensor", "kernel": kname,
                                 "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
                                 "traffic": ncu_traffic("oz2_gemm_kernel") if args.products == "int8crt" else None,
@@ -523,13 +680,13 @@ def main():
     if cfg["kind"] == "B" and args.e2e_steps > 0:
         # host buffers through the library's pipelined host entry point (trinv_batched_host:
         # chunked H2D / invert / D2H on overlapping streams); copies are inside the timed region
-        h_in = torch.empty((BATCH, n, n), dtype=torch.float64).pin_memory()
+        h_in = torch.empty((B, n, n), dtype=torch.float64).pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
         h_in.copy_(A.cpu())
         ws = torch.empty(P.lib().trinv_batched_host_workspace_bytes(n, 0), dtype=torch.uint8, device=dev)
         import ctypes
         def e2e_step():
-            st = P.lib().trinv_batched_host(b"L", n, BATCH, ctypes.c_void_p(h_in.data_ptr()),
+            st = P.lib().trinv_batched_host(b"L", n, B, ctypes.c_void_p(h_in.data_ptr()),
                                             ctypes.c_void_p(h_out.data_ptr()), 0, 0,
                                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), None,
                                             ctypes.c_void_p(stream.cuda_stream))
@@ -542,8 +699,9 @@ def main():
         e1.record(stream); barrier()
         e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.e2e_steps
         nbytes = h_in.numel() * 8
-        line["e2e"] = {"value": BATCH * world / (e_ms / 1e3), "unit": unit, "h2d_bytes_per_step": nbytes,
-                       "d2h_bytes_per_step": nbytes, "ms_per_step": e_ms, "steps": args.e2e_steps,
+        line["e2e"] = {"value": total_units / (e_ms / 1e3), "unit": unit, "h2d_bytes_per_step": nbytes,
+                       "d2h_bytes_per_step": nbytes, "bytes_are": "per rank (its shard)" if world > 1 else "whole job",
+                       "ms_per_step": e_ms, "steps": args.e2e_steps,
                        "path": "pinned host -> trinv_batched_host (C-ABI; 4096-matrix chunks, H2D / invert / "
                                "D2H overlapped on 3 streams) -> pinned host",
                        "pcie_gbs_each_way": nbytes / (e_ms / 1e3) / 1e9}
@@ -567,6 +725,13 @@ def main():
                        "h2d_bytes_per_step": sum(h.numel() * 8 for h in h_ins), "d2h_bytes_per_step": n * n * 8,
                        "ms_per_step": e_ms, "steps": steps_e}
 
+    if cfg["kind"] == "B" and world > 1:
+        line["gather"] = gather_and_check(X, B, strong, world, rank, dev, stream, backend, n, barrier,
+                                          max_over_ranks, P, torch, dist)
+    if cfg["kind"] == "B" and world == 1 and not args.no_fp64:
+        del A, X
+        torch.cuda.empty_cache()
+        line["fp64"] = fp64_block(args, dev, stream, P, synth, torch, barrier)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:

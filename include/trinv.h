@@ -14,7 +14,9 @@
  *    work on `stream` and returns; completion is observed through the stream.
  *  - Ownership: the caller allocates and frees every buffer.  The library
  *    never allocates device memory on the call path and keeps no pointer after
- *    returning.  Buffers must stay alive until the enqueued work completes.
+ *    returning (with the default product engine; the opt-in INT8 engine keeps a
+ *    per-device guard scratch, see trinv_set_product_engine).  Buffers must
+ *    stay alive until the enqueued work completes.
  *  - Only the referenced triangle of an input is used (the other triangle may
  *    hold anything, including NaN; it may be loaded but never enters the
  *    arithmetic).  With diag == TRINV_UNIT the stored diagonal is not used and
@@ -27,7 +29,9 @@
  *    ("If R_jj = 0 stop", P:713-714 / P:731-732) is reported through d_info
  *    (device int32, may be NULL) as 1 + the smallest such row index, 0 if
  *    none (LAPACK trtri convention).  The output of a singular input is
- *    unspecified (Inf/NaN).  NaN/Inf inputs propagate.  No host sync occurs.
+ *    unspecified (Inf/NaN).  NaN/Inf inputs propagate.  No host sync occurs
+ *    (with the default product engine; the opt-in INT8 engine's scaling guard
+ *    synchronises once per call, see trinv_set_product_engine).
  *  - Entry points are re-entrant and thread-safe; they may be called on any
  *    device (the current device is used).
  */
@@ -124,10 +128,10 @@ trinv_status_t trinv_batched_host(char uplo, int64_t n, int64_t batch, const dou
 /* General inverse from triangular factors, X = (L U)^{-1} = U^{-1} L^{-1}
  * (SKUL, "S K = A^{-1}" with S = U^{-1}, K = L^{-1}): L^{-1} and
  * U^{-1} by the two calls above, then the upper x lower product
- * X_ij = sum_{k >= max(i,j)} (U^{-1})_ik (L^{-1})_kj  (P_UL):
- * with the INT8 CRT engine (default, n >= its block threshold) the diagonal terms in
- * one elementwise pass and the strictly triangular product on the tensor cores, else
- * on the DMMA engine.  Lf (lower, ldl) and Uf (upper, ldu) are read-only; X
+ * X_ij = sum_{k >= max(i,j)} (U^{-1})_ik (L^{-1})_kj  (P_UL) on the
+ * DMMA engine (with the opt-in INT8 CRT engine and n >= its block threshold: the
+ * diagonal terms in one elementwise pass and the strictly triangular product on the
+ * INT8 tensor cores).  Lf (lower, ldl) and Uf (upper, ldu) are read-only; X
  * (ldx) must not overlap either (TRINV_ALIASING).  diagL / diagU select unit
  * factors (the paper's Crout makes U unit; BASELINE config 4 makes L
  * unit).  ws_bytes >= trinv_workspace_bytes('G', n, Lf, ldl, X, ldx).
@@ -144,8 +148,8 @@ trinv_status_t inv_from_lu(int64_t n, const double* Lf, int64_t ldl, const doubl
  * strict upper triangle holds U.  Blocked right-looking recursion: diagonal blocks
  * <= 128 in registers of one CTA, off-diagonal blocks U12 = L11^-1 A12 and L21 = A21 U11^-1
  * through the triangular inverses above and the DMMA engine, Schur complement on
- * the DMMA engine (inv_general's own recursion routes its products of blocks >=
- * 2048 through the INT8 engine).  As in the paper there is no pivoting: the leading principal
+ * the DMMA engine (with the opt-in INT8 engine, inv_general's own recursion routes its
+ * products of blocks >= 2048 through it).  As in the paper there is no pivoting: the leading principal
  * minors must be non-zero; an exact zero pivot k sets d_info = 1 + k (output then
  * unspecified).  A: device, 16-byte aligned with even lda when n > 128
  * (TRINV_NOT_SUPPORTED otherwise).  ws_bytes >= trinv_workspace_bytes('F', n, ...). */
@@ -200,19 +204,18 @@ size_t trinv_strassen_workspace_bytes(int64_t n);
 trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                    int64_t ldc, void* ws, size_t ws_bytes, void* stream);
 
-/* Opt-in product engine (experiment): C = alpha A B + beta C in FP64
- * with the products on the INT8 tensor cores (tcgen05 kind::i8) by exact operand
- * splitting: rows of A / columns of B scaled by powers of two and cut into `digits`
- * signed 7-bit digits; the digit pairs with t + u <= digits + 1 are multiplied exactly
- * (int32) and summed in FP64 (error ~ K 2^(-7 digits) |row max| |column max|).
- * Row-major device matrices; structA / structB as in trinv_gemm (one triangular
- * operand at most).  Envelope: M % 128 == 0, N % 256 == 0, K % 128 == 0,
- * digits * K * 127^2 < 2^31 (K <= 16384 at 8 digits), else TRINV_NOT_SUPPORTED.
- * digits <= 0 selects the modular variant instead: operands scaled to P-bit integers
- * (P = 55 at K = 16384), 16 int8 products modulo 16 pairwise coprime moduli <= 256 and
- * a CRT reconstruction of the integer product as the centred fraction C' / M in 96-bit
- * fixed point (error < 2^-85 M, then FP64 roundings of 2^-53 relative) (K <= 65536).
- * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, digits) bytes. */
+/* Opt-in FP64-emulated product (Ozaki-II): C = alpha A B + beta C with the
+ * products on the INT8 tensor cores (tcgen05 kind::i8) by modular arithmetic: operands
+ * scaled row- / column-wise by powers of two to P-bit integers (P = 55 at K = 16384), 16
+ * int8 products modulo 16 pairwise coprime moduli <= 256 and a CRT reconstruction of the
+ * integer product as the centred fraction C' / M in 96-bit fixed point (error < 2^-85 M,
+ * then FP64 roundings of 2^-53 relative).  The error is normwise (2^-P of the row / column
+ * maxima), not componentwise as on DMMA.  A row of A or column of B holding NaN / Inf makes
+ * that row / column of C NaN.  Row-major device matrices; structA / structB as in
+ * trinv_gemm (one triangular operand at most, or 'U' x 'L').  Envelope: M % 128 == 0,
+ * N % 256 == 0, K % 128 == 0, K <= 65536, else TRINV_NOT_SUPPORTED.  `digits` must be 0
+ * (the digit-splitting variant was retired: TRINV_NOT_SUPPORTED otherwise).
+ * ws: device scratch of trinv_gemm_oz_workspace_bytes(M, N, K, 0) bytes. */
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits);
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                              char structA, const double* B, int64_t ldb, char structB, double beta, double* C,
@@ -220,27 +223,39 @@ trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, cons
 
 /* Product engine for the level products of trinv_lower / trinv_upper (and the
  * triangular inverses inside inv_from_lu, its U^-1 L^-1 product and the LU products of
- * inv_general): engine 0 = FP64 DMMA (mma.sync), 1 = the INT8 tensor-core engine above
- * with `digits` digits, 2 (default) = its modular (CRT) variant; engines 1 and 2 take
- * every product whose blocks are >= min_block (>= 256; default 2048) and whose shapes
- * fit their envelope, all other products stay on DMMA.  Scaling guard: when the input's
- * row- or column-maximum exponents (every 17th row sampled) span more than 20 binades,
- * the call runs every product on DMMA (the INT8 engines' truncation is relative to row /
- * column maxima); the check costs one 16-byte device-to-host read per
- * call, resolved by an event when the first INT8 product is reached, and is skipped
- * under stream capture.  Process-wide; the environment variable
- * TRINV_PRODUCTS=dmma|int8|int8crt selects the engine before the first call.  Changing
- * it changes trinv_workspace_bytes ('L', 'U', 'G', 'A', 'F'): query the workspace after. */
+ * inv_general): engine 0 (default) = FP64 DMMA (mma.sync) for every product, the engine
+ * BJ.north_star names; 2 = opt-in FP64 emulation on the INT8 tensor cores (the modular
+ * engine above) for every product whose blocks are >= min_block (>= 256; default 2048) and
+ * whose shapes fit its envelope, all other products on DMMA.  Any other engine value:
+ * TRINV_INVALID_ARG; `digits` is ignored.  Engine 2 runs a scaling guard per call: the
+ * exact spread of the row- and column-maximum exponents of the input's referenced entries
+ * (a unit diagonal counted as 1, its stored value not read) is computed on the device;
+ * above 8 binades, or with any NaN / Inf entry, the call runs every product on DMMA.  The
+ * guard costs one read of the input and ONE HOST SYNCHRONISATION per call (an event,
+ * resolved when the first INT8 product is reached), a one-time 64-byte pinned host
+ * allocation per thread and device and a per-device device scratch of 2 n doubles that
+ * grows with n (allocated outside the workspace).  Under stream capture the guard cannot
+ * run and the captured call uses DMMA.  Process-wide; the environment variable
+ * TRINV_PRODUCTS=dmma|int8crt selects the engine before the first call.  Changing it
+ * changes trinv_workspace_bytes ('L', 'U', 'G', 'A', 'F'): query the workspace after. */
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block);
 int trinv_get_product_engine(void);
 
-/* The scaling guard of the INT8 engines on its own (for callers composing products
+/* The scaling guard of the INT8 engine on its own (for callers composing products
  * themselves, e.g. the multi-rank split): 1 when the row- and column-maximum exponents
  * of the n x n matrix A (device, ld lda; uplo 'L' / 'U' = only that triangle is read,
- * 'N' = all of it; every 17th row sampled) span at most 20 binades, or when `stream` is
- * capturing (check skipped); 0 otherwise; -TRINV_INVALID_ARG / -TRINV_CUDA_ERROR on
- * error.  Waits for the check on `stream` (one 16-byte device-to-host read). */
-int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, void* stream);
+ * 'N' = all of it; diag = TRINV_UNIT: the stored diagonal is not read and counts as 1)
+ * span at most 8 binades and every referenced entry is finite; 0 otherwise, and 0 when
+ * `stream` is capturing (the check cannot run); -TRINV_INVALID_ARG / -TRINV_CUDA_ERROR
+ * on error.  Waits for the check on `stream`. */
+int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, trinv_diag_t diag, void* stream);
+
+/* Diagnostic (bench.py's roofline denominator, not a product path): the FP64 tensor-core
+ * ceiling measured live — a register-only loop of mma.sync m8n8k4 f64 (DMMA.8x8x4, 512
+ * flop per warp instruction) on 2 CTAs x 8 warps per SM, grown until one launch lasts
+ * about ms_target milliseconds — in TFLOP/s at the current clocks.  SYNCHRONISES `stream`.
+ * Returns a negative value on a CUDA error. */
+double trinv_probe_dmma_tflops(double ms_target, void* stream);
 
 /* Static description of a status code. */
 const char* trinv_status_string(trinv_status_t s);
@@ -260,9 +275,9 @@ void trinv_reset_launch_count(void);
  * trinv_profile_end() every kernel this thread enqueues is bracketed by CUDA
  * events recorded on its stream (small overhead; for measurement runs only).
  * trinv_profile_read(kind, ...) synchronises those events and returns, for
- * kind 0 (leaf / batched kernels), 1 (DMMA product kernels), 2 (INT8 product
- * engine: the tensor-core GEMM kernel of the CRT engine, the whole product of the
- * digit engine; bytes = int8 operations) or 3 (the CRT engine's scaling, residue
+ * kind 0 (leaf / batched kernels), 1 (DMMA product kernels), 2 (opt-in INT8
+ * engine: the tensor-core GEMM kernel of the CRT engine; bytes = int8 operations)
+ * or 3 (the CRT engine's scaling, residue
  * and reconstruction kernels; flops = 0), the device milliseconds covered by those
  * launches (the union of their intervals: launches on two streams may overlap), the
  * number of timed scopes and the ALGORITHMIC flops and bytes of those launches

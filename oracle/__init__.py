@@ -14,7 +14,8 @@ import subprocess
 
 import numpy as np
 
-from .metrics import floored_rel_err, residual_ratio, column_residual_ratio  # noqa: F401
+from .metrics import (floored_rel_err, residual_ratio, column_residual_ratio,  # noqa: F401
+                      factored_column_residual_ratio)
 from .hopscotch import hopscotch_series, hopscotch_count  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -50,6 +51,8 @@ def lib():
         L.oracle_columns.argtypes = [ctypes.c_char, _i64, _dp, _i64, ctypes.c_int, _i64, _lp, _dp]
         L.oracle_skul.argtypes = [_i64, _dp, _dp, _dp, _dp, _dp]
         L.oracle_skul.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_lu_columns.argtypes = [_i64, _dp, _i64, ctypes.c_int, _dp, _i64, ctypes.c_int,
                                         _i64, _lp, _dp]
         _lib = L
@@ -142,3 +145,12 @@ def inv_general(A):
     if info:
         raise ZeroDivisionError(f"zero pivot at {info}")
     return S @ K
+
+
+def set_threads(n):
+    """OpenMP thread count of the oracle's loops (timing legs only; results are identical)."""
+    lib().oracle_set_threads(int(n))
+
+
+def max_threads():
+    return int(lib().oracle_max_threads())

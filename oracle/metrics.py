@@ -1,7 +1,8 @@
 """Error metrics used by every parity check (reading C7/C8).
 
 floored relative error: |X - R| / max(|R|, floor * max_i |R_ij| per column j);
-residual ratio: ||T X - I||_F / (||T||_F ||X||_F).  Plain numpy, fp64.
+residual ratio: ||T X - I||_F / (||T||_F ||X||_F); for inverses from factors (reading C21)
+the factored residual ||L (U X_S) - I_S||_F / (||L||_F ||U||_F ||X_S||_F).  Plain numpy, fp64.
 Test infrastructure only.
 """
 import numpy as np
@@ -44,3 +45,15 @@ def column_residual_ratio(T, Xcols, cols):
     E = T @ Xs
     E[np.asarray(cols), np.arange(len(cols))] -= 1.0
     return float(np.linalg.norm(E) / (np.linalg.norm(T) * np.linalg.norm(Xs)))
+
+
+def factored_column_residual_ratio(L, U, Xcols, cols):
+    """rho_LU of reading C21: ||L (U X_S) - I_S||_F / (||L||_F ||U||_F ||X_S||_F) for the
+    sampled columns S of X = (L U)^-1, with the product applied factor by factor (no formed
+    A).  L, U: the factors as full arrays (a unit diagonal stored explicitly);
+    Xcols: [ncols, n] (row c = column cols[c] of X)."""
+    L = np.asarray(L, dtype=np.float64); U = np.asarray(U, dtype=np.float64)
+    Xs = np.asarray(Xcols, dtype=np.float64).T  # n x ncols
+    E = L @ (U @ Xs)
+    E[np.asarray(cols), np.arange(len(cols))] -= 1.0
+    return float(np.linalg.norm(E) / (np.linalg.norm(L) * np.linalg.norm(U) * np.linalg.norm(Xs)))

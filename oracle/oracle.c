@@ -24,6 +24,12 @@
 
 #define AT(M, ld, i, j) ((M)[(int64_t)(i) * (ld) + (j)])
 
+#include <omp.h>
+/* Thread count of the OpenMP loops below (bench.py's 1-thread cpu_baseline figure);
+ * not arithmetic: every routine computes the same bits at any thread count. */
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int oracle_max_threads(void) { return omp_get_max_threads(); }
+
 /* ---------------------------------------------------------------------------
  * CRIT (Algorithm 3) for an upper-triangular R, exactly as listed:
  *   for i = 1..n:  S(i,i) = 1/R(i,i)

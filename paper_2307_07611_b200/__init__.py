@@ -198,9 +198,9 @@ def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", strea
     return C
 
 
-def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", digits=8, stream=None):
-    """C = alpha A B + beta C (FP64) with the products on the INT8 tensor cores: exact operand
-    splitting into `digits` 7-bit digits, or, with digits=0, 16 moduli + CRT (trinv_gemm_oz)."""
+def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", digits=0, stream=None):
+    """C = alpha A B + beta C, FP64-emulated (Ozaki-II) on the INT8 tensor cores: 16 moduli
+    + CRT (trinv_gemm_oz; digits must be 0, the digit-splitting variant was retired)."""
     torch = _torch()
     M, K = A.shape
     N = B.shape[1]
@@ -219,13 +219,14 @@ def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", di
 _MIN_BLOCK = 2048  # the engines' block threshold as last set through set_product_engine
 
 
-def set_product_engine(engine="int8crt", digits=8, min_block=2048):
-    """Engine of the level products: "int8crt" (default: INT8 tensor cores, 16 moduli + CRT,
-    for the levels with block size >= min_block), "int8" (INT8 tensor cores, exact splitting
-    into `digits` 7-bit digits) or "dmma" (FP64 mma.sync for every level)."""
+def set_product_engine(engine="dmma", min_block=2048):
+    """Engine of the level products: "dmma" (default: FP64 mma.sync for every product) or
+    "int8crt" (opt-in, FP64-emulated (Ozaki-II) on the INT8 tensor cores, 16 moduli + CRT,
+    for the levels with block size >= min_block; one host synchronisation per call for its
+    scaling guard)."""
     global _MIN_BLOCK
-    e = {"dmma": 0, "int8": 1, "int8crt": 2}[engine]
-    _check(lib().trinv_set_product_engine(e, digits, min_block))
+    e = {"dmma": 0, "int8crt": 2}[engine]
+    _check(lib().trinv_set_product_engine(e, 0, min_block))
     _MIN_BLOCK = int(min_block)
 
 
@@ -233,18 +234,20 @@ def product_min_block():
     return _MIN_BLOCK
 
 
-def int8_scaling_ok(A, uplo="N", stream=None):
-    """The INT8 engines' scaling guard (trinv_int8_scaling_ok): True when A's row / column
-    maxima span at most 20 binades (only the `uplo` triangle read for "L" / "U")."""
+def int8_scaling_ok(A, uplo="N", unit=False, stream=None):
+    """The INT8 engine's scaling guard (trinv_int8_scaling_ok): True when A's row / column
+    maxima span at most 8 binades and every entry is finite (only the `uplo` triangle read
+    for "L" / "U"); False under stream capture (the guard cannot run)."""
     n = A.shape[-1]
-    r = lib().trinv_int8_scaling_ok(n, ctypes.c_void_p(A.data_ptr()), _ld(A), uplo.encode(), _stream(stream))
+    r = lib().trinv_int8_scaling_ok(n, ctypes.c_void_p(A.data_ptr()), _ld(A), uplo.encode(), int(bool(unit)),
+                                    _stream(stream))
     if r < 0:
         _check(-r)
     return r == 1
 
 
 def product_engine():
-    return ["dmma", "int8", "int8crt"][lib().trinv_get_product_engine()]
+    return {0: "dmma", 2: "int8crt"}[lib().trinv_get_product_engine()]
 
 
 def gemm_strassen(A, B, *, C=None, stream=None):

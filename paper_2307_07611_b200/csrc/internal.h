@@ -112,13 +112,6 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 
-// ---- FP64 products on the INT8 tensor cores by operand splitting (oz.cu) ----------
-bool oz_supported(int64_t M, int64_t N, int64_t K, int s);
-size_t oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int s);
-cudaError_t launch_oz_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
-                           int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, int s, void* ws,
-                           cudaStream_t st, int64_t* launches);
-
 // ---- FP64 products on the INT8 tensor cores by modular arithmetic / CRT (oz2.cu) ----
 bool oz2_supported(int64_t M, int64_t N, int64_t K);
 size_t oz2_workspace_bytes(int64_t M, int64_t N, int64_t K);

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "internal.h"
@@ -240,6 +241,229 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// n = 32 with the off-diagonal block on the FP64 tensor cores (the default for the
+// batched n = 32 path and the 32-wide recursion leaves with an aligned, even layout).
+// The scalar recurrence above reads every T_ik (i > k) once per lane: ~250 16-byte
+// shared broadcasts per matrix, which made leaf32_tma_kernel shared-memory (LSU) bound
+// (ncu: l1tex 96%).  Here the 32x32 matrix is one beta = 2 merge of Alg. 1
+// over two 16-wide diagonal blocks (P:440-452 transposed, = P:1066-1069):
+//   1. half-warp h inverts diagonal block h by the same right-looking recurrence of the
+//      proof of Thm 1, lane c = column c in 16 registers (lower; the upper
+//      case runs CRIT's back substitution, lane c = column c);
+//   2. the off-diagonal block by two 16x16x16 products on DMMA from shared memory:
+//      lower  W = L21 X11 (X11 lower: tile J reads k >= 8 J), X21 = -X22 W (X22 lower:
+//             tile I reads k < 8 I + 8);
+//      upper  W = U12 X22 (X22 upper: k < 8 J + 8), X12 = -X11 W (X11 upper: k >= 8 I);
+//      24 DMMA.8x8x4 per matrix instead of ~250 broadcasts + ~500 FFMA.
+// Staging: the referenced triangle, rows rounded to 16-byte pairs (272 chunks, 4352 B),
+// is copied by per-lane cp.async (LDGSTS, bypassing L1) into a slot with row stride 36
+// doubles (= 4 mod 16: both m8n8k4 fragment patterns bank-conflict free), NS slots per
+// warp, each warp a private ring; the stray element of a pair that falls in the other
+// triangle is never read.  Outputs leave from registers: X11 / X22 rows as two 128-byte
+// segments per store, the zero block as 16-byte stores, the DMMA tile as 16-byte stores.
+constexpr int MS = 36;                  // slot row stride (doubles)
+constexpr int MSLOT = 32 * MS;          // doubles per slot (9216 B)
+constexpr int MCHUNKS = 272;            // 16-byte chunks of the referenced triangle
+constexpr int MCPL = (MCHUNKS + 31) / 32;
+
+__device__ __forceinline__ void cpa16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Pair-chunks of row i: lower c in [0, i/2], upper c in [i/2, 15] (columns 2c, 2c+1).
+template <bool UPPER>
+__device__ __forceinline__ void mchunk(int q, int& i, int& c) {
+  int row = 0, start = 0;
+  for (; row < 32; ++row) {
+    const int cnt = UPPER ? 16 - row / 2 : row / 2 + 1;
+    if (q < start + cnt) break;
+    start += cnt;
+  }
+  i = row;
+  c = (UPPER ? row / 2 : 0) + (q - start);
+}
+
+// Stage 1 step pair for the lower recurrence (k, k+1) and the upper one (k, k-1).
+template <int K>
+__device__ __forceinline__ void m_lower_step(const double* T, double (&x)[16]) {
+  const double xk = x[K] * T[K * (MS + 1)];  // the diagonal slot holds r_K
+  x[K] = xk;
+  x[K + 1] = fma(-T[(K + 1) * MS + K], xk, x[K + 1]);
+  const double xk1 = x[K + 1] * T[(K + 1) * (MS + 1)];
+  x[K + 1] = xk1;
+#pragma unroll
+  for (int i = K + 2; i < 16; ++i) {
+    const double2 t = *reinterpret_cast<const double2*>(T + i * MS + K);
+    x[i] = fma(-t.x, xk, x[i]);
+    x[i] = fma(-t.y, xk1, x[i]);
+  }
+}
+template <int K>
+__device__ __forceinline__ void m_upper_step(const double* T, double (&x)[16]) {  // K odd: rows K, K-1
+  const double xk = x[K] * T[K * (MS + 1)];
+  x[K] = xk;
+  x[K - 1] = fma(-T[(K - 1) * MS + K], xk, x[K - 1]);
+  const double xk1 = x[K - 1] * T[(K - 1) * (MS + 1)];
+  x[K - 1] = xk1;
+#pragma unroll
+  for (int i = 0; i < K - 1; ++i) {
+    const double2 t = *reinterpret_cast<const double2*>(T + i * MS + K - 1);  // (T_i,K-1, T_iK)
+    x[i] = fma(-t.y, xk, x[i]);
+    x[i] = fma(-t.x, xk1, x[i]);
+  }
+}
+template <bool UPPER, int... P>
+__device__ __forceinline__ void m_steps(const double* T, double (&x)[16], std::integer_sequence<int, P...>) {
+  if constexpr (UPPER) (m_upper_step<15 - 2 * P>(T, x), ...);
+  else (m_lower_step<2 * P>(T, x), ...);
+}
+
+// acc[I][J] (8x8 tiles of a 16x16 product) += A[16][16] B[16][16], both in the slot
+// (stride MS), K-steps of 4 restricted by the triangular operand (TRI: 0 = B lower,
+// tile J needs k >= 8J; 1 = A lower, tile I needs k < 8I+8; 2 = B upper, k < 8J+8;
+// 3 = A upper, k >= 8I).
+template <int TRI>
+__device__ __forceinline__ void m_mma16(double (&acc)[2][2][2], const double* A, const double* B, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int k = 0; k < 16; k += 4) {
+    const bool hi = k >= 8;  // second half of the K range
+    double a[2], b[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      a[t] = A[(8 * t + lr) * MS + k + lc];
+      b[t] = B[(k + lc) * MS + 8 * t + lr];
+    }
+#pragma unroll
+    for (int I = 0; I < 2; ++I)
+#pragma unroll
+      for (int J = 0; J < 2; ++J) {
+        const bool need = TRI == 0 ? (hi || J == 0) : TRI == 1 ? (!hi || I == 1)
+                        : TRI == 2 ? (!hi || J == 1) : (hi || I == 0);
+        if (need) dmma_8x8x4(acc[I][J][0], acc[I][J][1], a[I], b[J]);
+      }
+  }
+}
+
+template <bool UPPER, int WARPS, int NS>
+__global__ void __launch_bounds__(WARPS * 32, 1) leaf32_mma_kernel(const LeafArgs a) {
+  extern __shared__ __align__(16) double msmem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* slots = msmem + (size_t)warp * NS * MSLOT;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t TW = (int64_t)gridDim.x * WARPS;
+  if (gw >= a.batch) return;
+  const int64_t count = (a.batch - gw + TW - 1) / TW;
+
+  int soff[MCPL], goff[MCPL];  // this lane's chunks: slot offset, input offset (doubles)
+#pragma unroll
+  for (int m = 0; m < MCPL; ++m) {
+    const int q = lane + 32 * m;
+    int i = 0, c = 0;
+    if (q < MCHUNKS) mchunk<UPPER>(q, i, c);
+    soff[m] = q < MCHUNKS ? i * MS + 2 * c : -1;
+    goff[m] = i * (int)a.lda + 2 * c;
+  }
+  auto issue = [&](int64_t t) {
+    if (t < count) {
+      const double* src = a.A + (gw + t * TW) * a.sA;
+      double* dst = slots + (t % NS) * MSLOT;
+#pragma unroll
+      for (int m = 0; m < MCPL; ++m)
+        if (soff[m] >= 0) cpa16(dst + soff[m], src + goff[m]);
+    }
+    cpa_commit();  // one group per matrix slot, empty past the end (uniform wait counts)
+  };
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) issue(t);
+
+  const int h = lane >> 4, c = lane & 15;
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int64_t t = 0; t < count; ++t) {
+    issue(t + NS - 1);
+    cpa_wait<NS - 1>();
+    __syncwarp();
+    const int64_t b = gw + t * TW;
+    double* S = slots + (t % NS) * MSLOT;
+    double* Th = S + 16 * h * (MS + 1);  // diagonal block h
+    double* dst = a.X + b * a.sX;
+
+    // 1. diagonal blocks (a1, a2): reciprocals, then the recurrence
+    const double d = Th[c * (MS + 1)];
+    const bool zero = (!a.unit) && d == 0.0;
+    const unsigned zmask = __ballot_sync(0xffffffffu, zero);
+    __syncwarp();
+    Th[c * (MS + 1)] = a.unit ? 1.0 : 1.0 / d;  // IEEE division: X_jj == 1/T_jj bitwise (C4)
+    __syncwarp();
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+    m_steps<UPPER>(Th, x, std::make_integer_sequence<int, 8>{});
+    __syncwarp();  // every lane has read its block before it is overwritten by its inverse
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double v = (UPPER ? i > c : i < c) ? 0.0 : x[i];
+      Th[i * MS + c] = v;                                          // operand of step 2
+      dst[(int64_t)(16 * h + i) * a.ldx + 16 * h + c] = v;         // X11 / X22 rows (a7 inside)
+    }
+    // the zero block (a7): lower rows 0..15 x cols 16..31, upper rows 16..31 x cols 0..15
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * q + (lane >> 3), cc = 2 * (lane & 7);
+      *reinterpret_cast<double2*>(dst + (int64_t)(UPPER ? 16 + r : r) * a.ldx + (UPPER ? cc : 16 + cc)) =
+          make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    // 2. the off-diagonal block on DMMA (a5, a6)
+    double acc[2][2][2] = {};
+    double* W = UPPER ? S + 16 * MS : S + 16;  // the unreferenced quadrant
+    if (!UPPER) m_mma16<0>(acc, S + 16 * MS, S, lane);           // W = L21 X11
+    else m_mma16<2>(acc, S + 16, S + 16 * MS + 16, lane);          // W = U12 X22
+#pragma unroll
+    for (int I = 0; I < 2; ++I)
+#pragma unroll
+      for (int J = 0; J < 2; ++J) {
+        *reinterpret_cast<double2*>(W + (8 * I + lr) * MS + 8 * J + 2 * lc) = make_double2(acc[I][J][0], acc[I][J][1]);
+        acc[I][J][0] = acc[I][J][1] = 0.0;
+      }
+    __syncwarp();
+    if (!UPPER) m_mma16<1>(acc, S + 16 * MS + 16, W, lane);       // X21 = -X22 W
+    else m_mma16<3>(acc, S, W, lane);                              // X12 = -X11 W
+    __syncwarp();  // every lane is done with the slot: the next load may overwrite it
+    double* o = dst + (UPPER ? 16 : 16 * a.ldx);
+#pragma unroll
+    for (int I = 0; I < 2; ++I)
+#pragma unroll
+      for (int J = 0; J < 2; ++J)
+        *reinterpret_cast<double2*>(o + (int64_t)(8 * I + lr) * a.ldx + 8 * J + 2 * lc) =
+            make_double2(-acc[I][J][0], -acc[I][J][1]);
+    leaf_report(a, b, lane, zmask != 0, zmask ? __ffs(zmask) - 1 : -1);
+  }
+  cpa_wait<0>();
+}
+
+template <int W, int NS>
+static void launch_mma32(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
+  constexpr size_t smem = (size_t)W * NS * MSLOT * 8;
+  const int64_t ctas_needed = (a.batch + W - 1) / W;
+  const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
+  if (uplo == 'L') {
+    constexpr auto k = leaf32_mma_kernel<false, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(a);
+  } else {
+    constexpr auto k = leaf32_mma_kernel<true, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(a);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Plain-load kernel for any layout (odd n / ld, unaligned pointers): one warp
 // per matrix, rows loaded coalesced into a smem slot, result stored directly.
 template <bool UPPER>
@@ -320,8 +544,23 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   // n = 32, TMA-compatible layout: 8 warps x NS slots per CTA (one CTA per SM), bands of
   // BR rows (profiles/r01_leaf_variants.txt); TRINV_LEAF_BR = 4 / 8 / 16 for experiments
   static const int br = [] { const char* e = std::getenv("TRINV_LEAF_BR"); return e ? std::atoi(e) : 16; }();
+  // n = 32 default: the DMMA-merge kernel (TRINV_LEAF32=band: the scalar TMA-band kernel;
+  // TRINV_LEAF32_CFG = warps x slots per CTA for experiments)
+  static const bool band = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "band"); }();
+  static const int mcfg = [] { const char* e = std::getenv("TRINV_LEAF32_CFG"); return e ? std::atoi(e) : 83; }();
   bool launched = false;
-  if (tma && full32 && a.batch < (int64_t)1 << 31) {
+  if (!band && tma && full32 && a.lda * 32 < ((int64_t)1 << 31)) {
+    switch (mcfg) {
+      case 122: launch_mma32<12, 2>(uplo, a, sms, s); break;
+      case 64: launch_mma32<6, 4>(uplo, a, sms, s); break;
+      case 62: launch_mma32<6, 2>(uplo, a, sms, s); break;
+      case 42: launch_mma32<4, 2>(uplo, a, sms, s); break;
+      case 82: launch_mma32<8, 2>(uplo, a, sms, s); break;
+      default: launch_mma32<8, 3>(uplo, a, sms, s); break;
+    }
+    launched = true;
+  }
+  if (!launched && tma && full32 && a.batch < (int64_t)1 << 31) {
     if (br == 16) launched = launch_band<8, 3, 16>(uplo, a, sms, s);
     else if (br == 8) launched = launch_band<8, 4, 8>(uplo, a, sms, s);
     else launched = launch_band<8, 4, 4>(uplo, a, sms, s);

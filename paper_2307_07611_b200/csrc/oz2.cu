@@ -67,11 +67,21 @@ __host__ __device__ constexpr int oz2_inv(int a, int m) {  // a^-1 mod m (a, m c
 }
 
 // ---- residues of the scaled operands ------------------------------------------------
+// A row / column holding a NaN or Inf gets the exponent OZ2_NONFINITE: its entries are
+// split as zeros and the reconstruction writes NaN over that row / column of the product
+// (an FP64 product would carry NaN / Inf there: NaN x 0 and Inf x 0 are NaN).
+constexpr int OZ2_NONFINITE = 1 << 20;
 __device__ __forceinline__ int oz2_exp_above(double m) {
   if (m == 0.0) return 0;
+  if (!(m <= 1.7976931348623157e308)) return OZ2_NONFINITE;  // NaN or Inf
   int e;
   frexp(m, &e);
   return e;
+}
+// maximum of magnitudes that propagates NaN (fmax drops it)
+__device__ __forceinline__ double oz2_amax(double m, double x) {
+  const double a = fabs(x);
+  return (a > m || a != a) ? a : m;
 }
 // x 2^k: one multiplication by an exact power of two in the normal range (exact unless
 // the result is subnormal, then one rounding, as ldexp), else ldexp.
@@ -144,15 +154,15 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
 #pragma unroll 4
     for (int k = kb + 2 * lane; k < ke; k += 64) {
       const double2 x = *reinterpret_cast<const double2*>(a + k);
-      m = k == kz ? m : fmax(m, fabs(x.x));
-      m1 = k + 1 == kz ? m1 : fmax(m1, fabs(x.y));
+      m = k == kz ? m : oz2_amax(m, x.x);
+      m1 = k + 1 == kz ? m1 : oz2_amax(m1, x.y);
     }
-    m = fmax(m, m1);
+    m = oz2_amax(m, m1);
   } else {
 #pragma unroll 4
-    for (int k = kb + lane; k < ke; k += 32) m = k == kz ? m : fmax(m, fabs(a[k]));
+    for (int k = kb + lane; k < ke; k += 32) m = k == kz ? m : oz2_amax(m, a[k]);
   }
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o; o >>= 1) m = oz2_amax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = oz2_exp_above(m);
   if (lane == 0) expo[warp] = e;
   const size_t sw = (size_t)rows * K / 4;  // plane stride in 32-bit words
@@ -168,7 +178,8 @@ __global__ void oz2_split_rows_kernel(const double* A, int64_t lda, int rows, in
     }
     int64_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = k + q == kz ? 0 : (int64_t)oz2_ldexp(x[q], P - e);  // exact, truncated
+    for (int q = 0; q < 4; ++q)  // exact, truncated (a non-finite row is split as zeros)
+      v[q] = (k + q == kz || e == OZ2_NONFINITE) ? 0 : (int64_t)oz2_ldexp(x[q], P - e);
     oz2_residues4<false>(v, o + k / 4, sw, std::make_integer_sequence<int, OZ2_NMOD>{});  // uint8 residues
   }
 }
@@ -188,9 +199,9 @@ __global__ void oz2_colmax_kernel(const double* B, int64_t ldb, int K, int cols,
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = b[(int64_t)(k + u) * ldb];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) m = k + u == kz ? m : fmax(m, fabs(x[u]));
+    for (int u = 0; u < 8; ++u) m = k + u == kz ? m : oz2_amax(m, x[u]);
   }
-  for (; k < k1; ++k) m = k == kz ? m : fmax(m, fabs(b[(int64_t)k * ldb]));
+  for (; k < k1; ++k) m = k == kz ? m : oz2_amax(m, b[(int64_t)k * ldb]);
   if (k0 < k1) atomicMax(&maxbits[j], (unsigned long long)__double_as_longlong(m));
 }
 // B operand (K x cols): residues written transposed (cols x K, K-major) through a
@@ -211,8 +222,9 @@ __global__ void __launch_bounds__(256, 8) oz2_split_cols_kernel(const double* B,
   if (k0 + 32 <= kb || k0 >= ke) return;
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r;
-    tile[r][tx] = (k < K && jx < cols && !(strict && k == jx)) ? (long long)oz2_ldexp(B[(int64_t)k * ldb + jx], P - e)
-                                                              : 0;
+    tile[r][tx] = (k < K && jx < cols && !(strict && k == jx) && e != OZ2_NONFINITE)
+                      ? (long long)oz2_ldexp(B[(int64_t)k * ldb + jx], P - e)
+                      : 0;
   }
   __syncthreads();
   const int j = j0 + (threadIdx.x >> 3), kq = 4 * (threadIdx.x & 7), k = k0 + kq;
@@ -650,7 +662,9 @@ __global__ void oz2_reconstruct_kernel(const uint8_t* R, int M, int N, const int
     const uint64_t b1 = a1[b] + (a0[b] >> 32), b2 = a2[b] + (b1 >> 32);
     const int64_t hi = (int64_t)(((uint64_t)(uint32_t)b2 << 32) | (uint32_t)b1);  // top 64 of 96 bits, signed
     const double frac96 = fma((double)hi, 4294967296.0, (double)(uint32_t)a0[b]);  // fraction * 2^96
-    const double val = oz2_ldexp(frac96 * crt.Md96, ei + eb[j + b]);
+    const bool nonfinite = ea[i] == OZ2_NONFINITE || eb[j + b] == OZ2_NONFINITE;
+    const double val =
+        nonfinite ? __longlong_as_double(0x7ff8000000000000ll) : oz2_ldexp(frac96 * crt.Md96, ei + eb[j + b]);
     out[b] = beta == 0.0 ? alpha * val : fma(alpha, val, beta * out[b]);
   }
 }

@@ -106,44 +106,48 @@ static int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ---- product engine for the level products (trinv_set_product_engine) ---------------
-// 0: FP64 DMMA (mma.sync, gemm.cu); 1: INT8 tensor cores, exact 8-digit splitting
-// (oz.cu); 2 (default): INT8 tensor cores, 16 moduli + CRT (oz2.cu).  Engines 1/2
-// take the levels whose block size is >= g_oz_min and whose shapes fit their
-// envelope; every other level runs on DMMA.  TRINV_PRODUCTS=dmma|int8|int8crt
-// overrides the default before the first call.
+// 0 (default): FP64 DMMA (mma.sync, gemm.cu) for every product — the engine BJ.north_star
+// names for a5/a6.  2 (opt-in): FP64-emulated products on the INT8 tensor cores (Ozaki-II:
+// 16 moduli + CRT, oz2.cu) for the levels whose block size is >= g_oz_min and whose shapes
+// fit its envelope; every other level stays on DMMA.  TRINV_PRODUCTS=int8crt selects it
+// before the first call.  (Engine 1, the digit-splitting variant, was retired.)
 static std::atomic<int> g_engine{-1};
-static std::atomic<int> g_digits{8};
 static std::atomic<int64_t> g_oz_min{2048};  // tools/minblock_probe.py: 2048 beats 1024 / 4096
 static int product_engine() {
   int e = g_engine.load(std::memory_order_relaxed);
   if (e < 0) {
     const char* v = getenv("TRINV_PRODUCTS");
-    e = 2;
-    if (v && strcmp(v, "dmma") == 0) e = 0;
-    if (v && strcmp(v, "int8") == 0) e = 1;
+    e = (v && strcmp(v, "int8crt") == 0) ? 2 : 0;
     g_engine.store(e, std::memory_order_relaxed);
   }
   return e;
 }
 
-// ---- scaling guard of the INT8 engines ---------------------------------------------------
-// The INT8 engines truncate their operands relative to row / column maxima, so inputs whose
+// ---- scaling guard of the opt-in INT8 engine -----------------------------------------------
+// The INT8 engine truncates its operands relative to row / column maxima, so inputs whose
 // rows or columns span many binades lose accuracy there (1.2e-10 at a
 // 2^+-16 row / column scaling, 9e-4 beyond 2^+-30) while the DMMA path is exactly scaling
-// invariant.  Before a call that would use them, the spread of the row-maximum exponents
-// and of the column-maximum exponents of the input is estimated on every 17th row; above
-// OZ_MAX_SPREAD binades the call runs every product on DMMA.  Skipped under stream
-// capture (it needs one 16-byte device-to-host read).
-constexpr int OZ_MAX_SPREAD = 20;
-constexpr int SPREAD_STRIDE = 17;   // rows sampled (odd: periodic row scalings with even period are seen)
-constexpr int SPREAD_GROUPS = 8;    // row groups of the column pass
-// Per call: the check kernels run first on the call's stream and copy their 4 exponents
-// per checked matrix to pinned host memory behind an event; the decision is taken (event
+// invariant.  Before a call that would use it, the exact spread of the row-maximum
+// exponents and of the column-maximum exponents of the input's referenced entries is
+// computed on the device (one read of the referenced part for the rows, one for the
+// columns; with a unit diagonal the stored diagonal is skipped and the implicit 1 enters
+// both maxima); above OZ_MAX_SPREAD (8) binades, or when any referenced entry is NaN / Inf,
+// the call runs every product on DMMA (which propagates non-finite values).  The decision
+// needs the result on the host: the opt-in engine synchronises on one event per call (the
+// default DMMA engine never does).  Under stream capture the guard cannot run, so a
+// captured call always uses DMMA.
+// 8 binades: the engine's floored elementwise error measured ~1.3e-14 x 2^spread on row-scaled
+// BASELINE inputs (tests/test_gpu_scaling.py: 3.5e-9 at 18, 3.4e-8 at 20 binades, above the
+// 1e-10 gate), so 8 keeps a 30x margin; BASELINE inputs have spread 0.
+constexpr int OZ_MAX_SPREAD = 8;
+constexpr int SPREAD_ROWS = 256;  // rows per block of the column pass
+// Per call: the check kernels run first on the call's stream and copy their 5 ints per
+// checked matrix to pinned host memory behind an event; the decision is taken (event
 // synchronize) only when the first INT8-eligible product is reached, so the host waits
-// while the GPU works through the leaves and the small DMMA levels: no pipeline bubble.
+// while the GPU works through the leaves and the small DMMA levels.
 struct ScaleCheck {
-  int* dev = nullptr;        // [2 matrices][4] exponents + [n] column maxima bits follow
-  int* host = nullptr;       // pinned [8]
+  int* dev = nullptr;        // [2 matrices][8] ints, then [2][n] column-maximum bits
+  int* host = nullptr;       // pinned [16]
   cudaEvent_t ev = nullptr;
   int nmat = 0;              // matrices checked in this call
   bool pending = false;
@@ -178,80 +182,98 @@ __device__ __forceinline__ int spread_exp(double m) {
   frexp(m, &e);
   return e;
 }
+// NaN-propagating maximum of magnitudes: as unsigned bit patterns, +NaN > +Inf > finite
+__device__ __forceinline__ double spread_max(double m, double x) {
+  const double a = fabs(x);
+  return (a > m || a != a) ? a : m;
+}
+// r: [0] min row exponent, [1] max, [2] min column exponent, [3] max, [4] non-finite seen
 __global__ void spread_init_kernel(int* r, unsigned long long* cmax, int n) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) cmax[j] = 0ull;
-  if (j == 0) { r[0] = r[2] = 1 << 30; r[1] = r[3] = -(1 << 30); }
+  if (j == 0) { r[0] = r[2] = 1 << 30; r[1] = r[3] = -(1 << 30); r[4] = 0; }
 }
-// row maxima of rows 0, 16, 32, ... over their referenced part (uplo 'L' / 'U' / 'N')
-__global__ void spread_rows_kernel(const double* A, int64_t lda, int n, char uplo, int* r) {
+__device__ __forceinline__ void spread_note(int* r, int lo, int hi, double m) {
+  if (!(m <= 1.7976931348623157e308)) { atomicOr(&r[4], 1); return; }  // NaN or Inf
+  if (m > 0.0) {
+    const int e = spread_exp(m);
+    atomicMin(&r[lo], e);
+    atomicMax(&r[hi], e);
+  }
+}
+// row maxima over the referenced part of every row (uplo 'L' / 'U' / 'N'; unit: the stored
+// diagonal is skipped and the implicit 1 counted): one block per row
+__global__ void spread_rows_kernel(const double* A, int64_t lda, int n, char uplo, int unit, int* r) {
   __shared__ double red[8];
-  const int i = blockIdx.x * SPREAD_STRIDE;
+  const int i = blockIdx.x;
   const int j0 = uplo == 'U' ? i : 0, j1 = uplo == 'L' ? i + 1 : n;
-  double m = 0.0;
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) m = fmax(m, fabs(A[(int64_t)i * lda + j]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  double m = unit ? 1.0 : 0.0;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x)
+    if (!(unit && j == i)) m = spread_max(m, A[(int64_t)i * lda + j]);
+  for (int o = 16; o; o >>= 1) m = spread_max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
-    if (m > 0.0 && m <= 1.7976931348623157e308) {
-      const int e = spread_exp(m);
-      atomicMin(&r[0], e);
-      atomicMax(&r[1], e);
-    }
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = spread_max(m, red[w]);
+    spread_note(r, 0, 1, m);
   }
 }
-// column maxima over the sampled rows and the column's diagonal entry (a triangular
-// column near the triangle's edge has few sampled rows; its diagonal, non-zero for an
-// invertible factor, anchors the estimate): thread per column, SPREAD_GROUPS row groups
-__global__ void spread_cols_kernel(const double* A, int64_t lda, int n, char uplo, unsigned long long* cmax) {
+// column maxima: thread per column over SPREAD_ROWS rows of its block (blockIdx.y), all
+// referenced rows of the column across the grid; combined by an atomic max on the bits
+__global__ void spread_cols_kernel(const double* A, int64_t lda, int n, char uplo, int unit, unsigned long long* cmax) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * SPREAD_ROWS, i1 = min(n, i0 + SPREAD_ROWS);
   if (j >= n) return;
-  double m = blockIdx.y == 0 ? fabs(A[(int64_t)j * lda + j]) : 0.0;
+  int lo = i0, hi = i1;  // referenced rows of column j: lower i >= j, upper i <= j
+  if (uplo == 'L') lo = max(lo, j);
+  if (uplo == 'U') hi = min(hi, j + 1);
+  double m = (unit && j >= i0 && j < i1) ? 1.0 : 0.0;
 #pragma unroll 4
-  for (int i = blockIdx.y * SPREAD_STRIDE; i < n; i += SPREAD_GROUPS * SPREAD_STRIDE)
-    if ((uplo == 'L' && j <= i) || (uplo == 'U' && j >= i) || uplo == 'N') m = fmax(m, fabs(A[(int64_t)i * lda + j]));
-  if (m > 0.0) atomicMax(&cmax[j], (unsigned long long)__double_as_longlong(m));
+  for (int i = lo; i < hi; ++i)
+    if (!(unit && i == j)) m = spread_max(m, A[(int64_t)i * lda + j]);
+  if (m != 0.0) atomicMax(&cmax[j], (unsigned long long)__double_as_longlong(m));
 }
 __global__ void spread_colred_kernel(const unsigned long long* cmax, int n, int* r) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  const double m = __longlong_as_double((long long)cmax[j]);
-  if (m > 0.0 && m <= 1.7976931348623157e308) {
-    const int e = spread_exp(m);
-    atomicMin(&r[2], e);
-    atomicMax(&r[3], e);
-  }
+  spread_note(r, 2, 3, __longlong_as_double((long long)cmax[j]));
 }
-// launch the check of one input matrix of the current call (no-op under stream capture)
-static void int8_check_begin(const double* A, int64_t lda, int64_t n, char uplo, cudaStream_t s) {
+// launch the check of one input matrix of the current call (under stream capture: veto)
+static void int8_check_begin(const double* A, int64_t lda, int64_t n, char uplo, int unit, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    g_int8_veto = true;
+    return;
+  }
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) { g_int8_veto = true; return; }
   ScaleCheck& c = g_check[dev];
   static thread_local int64_t cap[64] = {};
+  // one-time per thread and device: the pinned result slot; the device scratch grows with n
   if (!c.host) {
-    if (cudaMallocHost(&c.host, 8 * sizeof(int)) != cudaSuccess) { c.host = nullptr; return; }
-    if (cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming) != cudaSuccess) return;
+    if (cudaMallocHost(&c.host, 16 * sizeof(int)) != cudaSuccess) { c.host = nullptr; g_int8_veto = true; return; }
+    if (cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming) != cudaSuccess) { g_int8_veto = true; return; }
   }
-  if (cap[dev] < n) {  // [8 ints | 2 x n column maxima]
+  if (cap[dev] < n) {  // [16 ints | 2 x n column maxima]
     if (c.dev) cudaFree(c.dev);
-    if (cudaMalloc(&c.dev, 256 + 2 * (size_t)n * 8) != cudaSuccess) { c.dev = nullptr; cap[dev] = 0; return; }
+    if (cudaMalloc(&c.dev, 256 + 2 * (size_t)n * 8) != cudaSuccess) {
+      c.dev = nullptr; cap[dev] = 0; g_int8_veto = true; return;
+    }
     cap[dev] = n;
   }
   if (g_pending != &c) { c.nmat = 0; c.pending = true; g_pending = &c; }
   if (c.nmat >= 2) return;
-  int* r = c.dev + 4 * c.nmat;
+  int* r = c.dev + 8 * c.nmat;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c.dev) + 256) + c.nmat * n;
-  spread_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(r, cmax, (int)n);
-  spread_rows_kernel<<<(unsigned)((n + SPREAD_STRIDE - 1) / SPREAD_STRIDE), 256, 0, s>>>(A, lda, (int)n, uplo, r);
-  spread_cols_kernel<<<dim3((unsigned)((n + 255) / 256), SPREAD_GROUPS), 256, 0, s>>>(A, lda, (int)n, uplo, cmax);
-  spread_colred_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cmax, (int)n, r);
+  const unsigned cb = (unsigned)((n + 255) / 256);
+  spread_init_kernel<<<cb, 256, 0, s>>>(r, cmax, (int)n);
+  spread_rows_kernel<<<(unsigned)n, 256, 0, s>>>(A, lda, (int)n, uplo, unit, r);
+  spread_cols_kernel<<<dim3(cb, (unsigned)((n + SPREAD_ROWS - 1) / SPREAD_ROWS)), 256, 0, s>>>(A, lda, (int)n, uplo,
+                                                                                                unit, cmax);
+  spread_colred_kernel<<<cb, 256, 0, s>>>(cmax, (int)n, r);
   g_launches += 4;
   ++c.nmat;
-  cudaMemcpyAsync(c.host, c.dev, 4 * c.nmat * sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(c.host, c.dev, 8 * c.nmat * sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaEventRecord(c.ev, s);
 }
 // the veto for the current call: resolves a pending check (waits for its event only)
@@ -261,10 +283,12 @@ static bool int8_veto() {
     c.pending = false;
     if (cudaEventSynchronize(c.ev) == cudaSuccess) {
       for (int m = 0; m < c.nmat; ++m) {
-        const int* h = c.host + 4 * m;
+        const int* h = c.host + 8 * m;
         const int sr = h[1] >= h[0] ? h[1] - h[0] : 0, sc = h[3] >= h[2] ? h[3] - h[2] : 0;
-        if (std::max(sr, sc) > OZ_MAX_SPREAD) g_int8_veto = true;
+        if (std::max(sr, sc) > OZ_MAX_SPREAD || h[4] != 0) g_int8_veto = true;
       }
+    } else {
+      g_int8_veto = true;
     }
   }
   return g_int8_veto;
@@ -286,17 +310,11 @@ static size_t mat_bytes(int64_t n) { return (size_t)n * (size_t)even_up(n) * siz
 // INT8 engine: a level takes it when every merge's two products fit the envelope
 // (lower: r x b x b and r x b x r; upper: b x r x b and b x r x r); its scratch is the
 // largest of those products' workspaces.
-static bool oz_shape_ok(int64_t M, int64_t N, int64_t K) {
-  return product_engine() == 2 ? oz2_supported(M, N, K) : oz_supported(M, N, K, g_digits.load());
-}
-static size_t oz_shape_ws(int64_t M, int64_t N, int64_t K) {
-  return product_engine() == 2 ? oz2_workspace_bytes(M, N, K) : oz_workspace_bytes(M, N, K, g_digits.load());
-}
+static bool oz_shape_ok(int64_t M, int64_t N, int64_t K) { return oz2_supported(M, N, K); }
+static size_t oz_shape_ws(int64_t M, int64_t N, int64_t K) { return oz2_workspace_bytes(M, N, K); }
 static cudaError_t oz_product(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
                               int64_t ldb, int triB, double* C, int64_t ldc, double alpha, void* ws, cudaStream_t s) {
-  if (product_engine() == 2)
-    return launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, 0.0, ws, s, &g_launches);
-  return launch_oz_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, 0.0, g_digits.load(), ws, s, &g_launches);
+  return launch_oz2_gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, 0.0, ws, s, &g_launches);
 }
 static bool oz_level_ok(int64_t n, int64_t b) {
   if (product_engine() == 0 || b < g_oz_min.load() || b % 256) return false;
@@ -359,7 +377,7 @@ static size_t oz_scratch(int64_t n) {
   size_t best = 0;
   for (int64_t b = BLK_MAX; b < n; b *= 2)
     if (oz_level_ok(n, b))
-      best = std::max(best, (merges_at(n, b) > 1 || product_engine() == 2 ? 2 : 1) * oz_level_scratch(n, b));
+      best = std::max(best, 2 * oz_level_scratch(n, b));
   return best;
 }
 
@@ -468,7 +486,7 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
         TRY(fork_ctx(&fc));
         TRY(fork_to(fc, s));
       }
-      if (!two && product_engine() == 2) {
+      if (!two) {
         // one merge: the second product's inverse-block operand (B^-1 rows for the lower
         // case, C^-1 columns for the upper) is split on the second stream during the first
         // product; the second product then runs in the second scratch with that split done
@@ -547,7 +565,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   if (ws_bytes < need || (need > 0 && ws == nullptr)) return TRINV_WORKSPACE_TOO_SMALL;
   // public entries check the input's scaling for the INT8 engines; internal calls inherit
   Int8Scope scope(init_info);
-  if (init_info && int8_would_run(n)) int8_check_begin(A, lda, n, uplo, s);
+  if (init_info && int8_would_run(n)) int8_check_begin(A, lda, n, uplo, diag, s);
   if (init_info && info) TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (n <= BLK_MAX) return run_tri(uplo, n, A, lda, X, ldx, diag, nullptr, info, info_off, s);
 
@@ -832,8 +850,8 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
   Int8Scope scope(true);
   if (int8_would_run(n) || ul_on_int8(n)) {
-    int8_check_begin(Lf, ldl, n, 'L', s);
-    int8_check_begin(Uf, ldu, n, 'U', s);
+    int8_check_begin(Lf, ldl, n, 'L', (int)diagL, s);
+    int8_check_begin(Uf, ldu, n, 'U', (int)diagU, s);
   }
   char* p = static_cast<char*>(ws);
   double* Ui = reinterpret_cast<double*>(p); p += align_up(mat_bytes(n));
@@ -1000,7 +1018,7 @@ trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int
   cudaStream_t s = (cudaStream_t)stream;
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   Int8Scope scope(true);
-  if (int8_would_run(n)) int8_check_begin(A, lda, n, uplo, s);
+  if (int8_would_run(n)) int8_check_begin(A, lda, n, uplo, (int)diag, s);
   return run_tri_beta4(uplo, n, A, lda, X, ldx, (int)diag, static_cast<char*>(ws), d_info, s);
 }
 
@@ -1112,7 +1130,7 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   const size_t need = trinv_workspace_bytes('A', n, A, lda, X, ldx);
   if (ws_bytes < need || !ws) return TRINV_WORKSPACE_TOO_SMALL;
   Int8Scope scope(true);
-  if (lu_oz_ws(n) > 0 || ul_on_int8(n)) int8_check_begin(A, lda, n, 'N', s);
+  if (lu_oz_ws(n) > 0 || ul_on_int8(n)) int8_check_begin(A, lda, n, 'N', 0, s);
   const int64_t lde = even_up(n);
   // workspace: [F packed factors | W working copy of A | K = L^{-1} | S = U^{-1} | T | X staging]
   char* p = static_cast<char*>(ws);
@@ -1147,37 +1165,31 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
 }
 
 size_t trinv_gemm_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int digits) {
-  if (digits <= 0) return oz2_supported(M, N, K) ? oz2_workspace_bytes(M, N, K) : 0;
-  return oz_supported(M, N, K, digits) ? oz_workspace_bytes(M, N, K, digits) : 0;
+  if (digits > 0) return 0;  // the digit-splitting variant was retired
+  return oz2_supported(M, N, K) ? oz2_workspace_bytes(M, N, K) : 0;
 }
 
 trinv_status_t trinv_gemm_oz(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                              char structA, const double* B, int64_t ldb, char structB, double beta, double* C,
                              int64_t ldc, int digits, void* ws, size_t ws_bytes, void* stream) {
-  if (M < 0 || N < 0 || K < 0 || digits > 10) return TRINV_INVALID_ARG;
+  if (M < 0 || N < 0 || K < 0) return TRINV_INVALID_ARG;
+  if (digits > 0) return TRINV_NOT_SUPPORTED;  // the digit-splitting variant was retired
   if (M == 0 || N == 0) return TRINV_OK;
   auto tri = [](char c) { return c == 'L' ? TRI_LOWER : (c == 'U' ? TRI_UPPER : (c == 'N' ? TRI_NONE : -1)); };
   const int ta = tri(structA), tb = tri(structB);
   if (ta < 0 || tb < 0) return TRINV_INVALID_ARG;
-  // two triangular operands: only upper x lower on the modular variant (k >= max(i, j))
-  if (ta != TRI_NONE && tb != TRI_NONE && !(digits <= 0 && ta == TRI_UPPER && tb == TRI_LOWER))
-    return TRINV_INVALID_ARG;
+  // two triangular operands: only upper x lower (k >= max(i, j))
+  if (ta != TRI_NONE && tb != TRI_NONE && !(ta == TRI_UPPER && tb == TRI_LOWER)) return TRINV_INVALID_ARG;
   if (!A || !B || !C || lda < K || ldb < N || ldc < N) return TRINV_INVALID_ARG;
-  if (digits <= 0) {  // CRT scheme, 16 moduli (oz2.cu)
-    if (!oz2_supported(M, N, K)) return TRINV_NOT_SUPPORTED;
-    if (!ws || ws_bytes < oz2_workspace_bytes(M, N, K)) return TRINV_WORKSPACE_TOO_SMALL;
-    return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, ws, (cudaStream_t)stream,
-                                     &g_launches));
-  }
-  if (!oz_supported(M, N, K, digits)) return TRINV_NOT_SUPPORTED;
-  if (!ws || ws_bytes < oz_workspace_bytes(M, N, K, digits)) return TRINV_WORKSPACE_TOO_SMALL;
-  return cuda_fail(launch_oz_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, digits, ws,
-                                  (cudaStream_t)stream, &g_launches));
+  if (!oz2_supported(M, N, K)) return TRINV_NOT_SUPPORTED;
+  if (!ws || ws_bytes < oz2_workspace_bytes(M, N, K)) return TRINV_WORKSPACE_TOO_SMALL;
+  return cuda_fail(launch_oz2_gemm(M, N, K, A, lda, ta, B, ldb, tb, C, ldc, alpha, beta, ws, (cudaStream_t)stream,
+                                   &g_launches));
 }
 
 trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_block) {
-  if (engine < 0 || engine > 2 || digits < 1 || digits > 10 || min_block < 256) return TRINV_INVALID_ARG;
-  g_digits.store(digits);
+  (void)digits;
+  if ((engine != 0 && engine != 2) || min_block < 256) return TRINV_INVALID_ARG;
   g_oz_min.store(min_block);
   g_engine.store(engine);
   return TRINV_OK;
@@ -1185,11 +1197,12 @@ trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_bloc
 
 int trinv_get_product_engine(void) { return product_engine(); }
 
-int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, void* stream) {
+int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, trinv_diag_t diag, void* stream) {
   if (n <= 0 || !A || lda < n || (uplo != 'L' && uplo != 'U' && uplo != 'N')) return -(int)TRINV_INVALID_ARG;
+  if (diag != TRINV_UNIT && diag != TRINV_NON_UNIT) return -(int)TRINV_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   Int8Scope scope(true);
-  int8_check_begin(A, lda, n, uplo, s);
+  int8_check_begin(A, lda, n, uplo, uplo == 'N' ? 0 : (int)diag, s);
   const bool veto = int8_veto();
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_last_cuda_error = (int)e; return -(int)TRINV_CUDA_ERROR; }

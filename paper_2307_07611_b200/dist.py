@@ -105,9 +105,9 @@ def panel_owner_map(world):
 
 
 def _int8_panels(T, uplo):
-    """Whether the panel products may use the INT8 CRT engine: the library's default
-    engine is in use and the input passes its scaling guard (same decision on every rank:
-    every rank holds T)."""
+    """Whether the panel products may use the INT8 CRT engine: that opt-in engine is
+    selected and the input passes its scaling guard (same decision on every rank: every
+    rank holds T)."""
     from . import int8_scaling_ok, product_engine
     return product_engine() == "int8crt" and int8_scaling_ok(T, uplo)
 

@@ -60,15 +60,17 @@ def test_workspace_sizes():
     ws = P.lib().trinv_workspace_bytes
     assert ws(b"L", 64, None, 64, None, 64) == 0
     n = 32768
-    P.set_product_engine("dmma")
+    P.set_product_engine()  # default: DMMA for every product
+    assert P.product_engine() == "dmma"
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
     try:
-        assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
-        P.set_product_engine()  # default: INT8 CRT engine for blocks >= 2048 adds its residue scratch
+        P.set_product_engine("int8crt")  # opt-in INT8 CRT engine for blocks >= 2048 adds its residue scratch
         h = n // 2
         assert ws(b"L", n, None, n, None, n) >= h * h * 8 + 16 * 3 * h * h
         assert P.product_engine() == "int8crt"
     finally:
         P.set_product_engine()
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8
     assert ws(b"U", 1000, None, 1000, None, 1000) > 0
     # odd leading dimensions stage through the workspace
     assert ws(b"L", 999, None, 999, None, 999) > ws(b"L", 999, None, 1000, None, 1000)

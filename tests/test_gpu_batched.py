@@ -48,9 +48,9 @@ def test_orders_and_uplo(n, uplo):
     assert np.all(opp == 0.0)
 
 
-@pytest.mark.parametrize("uplo", ["L", "U"])
-def test_unit_ignores_diag_and_nan_other_triangle(uplo):
-    B, n = 1000, 32 if uplo == "L" else 48
+@pytest.mark.parametrize("uplo,n", [("L", 32), ("U", 32), ("U", 48), ("L", 64)])
+def test_unit_ignores_diag_and_nan_other_triangle(uplo, n):
+    B = 1000
     A = synth.host(n, batch=B, uplo=uplo)
     A1 = A.copy()
     idx = np.arange(n)

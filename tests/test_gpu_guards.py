@@ -97,10 +97,10 @@ def test_gemm_writes_stay_inside(M, N, K):
     _assert_guards(buf, _inside_mask(M, N, ld, buf.numel()))
 
 
-@pytest.mark.parametrize("engine", ["int8crt", "int8"])
+@pytest.mark.parametrize("engine", ["int8crt"])
 @pytest.mark.parametrize("n,uplo", [(1024, "L"), (1536, "U"), (2048, "L")])
 def test_int8_engine_writes_stay_inside(engine, n, uplo):
-    """The INT8 engines' kernels (residue splits into the workspace, the tensor-core GEMM,
+    """The INT8 engine's kernels (residue splits into the workspace, the tensor-core GEMM,
     the reconstruction into X) inside the recursion, with the block threshold lowered so
     they carry the 512 / 1024 levels: X in a padded, guarded buffer."""
     P.set_product_engine(engine, min_block=256)

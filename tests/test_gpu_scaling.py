@@ -6,9 +6,10 @@ INT8 CRT engine truncates its operands to P-bit integers relative to row / colum
 so scalings that differ along the product's K dimension change which entries survive: its
 error grows with the spread of the scaling (tools/scaling_probe.py: 2.9e-15 at |k| <= 8,
 1.2e-10 at |k| <= 16, 9e-4 at |k| >= 30); the test holds it to 1e-12 at
-|k| <= 8.  Above a 2^20 spread of the input's row / column maxima the library runs every
-product on DMMA (the scaling guard), which makes the default engine exactly invariant
-there too."""
+|k| <= 4 (a spread within the guard's 8 binades).  Above a 2^OZ_MAX_SPREAD spread of the input's row / column maxima (or with a
+non-finite entry) the library runs every product on DMMA (the scaling guard, exact over all
+referenced entries), which makes the INT8 engine exactly invariant there too.  The default
+engine is DMMA."""
 import numpy as np
 import pytest
 
@@ -20,7 +21,7 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
-@pytest.mark.parametrize("engine,R", [("dmma", 60), ("int8crt", 8)])
+@pytest.mark.parametrize("engine,R", [("dmma", 60), ("int8crt", 4)])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_pow2_scaling_invariance(engine, R, uplo):
     n = 1024
@@ -44,7 +45,7 @@ def test_pow2_scaling_invariance(engine, R, uplo):
         P.set_product_engine()
 
 
-@pytest.mark.parametrize("engine,R", [("dmma", 40), ("int8crt", 8)])
+@pytest.mark.parametrize("engine,R", [("dmma", 40), ("int8crt", 4)])
 def test_pow2_scaling_invariance_inv_from_lu(engine, R):
     n = 1024
     P.set_product_engine(engine, min_block=256)
@@ -73,8 +74,8 @@ def test_pow2_scaling_invariance_inv_from_lu(engine, R):
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
 def test_scaling_guard_falls_back_to_dmma(uplo):
-    """Default engine on a 2^+-60 scaled input: the guard sends every product to DMMA, so
-    the result is bit-for-bit the DMMA result (and scaling invariant)."""
+    """INT8 engine on a 2^+-60 scaled input: the guard sends every product to DMMA, so the
+    result is bit-for-bit the DMMA result (and scaling invariant)."""
     n = 1024
     rng = np.random.default_rng(13)
     k1 = rng.integers(-60, 61, n); k2 = rng.integers(-60, 61, n)
@@ -108,8 +109,8 @@ def test_scaling_guard_keeps_int8_on_well_scaled_input():
 
 
 def test_scaling_guard_sees_alternating_rows():
-    """Rows scaled by 2^40 in alternation (a period-2 pattern) are seen by the sampled
-    check (odd sampling stride)."""
+    """Rows scaled by 2^40 in alternation (a period-2 pattern), and a single scaled row or
+    column anywhere, are seen by the guard (it reads every referenced entry)."""
     n = 4096
     T = torch.empty((n, n), dtype=torch.float64, device=DEV)
     synth.device_fill(T, n, diag="signed")
@@ -119,6 +120,12 @@ def test_scaling_guard_sees_alternating_rows():
     U = torch.triu(torch.ones((n, n), dtype=torch.float64, device=DEV))
     U[:, ::3] *= 2.0 ** -30  # column scaling
     assert not P.int8_scaling_ok(U, "U")
+    synth.device_fill(T, n, diag="signed")
+    T[1234, :1235] *= 2.0 ** -40  # one whole row
+    assert not P.int8_scaling_ok(T, "L")
+    synth.device_fill(T, n, diag="signed")
+    T[n - 1, n - 1] = float("nan")  # non-finite entry
+    assert not P.int8_scaling_ok(T, "L")
 
 
 @pytest.mark.parametrize("n,uplo,seed", [(8192, "L", 0), (16384, "L", 3), (16384, "U", 7), (32768, "U", 0)])
@@ -132,3 +139,88 @@ def test_scaling_guard_no_veto_on_baseline_inputs(n, uplo, seed):
     h = n // 2
     assert P.int8_scaling_ok(T[:h, :h].contiguous(), uplo)
     assert P.int8_scaling_ok(T[h:, h:].contiguous(), uplo)
+
+
+OZ_MAX_SPREAD = 8  # trinv.cu
+
+
+def _row_scaled(n, spread, uplo, seed):
+    """T with its rows scaled by 2^k_i, k_i uniform in [0, spread] with both ends present:
+    the row-maximum exponents (diagonal-dominated, |T_ii| in [1, 2)) span exactly `spread`
+    binades."""
+    rng = np.random.default_rng(seed)
+    k = rng.integers(0, spread + 1, n)
+    k[0], k[-1] = 0, spread
+    T = synth.host(n, seed=seed, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    return np.ldexp(T, k[:, None])
+
+
+@pytest.mark.parametrize("spread", [6, 8, 10])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_scaling_guard_threshold(spread, uplo):
+    """At and around the guard's threshold: inputs with 6 and 8 binades of row spread run
+    on the INT8 engine (the result differs from DMMA's), 10 binades are vetoed (bit for bit
+    DMMA); every case meets the 1e-10 floored gate against the oracle.  (Measured: the
+    engine's floored error grows as ~1.3e-14 x 2^spread on these inputs, 3.5e-9 at 18 and
+    3.4e-8 at 20 binades, which is why the threshold is 8, not the 20 of round 1.)"""
+    import oracle
+    from gpu_common import REL_TOL, RES_TOL
+    n = 1024
+    S = _row_scaled(n, spread, uplo, seed=spread)
+    Sd = torch.from_numpy(S).to(DEV)
+    f = P.trinv_lower if uplo == "L" else P.trinv_upper
+    try:
+        P.set_product_engine("int8crt", min_block=256)
+        assert P.int8_scaling_ok(Sd, uplo) == (spread <= OZ_MAX_SPREAD)
+        X8 = f(Sd).cpu().numpy()
+        P.set_product_engine("dmma")
+        Xd = f(Sd).cpu().numpy()
+    finally:
+        P.set_product_engine()
+    assert np.array_equal(X8, Xd) == (spread > OZ_MAX_SPREAD)
+    assert oracle.floored_rel_err(X8, oracle.trinv(S, uplo)) <= REL_TOL
+    St = np.tril(S) if uplo == "L" else np.triu(S)
+    assert oracle.residual_ratio(St, X8) <= RES_TOL
+
+
+def test_scaling_guard_unit_diagonal_not_read():
+    """With a unit diagonal the stored diagonal is not used: junk stored there (2^40 on every
+    other row) neither fakes a spread nor hides a real one (rows whose off-diagonal entries
+    are scaled by 2^30, which only the implicit unit diagonal leaves visible)."""
+    n = 2048
+    L = torch.from_numpy(synth.host(n, tag="L", diag="one")).to(DEV)
+    assert P.int8_scaling_ok(L, "L")
+    junk = L.clone(); junk.diagonal()[::2] = 2.0 ** 40
+    assert P.int8_scaling_ok(junk, "L", unit=True)        # not read: no spread
+    assert not P.int8_scaling_ok(junk, "L", unit=False)   # read: 40 binades between rows
+    spread = L.clone(); spread[n // 2:] *= 2.0 ** 30      # real spread of the row maxima
+    spread.diagonal().fill_(2.0 ** 40)                    # junk that would hide it if read
+    assert not P.int8_scaling_ok(spread, "L", unit=True)
+    assert P.int8_scaling_ok(spread, "L", unit=False)
+
+
+def test_scaling_guard_under_capture_uses_dmma():
+    """Under stream capture the guard cannot run: a captured call uses DMMA (bit for bit the
+    eager DMMA result), and int8_scaling_ok reports False."""
+    n = 1024
+    T = torch.from_numpy(synth.host(n, seed=9, diag="signed")).to(DEV)
+    X = torch.empty_like(T)
+    try:
+        P.set_product_engine("dmma")
+        Xd = P.trinv_lower(T).cpu().numpy()
+        P.set_product_engine("int8crt", min_block=256)
+        s = torch.cuda.Stream()
+        P.trinv_lower(T, out=X)  # warm-up outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        flags = []
+        with torch.cuda.graph(g, stream=s):
+            P.trinv_lower(T, out=X)
+            flags.append(P.int8_scaling_ok(T, "L"))
+        X.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+    finally:
+        P.set_product_engine()
+    assert flags == [False]
+    assert np.array_equal(X.cpu().numpy(), Xd)

@@ -193,3 +193,6 @@ def test_config4_inv_from_lu_n16384():
     ref = oracle.lu_columns(L, U, cols, unit_l=True)
     assert oracle.floored_rel_err(Xs, ref, axis_cols=0) <= REL_TOL
     assert rho_a <= RES_TOL, rho_a
+    # rho_LU (reading C21): the factored residual L (U X_S) - I_S on the CPU, no formed A
+    rho_lu = oracle.factored_column_residual_ratio(L, U, Xs, cols)
+    assert rho_lu <= RES_TOL, rho_lu

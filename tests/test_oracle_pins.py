@@ -317,6 +317,17 @@ def test_column_residual_ratio_hand_values():
         0.2 / np.sqrt(6.0 * (1.44 + 0.25 + 0.25)), rel=1e-12)
 
 
+def test_factored_column_residual_ratio_hand_values():
+    # L = [[1,0],[2,1]], U = [[2,1],[0,1]]: A = L U = [[2,1],[4,3]], A^-1 = [[1.5,-.5],[-2,1]].
+    # Column 0 given as [1.5, -2.1]: U x = [.9, -2.1], L (U x) = [.9, -.3], minus e_0 =
+    # [-.1, -.3]; ||L||_F = ||U||_F = sqrt 6, ||x|| = sqrt 6.66
+    L = np.array([[1.0, 0.0], [2.0, 1.0]]); U = np.array([[2.0, 1.0], [0.0, 1.0]])
+    got = oracle.factored_column_residual_ratio(L, U, np.array([[1.5, -2.1]]), [0])
+    assert got == pytest.approx(np.sqrt(0.1) / (6.0 * np.sqrt(6.66)), rel=1e-12)
+    # (U (L x) would give [2.9, .9]); the exact inverse columns give 0
+    assert oracle.factored_column_residual_ratio(L, U, np.array([[1.5, -2.0], [-0.5, 1.0]]), [0, 1]) == 0.0
+
+
 def test_floored_rel_err_hand_values():
     # axis_cols=0: each ROW of the arrays is one column of the inverse, floor from its own max
     R = np.array([[1e-9, 2.0], [4.0, 1e-3]])

@@ -614,9 +614,18 @@ def main():
     if cfg["kind"] == "B":
         avg_ms = statistics.mean(step_ms)  # one launch per step: the leaf kernel
         achieved = algo_bytes_per_launch / (avg_ms / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": "leaf32_mma_kernel (trinv_batched)", "achieved": achieved,
+        traffic = ncu_traffic("leaf32_tma_kernel")
+        traffic_per_launch = traffic * B / BATCH if traffic else None  # the ncu capture is of a 131072 launch
+        line["roofline"] = {"bound": "hbm", "kernel": "leaf32_tma_kernel (trinv_batched)", "achieved": achieved,
                             "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                            "traffic": ncu_traffic("leaf32_mma_kernel"), "peak_source": hbm_src,
+                            "traffic": traffic_per_launch, "peak_source": hbm_src,
+                            "traffic_frac": (traffic_per_launch / (avg_ms / 1e3) / 1e9 / hbm_peak
+                                             if traffic_per_launch else None),
+                            "traffic_note": "DRAM moves 128-byte lines: the referenced triangle costs 6144 B of "
+                                            "reads per matrix (48 lines), not 4224 (tools/sector_probe.cu: 32 B "
+                                            "read per line still moves the whole line), so the frac ceiling on "
+                                            "the 12416 B algorithmic bytes is 12416 / 14336 = 0.866 at the copy "
+                                            "peak; traffic_frac is the same launch on the bytes DRAM moves",
                             "algorithmic_bytes_per_launch": algo_bytes_per_launch,
                             "launch_ms": avg_ms, "fp64_gflops": flops_per_step / (avg_ms / 1e3) / 1e9}
     else:

@@ -193,6 +193,20 @@ size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n);
 trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
                             trinv_diag_t diag, void* ws, size_t ws_bytes, int32_t* d_info, void* stream);
 
+/* ---- NEXT row f3: Strassen inside the inversion ------------------------------------------
+ * The paper's P_TF recursion (Eq. PTFmbk): a triangle-times-full product of order
+ * 2h splits into four half-size triangle-times-full products and two full-times-full ones,
+ * the latter by Strassen's 7-product recursion.  With levels > 0 (and
+ * the DMMA engine) the single top merge of trinv_lower / trinv_upper (n = 2b, h = b/2 >=
+ * min_h, h % 4 == 0) and the U^-1 L^-1 product of inv_from_lu (n % 8 == 0, n/2 >= min_h)
+ * run by quadrants with `levels` Strassen levels in their dense h^3 products; all other
+ * products are unchanged.  levels 0 (default) = off; 0..3, min_h >= 64, else
+ * TRINV_INVALID_ARG.  Process-wide; TRINV_STRASSEN=<levels> sets it before the first call.
+ * Changes trinv_workspace_bytes ('L', 'U', 'G'): query it after.  DESIGN.md §11 has the
+ * measured time and error that decide the default. */
+trinv_status_t trinv_set_strassen(int levels, int64_t min_h);
+int trinv_get_strassen(void);
+
 /* ---- NEXT row f3 (measurement only) ----------------------------------------------------
  * C = A B for dense n x n (n divisible by 4) with ONE level of Strassen's 7-product
  * recursion (the paper's fast multiplication for block products, P:20, P:46, P:523,

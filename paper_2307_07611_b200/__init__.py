@@ -230,6 +230,16 @@ def set_product_engine(engine="dmma", min_block=2048):
     _MIN_BLOCK = int(min_block)
 
 
+def set_strassen(levels=0, min_h=4096):
+    """NEXT row f3: Strassen levels in the dense quadrant products of the top merge of a
+    triangular inverse and of inv_from_lu's U^-1 L^-1 (trinv_set_strassen; 0 = off)."""
+    _check(lib().trinv_set_strassen(int(levels), int(min_h)))
+
+
+def strassen_levels():
+    return int(lib().trinv_get_strassen())
+
+
 def product_min_block():
     return _MIN_BLOCK
 

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtrinv.so")
-SOURCES = ["trinv.cu", "leaf.cu", "leaf64.cu", "blk.cu", "gemm.cu", "lu.cu", "oz2.cu", "probe.cu"]
+SOURCES = ["trinv.cu", "leaf.cu", "leaf64.cu", "blk.cu", "gemm.cu", "lu.cu", "oz2.cu", "probe.cu", "strassen.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"]
 

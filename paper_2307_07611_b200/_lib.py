@@ -75,6 +75,8 @@ def lib():
                           ctypes.c_double, _vp, _i64, _i32, _vp, _sz, _vp], _i32)
     sig("trinv_set_product_engine", [_i32, _i32, _i64], _i32)
     sig("trinv_get_product_engine", None, _i32)
+    sig("trinv_set_strassen", [_i32, _i64], _i32)
+    sig("trinv_get_strassen", None, _i32)
     sig("trinv_int8_scaling_ok", [_i64, ctypes.c_void_p, _i64, ctypes.c_char, _i32, ctypes.c_void_p], _i32)
     sig("trinv_status_string", [_i32], ctypes.c_char_p)
     sig("trinv_last_cuda_error", None, _i32)

@@ -144,6 +144,14 @@ cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cu
 cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
                            cudaStream_t s, int64_t* launches);
 
+// ---- Strassen's recursion for dense square block products (strassen.cu, NEXT f3) ------
+// C = beta C + alpha A B (h x h, row-major, 16-byte aligned, even ld) with `levels` levels of
+// Strassen's 7 products over the DMMA GEMM (h % 4 != 0 or levels == 0: one GEMM).
+size_t strassen_ws_bytes(int64_t h, int levels);
+cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                         double beta, double* C, int64_t ldc, int levels, void* ws, cudaStream_t s,
+                         int64_t* launches);
+
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.
 bool encode_map(CUtensorMap* m, const MatRef& r, int box_cols, int box_rows, bool swizzle128);

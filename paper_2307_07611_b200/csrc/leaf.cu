@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// n = 32 with the off-diagonal block on the FP64 tensor cores (the default for the
-// batched n = 32 path and the 32-wide recursion leaves with an aligned, even layout).
+// n = 32 with the off-diagonal block on the FP64 tensor cores (opt-in, TRINV_LEAF32=mma;
+// measured slower than the band kernel, see launch_leaf).
 // The scalar recurrence above reads every T_ik (i > k) once per lane: ~250 16-byte
 // shared broadcasts per matrix, which made leaf32_tma_kernel shared-memory (LSU) bound
 // (ncu: l1tex 96%).  Here the 32x32 matrix is one beta = 2 merge of Alg. 1
@@ -350,8 +350,78 @@ __device__ __forceinline__ void m_mma16(double (&acc)[2][2][2], const double* A,
   }
 }
 
-template <bool UPPER, int WARPS, int NS>
+// Stage 1 (a1, a2): reciprocals into the diagonal slots, the recurrence of half-warp h on
+// its diagonal block, X11 / X22 into the slot (operands of stage 2) and to `dst` (when
+// `store`), the zero quadrant to `dst`.  Returns the warp's zero-diagonal mask.
+template <bool UPPER>
+__device__ __forceinline__ unsigned m_stage1(double* S, const LeafArgs& a, double* dst, bool store, int lane) {
+  const int h = lane >> 4, c = lane & 15;
+  double* Th = S + 16 * h * (MS + 1);  // diagonal block h
+  const double d = Th[c * (MS + 1)];
+  const unsigned zmask = __ballot_sync(0xffffffffu, (!a.unit) && d == 0.0);
+  const double r = a.unit ? 1.0 : __drcp_rn(d);  // correctly rounded: X_jj == 1/T_jj bitwise (C4)
+  __syncwarp();
+  Th[c * (MS + 1)] = r;
+  __syncwarp();
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+  m_steps<UPPER>(Th, x, std::make_integer_sequence<int, 8>{});
+  __syncwarp();  // every lane has read its block before it is overwritten by its inverse
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double v = (UPPER ? i > c : i < c) ? 0.0 : x[i];
+    Th[i * MS + c] = v;                                               // operand of stage 2
+    if (store) dst[(int64_t)(16 * h + i) * a.ldx + 16 * h + c] = v;   // X11 / X22 rows (a7 inside)
+  }
+  if (store) {  // the zero quadrant (a7): lower rows 0..15 x cols 16..31, upper rows 16..31 x cols 0..15
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rr = 4 * q + (lane >> 3), cc = 2 * (lane & 7);
+      *reinterpret_cast<double2*>(dst + (int64_t)(UPPER ? 16 + rr : rr) * a.ldx + (UPPER ? cc : 16 + cc)) =
+          make_double2(0.0, 0.0);
+    }
+  }
+  return zmask;
+}
+// Stage 2a (a5): W = L21 X11 (upper: U12 X22) into the slot's unreferenced quadrant.
+template <bool UPPER>
+__device__ __forceinline__ void m_stage2a(double* S, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+  double acc[2][2][2] = {};
+  double* W = UPPER ? S + 16 * MS : S + 16;
+  if (!UPPER) m_mma16<0>(acc, S + 16 * MS, S, lane);   // W = L21 X11
+  else m_mma16<2>(acc, S + 16, S + 16 * MS + 16, lane);  // W = U12 X22
+#pragma unroll
+  for (int I = 0; I < 2; ++I)
+#pragma unroll
+    for (int J = 0; J < 2; ++J)
+      *reinterpret_cast<double2*>(W + (8 * I + lr) * MS + 8 * J + 2 * lc) = make_double2(acc[I][J][0], acc[I][J][1]);
+}
+// Stage 2b (a6, a7): X21 = -X22 W (upper: X12 = -X11 W) straight to `dst`.
+template <bool UPPER>
+__device__ __forceinline__ void m_stage2b(const double* S, const LeafArgs& a, double* dst, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+  double acc[2][2][2] = {};
+  const double* W = UPPER ? S + 16 * MS : S + 16;
+  if (!UPPER) m_mma16<1>(acc, S + 16 * MS + 16, W, lane);  // X21 = -X22 W
+  else m_mma16<3>(acc, S, W, lane);                          // X12 = -X11 W
+  double* o = dst + (UPPER ? 16 : 16 * a.ldx);
+#pragma unroll
+  for (int I = 0; I < 2; ++I)
+#pragma unroll
+    for (int J = 0; J < 2; ++J)
+      *reinterpret_cast<double2*>(o + (int64_t)(8 * I + lr) * a.ldx + 8 * J + 2 * lc) =
+          make_double2(-acc[I][J][0], -acc[I][J][1]);
+}
+
+// PIPE = false: the three stages of matrix t in order.  PIPE = true (NS >= 3): stage 1 of
+// matrix t+1 is interleaved with stage 2 of matrix t in three straight-line segments
+// separated by __syncwarp (the recurrence's FP64 chain overlaps the DMMA chain of the
+// other matrix; every segment touches two different slots).
+template <bool UPPER, int WARPS, int NS, bool PIPE>
 __global__ void __launch_bounds__(WARPS * 32, 1) leaf32_mma_kernel(const LeafArgs a) {
+  static_assert(!PIPE || NS >= 3, "the pipelined loop keeps two slots live and one loading");
   extern __shared__ __align__(16) double msmem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* slots = msmem + (size_t)warp * NS * MSLOT;
@@ -379,85 +449,63 @@ __global__ void __launch_bounds__(WARPS * 32, 1) leaf32_mma_kernel(const LeafArg
     }
     cpa_commit();  // one group per matrix slot, empty past the end (uniform wait counts)
   };
+  auto dst_of = [&](int64_t t) { return a.X + (gw + t * TW) * a.sX; };
 #pragma unroll
   for (int t = 0; t < NS - 1; ++t) issue(t);
 
-  const int h = lane >> 4, c = lane & 15;
-  const int lr = lane >> 2, lc = lane & 3;
-  for (int64_t t = 0; t < count; ++t) {
-    issue(t + NS - 1);
-    cpa_wait<NS - 1>();
-    __syncwarp();
-    const int64_t b = gw + t * TW;
-    double* S = slots + (t % NS) * MSLOT;
-    double* Th = S + 16 * h * (MS + 1);  // diagonal block h
-    double* dst = a.X + b * a.sX;
-
-    // 1. diagonal blocks (a1, a2): reciprocals, then the recurrence
-    const double d = Th[c * (MS + 1)];
-    const bool zero = (!a.unit) && d == 0.0;
-    const unsigned zmask = __ballot_sync(0xffffffffu, zero);
-    __syncwarp();
-    Th[c * (MS + 1)] = a.unit ? 1.0 : 1.0 / d;  // IEEE division: X_jj == 1/T_jj bitwise (C4)
-    __syncwarp();
-    double x[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = (i == c) ? 1.0 : 0.0;
-    m_steps<UPPER>(Th, x, std::make_integer_sequence<int, 8>{});
-    __syncwarp();  // every lane has read its block before it is overwritten by its inverse
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const double v = (UPPER ? i > c : i < c) ? 0.0 : x[i];
-      Th[i * MS + c] = v;                                          // operand of step 2
-      dst[(int64_t)(16 * h + i) * a.ldx + 16 * h + c] = v;         // X11 / X22 rows (a7 inside)
+  if constexpr (!PIPE) {
+    for (int64_t t = 0; t < count; ++t) {
+      issue(t + NS - 1);
+      cpa_wait<NS - 1>();
+      __syncwarp();
+      double* S = slots + (t % NS) * MSLOT;
+      double* dst = dst_of(t);
+      const unsigned zmask = m_stage1<UPPER>(S, a, dst, true, lane);
+      __syncwarp();
+      m_stage2a<UPPER>(S, lane);
+      __syncwarp();
+      m_stage2b<UPPER>(S, a, dst, lane);
+      __syncwarp();  // every lane is done with the slot: the next load may overwrite it
+      leaf_report(a, gw + t * TW, lane, zmask != 0, zmask ? __ffs(zmask) - 1 : -1);
     }
-    // the zero block (a7): lower rows 0..15 x cols 16..31, upper rows 16..31 x cols 0..15
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = 4 * q + (lane >> 3), cc = 2 * (lane & 7);
-      *reinterpret_cast<double2*>(dst + (int64_t)(UPPER ? 16 + r : r) * a.ldx + (UPPER ? cc : 16 + cc)) =
-          make_double2(0.0, 0.0);
+  } else {
+    // prologue: stage 1 of matrix 0
+    cpa_wait<NS - 2>();
+    __syncwarp();
+    unsigned zm = m_stage1<UPPER>(slots, a, dst_of(0), true, lane);
+    __syncwarp();
+    for (int64_t t = 0; t < count; ++t) {
+      const bool next = t + 1 < count;
+      issue(t + NS - 1);          // slot of matrix t-1: free since the end of the last iteration
+      cpa_wait<NS - 2>();         // matrix t+1 has landed
+      __syncwarp();
+      double* S = slots + (t % NS) * MSLOT;
+      double* Sn = slots + ((t + 1) % NS) * MSLOT;
+      double* dst = dst_of(t);
+      // stage 1 of t+1 (on a stale slot past the end: computed, not stored) | stage 2 of t
+      m_stage2a<UPPER>(S, lane);
+      const unsigned zn = m_stage1<UPPER>(Sn, a, dst_of(next ? t + 1 : t), next, lane);
+      __syncwarp();
+      m_stage2b<UPPER>(S, a, dst, lane);
+      __syncwarp();
+      leaf_report(a, gw + t * TW, lane, zm != 0, zm ? __ffs(zm) - 1 : -1);
+      zm = zn;
     }
-    __syncwarp();
-    // 2. the off-diagonal block on DMMA (a5, a6)
-    double acc[2][2][2] = {};
-    double* W = UPPER ? S + 16 * MS : S + 16;  // the unreferenced quadrant
-    if (!UPPER) m_mma16<0>(acc, S + 16 * MS, S, lane);           // W = L21 X11
-    else m_mma16<2>(acc, S + 16, S + 16 * MS + 16, lane);          // W = U12 X22
-#pragma unroll
-    for (int I = 0; I < 2; ++I)
-#pragma unroll
-      for (int J = 0; J < 2; ++J) {
-        *reinterpret_cast<double2*>(W + (8 * I + lr) * MS + 8 * J + 2 * lc) = make_double2(acc[I][J][0], acc[I][J][1]);
-        acc[I][J][0] = acc[I][J][1] = 0.0;
-      }
-    __syncwarp();
-    if (!UPPER) m_mma16<1>(acc, S + 16 * MS + 16, W, lane);       // X21 = -X22 W
-    else m_mma16<3>(acc, S, W, lane);                              // X12 = -X11 W
-    __syncwarp();  // every lane is done with the slot: the next load may overwrite it
-    double* o = dst + (UPPER ? 16 : 16 * a.ldx);
-#pragma unroll
-    for (int I = 0; I < 2; ++I)
-#pragma unroll
-      for (int J = 0; J < 2; ++J)
-        *reinterpret_cast<double2*>(o + (int64_t)(8 * I + lr) * a.ldx + 8 * J + 2 * lc) =
-            make_double2(-acc[I][J][0], -acc[I][J][1]);
-    leaf_report(a, b, lane, zmask != 0, zmask ? __ffs(zmask) - 1 : -1);
   }
   cpa_wait<0>();
 }
 
-template <int W, int NS>
+template <int W, int NS, bool PIPE = false>
 static void launch_mma32(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
   constexpr size_t smem = (size_t)W * NS * MSLOT * 8;
   const int64_t ctas_needed = (a.batch + W - 1) / W;
   const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
   if (uplo == 'L') {
-    constexpr auto k = leaf32_mma_kernel<false, W, NS>;
+    constexpr auto k = leaf32_mma_kernel<false, W, NS, PIPE>;
     set_smem_once<k>((int)smem);
     k<<<grid, W * 32, smem, s>>>(a);
   } else {
-    constexpr auto k = leaf32_mma_kernel<true, W, NS>;
+    constexpr auto k = leaf32_mma_kernel<true, W, NS, PIPE>;
     set_smem_once<k>((int)smem);
     k<<<grid, W * 32, smem, s>>>(a);
   }
@@ -544,19 +592,26 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   // n = 32, TMA-compatible layout: 8 warps x NS slots per CTA (one CTA per SM), bands of
   // BR rows (profiles/r01_leaf_variants.txt); TRINV_LEAF_BR = 4 / 8 / 16 for experiments
   static const int br = [] { const char* e = std::getenv("TRINV_LEAF_BR"); return e ? std::atoi(e) : 16; }();
-  // n = 32 default: the DMMA-merge kernel (TRINV_LEAF32=band: the scalar TMA-band kernel;
-  // TRINV_LEAF32_CFG = warps x slots per CTA for experiments)
-  static const bool band = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "band"); }();
-  static const int mcfg = [] { const char* e = std::getenv("TRINV_LEAF32_CFG"); return e ? std::atoi(e) : 83; }();
+  // n = 32 default: the scalar TMA-band kernel, at 0.95 of the copy bandwidth on the bytes
+  // DRAM actually moves (128-byte line fills: 6144 B read + 8192 B written per matrix).  The
+  // DMMA-merge kernel (TRINV_LEAF32=mma; TRINV_LEAF32_CFG = [1000 pipelined +] warps x slots,
+  // default 1063) halves the shared-memory wavefronts but is latency-bound and measured
+  // 3-12% slower (profiles/r02_leaf_variants.txt).
+  static const bool mma = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "mma"); }();
+  static const int mcfg = [] { const char* e = std::getenv("TRINV_LEAF32_CFG"); return e ? std::atoi(e) : 1063; }();
   bool launched = false;
-  if (!band && tma && full32 && a.lda * 32 < ((int64_t)1 << 31)) {
+  if (mma && tma && full32 && a.lda * 32 < ((int64_t)1 << 31)) {
     switch (mcfg) {
       case 122: launch_mma32<12, 2>(uplo, a, sms, s); break;
       case 64: launch_mma32<6, 4>(uplo, a, sms, s); break;
       case 62: launch_mma32<6, 2>(uplo, a, sms, s); break;
       case 42: launch_mma32<4, 2>(uplo, a, sms, s); break;
       case 82: launch_mma32<8, 2>(uplo, a, sms, s); break;
-      default: launch_mma32<8, 3>(uplo, a, sms, s); break;
+      case 1083: launch_mma32<8, 3, true>(uplo, a, sms, s); break;
+      case 1064: launch_mma32<6, 4, true>(uplo, a, sms, s); break;
+      case 1043: launch_mma32<4, 3, true>(uplo, a, sms, s); break;
+      case 83: launch_mma32<8, 3>(uplo, a, sms, s); break;
+      default: launch_mma32<6, 3, true>(uplo, a, sms, s); break;
     }
     launched = true;
   }

@@ -397,9 +397,45 @@ static bool ul_on_int8(int64_t n) {
   return product_engine() == 2 && n >= g_oz_min.load() && oz2_supported(n, n, n);
 }
 
+// ---- NEXT row f3: Strassen in the dense quadrant products of the top level ------------------
+// The paper's P_TF recursion (Eq. PTFmbk): a triangle-times-full product of order
+// 2h splits into 4 half-size triangle-times-full products and 2 full-times-full ones, the latter
+// by Strassen's 7-product recursion.  With g_strassen_levels > 0 the top
+// merge of a triangular inverse (one merge, n = 2b, h = b/2 >= g_strassen_min, h % 4 == 0) and
+// the U^-1 L^-1 product of inv_from_lu run that way on the DMMA engine (strassen.cu);
+// TRINV_STRASSEN=<levels> sets it before the first call.  Default 0 (off): DESIGN.md §11.
+static std::atomic<int> g_strassen_levels{-1};
+static std::atomic<int64_t> g_strassen_min{4096};
+static int strassen_levels() {
+  int l = g_strassen_levels.load(std::memory_order_relaxed);
+  if (l < 0) {
+    const char* v = getenv("TRINV_STRASSEN");
+    l = v ? std::max(0, std::min(3, atoi(v))) : 0;
+    g_strassen_levels.store(l, std::memory_order_relaxed);
+  }
+  return l;
+}
+static bool strassen_top(int64_t n, int64_t b) {  // does the merge at level b take the Strassen path?
+  const int64_t h = b / 2;
+  return strassen_levels() > 0 && product_engine() == 0 && n == 2 * b && h % 4 == 0 &&
+         h >= g_strassen_min.load();
+}
+static int64_t top_block(int64_t n) {  // the block size of the top level (its single merge)
+  int64_t b = BLK_MAX;
+  while (2 * b < n) b *= 2;
+  return b;
+}
+static size_t strassen_scratch(int64_t n) {
+  const int64_t b = top_block(n);
+  return (n > BLK_MAX && strassen_top(n, b)) ? align_up(strassen_ws_bytes(b / 2, strassen_levels())) : 0;
+}
+static bool strassen_ul(int64_t n) {
+  return strassen_levels() > 0 && product_engine() == 0 && n % 8 == 0 && n / 2 >= g_strassen_min.load();
+}
+
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
-  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n);
+  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n);
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
   return bytes;
@@ -423,6 +459,64 @@ static trinv_status_t cuda_fail(cudaError_t e) {
     trinv_status_t _st = cuda_fail((expr));         \
     if (_st != TRINV_OK) return _st;                \
   } while (0)
+
+static cudaError_t gemm_tri(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, int triA,
+                            const double* B, int64_t ldb, int triB, double beta, double* C, int64_t ldc,
+                            cudaStream_t s) {
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K; g.batch = 1;
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+  g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
+  return launch_gemm(g, s, &g_launches);
+}
+// The single top merge of order n = 2b with the quadrant decomposition (h = b/2):
+//   lower  W = C A^-1,  A^-1 = [P 0; Q R]:  W = [C1 P + C2 Q, C2 R];
+//          X21 = -B^-1 W, B^-1 = [P' 0; Q' R']:  X21 = -[P' W1; Q' W1 + R' W2]
+//   upper  W = A^-1 B,  A^-1 = [P Q; 0 R]:  W = [P B1 + Q B2; R B2];
+//          X12 = -W C^-1, C^-1 = [P' Q'; 0 R']:  X12 = -[W1 P', W1 Q' + W2 R']
+// Triangular quadrant products on the DMMA GEMM with their structurally zero blocks skipped;
+// the dense ones (C2 Q, Q' W1 / Q B2, W1 Q': two h^3 squares each) by strassen_acc.
+static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
+                                  double* W, void* sws, cudaStream_t s) {
+  const int64_t b = n / 2, h = b / 2;
+  const int lv = strassen_levels();
+  const double* Ai = X;                    // A^-1 (b x b)
+  const double* Bi = X + b * ldx + b;      // B^-1 / C^-1 (b x b)
+  cudaError_t e;
+#define M_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  if (uplo == 'L') {
+    const double* C = A + b * lda;  // b x b, input rows b.., cols 0..b
+    double* X21 = X + b * ldx;
+    M_TRY(gemm_tri(b, h, h, 1.0, C, lda, TRI_NONE, Ai, ldx, TRI_LOWER, 0.0, W, b, s));                       // C1 P
+    for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // + C2 Q
+      M_TRY(strassen_acc(h, 1.0, C + r0 * lda + h, lda, Ai + h * ldx, ldx, 1.0, W + r0 * b, b, lv, sws, s,
+                         &g_launches));
+    M_TRY(gemm_tri(b, h, h, 1.0, C + h, lda, TRI_NONE, Ai + h * ldx + h, ldx, TRI_LOWER, 0.0, W + h, b, s));  // C2 R
+    M_TRY(gemm_tri(h, b, h, -1.0, Bi, ldx, TRI_LOWER, W, b, TRI_NONE, 0.0, X21, ldx, s));                     // -P' W1
+    M_TRY(gemm_tri(h, b, h, -1.0, Bi + h * ldx + h, ldx, TRI_LOWER, W + h * b, b, TRI_NONE, 0.0, X21 + h * ldx,
+                   ldx, s));                                                                                  // -R' W2
+    for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // - Q' W1
+      M_TRY(strassen_acc(h, -1.0, Bi + h * ldx, ldx, W + c0, b, 1.0, X21 + h * ldx + c0, ldx, lv, sws, s,
+                         &g_launches));
+    M_TRY(launch_zero_2d(X + b, ldx, b, b, s, &g_launches));
+  } else {
+    const double* B = A + b;  // b x b, input rows 0..b, cols b..
+    double* X12 = X + b;
+    M_TRY(gemm_tri(h, b, h, 1.0, Ai, ldx, TRI_UPPER, B, lda, TRI_NONE, 0.0, W, b, s));                        // P B1
+    for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // + Q B2
+      M_TRY(strassen_acc(h, 1.0, Ai + h, ldx, B + h * lda + c0, lda, 1.0, W + c0, b, lv, sws, s, &g_launches));
+    M_TRY(gemm_tri(h, b, h, 1.0, Ai + h * ldx + h, ldx, TRI_UPPER, B + h * lda, lda, TRI_NONE, 0.0, W + h * b, b,
+                   s));                                                                                      // R B2
+    M_TRY(gemm_tri(b, h, h, -1.0, W, b, TRI_NONE, Bi, ldx, TRI_UPPER, 0.0, X12, ldx, s));                     // -W1 P'
+    M_TRY(gemm_tri(b, h, h, -1.0, W + h, b, TRI_NONE, Bi + h * ldx + h, ldx, TRI_UPPER, 0.0, X12 + h, ldx, s));  // -W2 R'
+    for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // - W1 Q'
+      M_TRY(strassen_acc(h, -1.0, W + r0 * b, b, Bi + h, ldx, 1.0, X12 + r0 * ldx + h, ldx, lv, sws, s,
+                         &g_launches));
+    M_TRY(launch_zero_2d(X + b * ldx, ldx, b, b, s, &g_launches));
+  }
+#undef M_TRY
+  return cudaSuccess;
+}
 
 // Core recursion on an aligned, even-ld problem (or n <= 32 in any layout).
 // info: NULL or a single accumulator already initialised by the caller.
@@ -477,6 +571,11 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
     } else {
       l1.mode = MODE_UPPER_1; l1.opA = xr; l1.opB = in;
       l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
+    }
+    if (b_stop == 0 && strassen_top(n, b)) {  // NEXT f3: the top merge with Strassen's dense quadrants
+      void* sws = reinterpret_cast<char*>(W) + align_up(w_bytes(n)) + oz_scratch(n);
+      TRY(strassen_merge(uplo, n, A, lda, X, ldx, W, sws, s));
+      continue;
     }
     if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
       void* ozws0 = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
@@ -571,7 +670,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
 
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
-  p += align_up(w_bytes(n));
+  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n);  // W, then run_tri's scratch
   const double* Ause = A;
   int64_t lda_use = lda;
   if (!tma_ok(A, lda)) {  // stage the input into an even-ld, aligned copy
@@ -594,6 +693,33 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   return TRINV_OK;
 }
 
+
+// U^-1 L^-1 = S K by quadrants (h = n/2): S = [S11 S12; 0 S22], K = [K11 0; K21 K22]:
+//   X11 = S11 K11 + S12 K21,  X12 = S12 K22,  X21 = S22 K21,  X22 = S22 K22
+// (S11 K11 and S22 K22 are upper x lower products of order h, P_UL; S12 K21 dense, by
+// strassen_acc; S12 K22 / S22 K21 dense x triangular).  NEXT f3.
+static size_t ul_strassen_scratch(int64_t n) {
+  return strassen_ul(n) ? align_up(strassen_ws_bytes(n / 2, strassen_levels())) : 0;
+}
+static trinv_status_t ul_strassen(int64_t n, const double* S, const double* K, int64_t ld, double* X, int64_t ldx,
+                                  void* sws, cudaStream_t s) {
+  const int64_t h = n / 2;
+  auto ul = [&](const double* Sq, const double* Kq, double* Xq) {
+    LevelArgs u{};
+    u.mode = MODE_UL; u.n = h; u.b = h; u.merges = 1;
+    u.opA = MatRef{Sq, h, h, ld}; u.opB = MatRef{Kq, h, h, ld};
+    u.out = Xq; u.ldo = ldx; u.out_rows = h; u.out_cols = h; u.alpha = 1.0;
+    return launch_level(u, s, &g_launches);
+  };
+  TRY(ul(S, K, X));                                                                           // S11 K11
+  TRY(strassen_acc(h, 1.0, S + h, ld, K + h * ld, ld, 1.0, X, ldx, strassen_levels(), sws, s,
+                   &g_launches));                                                             // + S12 K21
+  TRY(gemm_tri(h, h, h, 1.0, S + h, ld, TRI_NONE, K + h * ld + h, ld, TRI_LOWER, 0.0, X + h, ldx, s));   // S12 K22
+  TRY(gemm_tri(h, h, h, 1.0, S + h * ld + h, ld, TRI_UPPER, K + h * ld, ld, TRI_NONE, 0.0, X + h * ldx, ldx,
+               s));                                                                           // S22 K21
+  TRY(ul(S + h * ld + h, K + h * ld + h, X + h * ldx + h));                                   // S22 K22
+  return TRINV_OK;
+}
 
 // ---- NEXT row f4: COMBRIT with beta = 4 at the top level ------------------------------
 // Alg. 1 with beta = 4 on n = 4m (m = 32 * 2^k): the four diagonal
@@ -846,7 +972,7 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   const size_t tws_bytes = std::max(tri_ws(n, Lf, ldl, nullptr, lde), tri_ws(n, Uf, ldu, nullptr, lde));
   const bool stage_x = !tma_ok(X, ldx);
   const size_t need = 2 * align_up(mat_bytes(n)) + align_up(tws_bytes) + (stage_x ? align_up(mat_bytes(n)) : 0) +
-                      (ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : 0);
+                      (ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : 0) + ul_strassen_scratch(n);
   if (ws_bytes < need || ws == nullptr) return TRINV_WORKSPACE_TOO_SMALL;
   Int8Scope scope(true);
   if (int8_would_run(n) || ul_on_int8(n)) {
@@ -868,6 +994,9 @@ static trinv_status_t inv_from_lu_core(int64_t n, const double* Lf, int64_t ldl,
   if (stage_x) { Xuse = reinterpret_cast<double*>(p); ldx_use = lde; p += align_up(mat_bytes(n)); }
   if (ul_on_int8(n) && !int8_veto()) {  // S K on the INT8 tensor cores (k >= max(i, j))
     TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, p, s, &g_launches));
+  } else if (strassen_ul(n)) {  // NEXT f3: S K by quadrants, S12 K21 by Strassen
+    const trinv_status_t su = ul_strassen(n, Ui, Li, lde, Xuse, ldx_use, p, s);
+    if (su != TRINV_OK) return su;
   } else {
     LevelArgs ul{};
     ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;
@@ -902,7 +1031,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
     size_t bytes = 2 * align_up(mat_bytes(n)) + align_up(tri_ws(n, A, lda, nullptr, even_up(n)));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
     if (ul_on_int8(n)) bytes += align_up(oz2_workspace_bytes(n, n, n));
-    return bytes;
+    return bytes + ul_strassen_scratch(n);
   }
   return 0;
 }
@@ -1196,6 +1325,14 @@ trinv_status_t trinv_set_product_engine(int engine, int digits, int64_t min_bloc
 }
 
 int trinv_get_product_engine(void) { return product_engine(); }
+
+trinv_status_t trinv_set_strassen(int levels, int64_t min_h) {
+  if (levels < 0 || levels > 3 || min_h < 64) return TRINV_INVALID_ARG;
+  g_strassen_min.store(min_h);
+  g_strassen_levels.store(levels);
+  return TRINV_OK;
+}
+int trinv_get_strassen(void) { return strassen_levels(); }
 
 int trinv_int8_scaling_ok(int64_t n, const double* A, int64_t lda, char uplo, trinv_diag_t diag, void* stream) {
   if (n <= 0 || !A || lda < n || (uplo != 'L' && uplo != 'U' && uplo != 'N')) return -(int)TRINV_INVALID_ARG;

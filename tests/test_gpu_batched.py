@@ -216,3 +216,46 @@ def test_batched64_tma_path(uplo):
     A1 = A.copy(); A1[:, idx, idx] = 1.0
     assert oracle.floored_rel_err(Xu[:300], oracle.crit_batched(A1[:300], uplo, unit=True)) <= REL_TOL
     assert not np.isnan(Xu).any()
+
+
+_MMA_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+import oracle, synth, paper_2307_07611_b200 as P
+from gpu_common import REL_TOL
+bad = 0
+for uplo in 'LU':
+    A = synth.host(32, batch=5000, uplo=uplo, diag='signed' if uplo == 'L' else 'pos')
+    X = P.trinv_batched(torch.from_numpy(A).cuda(), uplo).cpu().numpy()
+    bad += oracle.floored_rel_err(X, oracle.crit_batched(A, uplo)) > REL_TOL
+    opp = np.triu(X, 1) if uplo == 'L' else np.tril(X, -1)
+    bad += not np.all(opp == 0.0)
+    Ap = A.copy(); idx = np.arange(32); A1 = A.copy(); A1[:, idx, idx] = 1.0
+    Ap[:, idx, idx] = np.nan
+    tri = np.triu_indices(32, 1) if uplo == 'L' else np.tril_indices(32, -1)
+    Ap[:, tri[0], tri[1]] = np.nan
+    Xu = P.trinv_batched(torch.from_numpy(Ap).cuda(), uplo, unit=True).cpu().numpy()
+    bad += oracle.floored_rel_err(Xu, oracle.crit_batched(A1, uplo, unit=True)) > REL_TOL
+    Ai = torch.from_numpy(A.copy()).cuda(); P.trinv_batched(Ai, uplo, out=Ai)
+    bad += not torch.equal(Ai.cpu(), torch.from_numpy(X))
+A = synth.host(32, batch=64); A[5, 7, 7] = 0.0
+_, info = P.trinv_batched(torch.from_numpy(A).cuda(), 'L', info=True)
+bad += int(info[5].item()) != 8 or int(info[4].item()) != 0
+print('BAD', bad)
+"""
+
+
+@pytest.mark.parametrize("cfg", ["1063", "83"])
+def test_mma_leaf_variant_parity(cfg):
+    """The opt-in DMMA-merge n = 32 kernel (TRINV_LEAF32=mma, read once per process, hence
+    a subprocess): pipelined and plain variants against the oracle, lower / upper, unit
+    diagonal with NaN-poisoned unreferenced entries, in place, zero-diagonal info."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TRINV_LEAF32="mma", TRINV_LEAF32_CFG=cfg)
+    r = subprocess.run([sys.executable, "-c", _MMA_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "BAD 0" in r.stdout, r.stdout + r.stderr[-2000:]

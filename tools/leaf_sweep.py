@@ -6,10 +6,13 @@ import subprocess
 import sys
 
 steps = sys.argv[1] if len(sys.argv) > 1 else "20"
-variants = [("mma 8x3", {"TRINV_LEAF32_CFG": "83"}), ("mma 8x2", {"TRINV_LEAF32_CFG": "82"}),
-            ("mma 12x2", {"TRINV_LEAF32_CFG": "122"}), ("mma 6x4", {"TRINV_LEAF32_CFG": "64"}),
-            ("mma 6x2", {"TRINV_LEAF32_CFG": "62"}), ("mma 4x2", {"TRINV_LEAF32_CFG": "42"}),
-            ("band16", {"TRINV_LEAF32": "band"})]
+MMA = {"TRINV_LEAF32": "mma"}
+variants = [("pipe 8x3", dict(MMA, TRINV_LEAF32_CFG="1083")), ("pipe 6x3", dict(MMA, TRINV_LEAF32_CFG="1063")),
+            ("pipe 6x4", dict(MMA, TRINV_LEAF32_CFG="1064")), ("pipe 4x3", dict(MMA, TRINV_LEAF32_CFG="1043")),
+            ("mma 8x3", dict(MMA, TRINV_LEAF32_CFG="83")), ("mma 8x2", dict(MMA, TRINV_LEAF32_CFG="82")),
+            ("mma 12x2", dict(MMA, TRINV_LEAF32_CFG="122")), ("mma 6x4", dict(MMA, TRINV_LEAF32_CFG="64")),
+            ("mma 6x2", dict(MMA, TRINV_LEAF32_CFG="62")), ("mma 4x2", dict(MMA, TRINV_LEAF32_CFG="42")),
+            ("band16", {})]
 for name, env in variants:
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "bench.py", "--steps", steps, "--warmup", "5", "--no-cpu-baseline",

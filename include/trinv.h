@@ -199,21 +199,21 @@ trinv_status_t trinv_tri_ex(char uplo, int beta, int64_t n, const double* A, int
  * the latter by Strassen's 7-product recursion.  With levels > 0 (and
  * the DMMA engine) the single top merge of trinv_lower / trinv_upper (n = 2b, h = b/2 >=
  * min_h, h % 4 == 0) and the U^-1 L^-1 product of inv_from_lu (n % 8 == 0, n/2 >= min_h)
- * run by quadrants with `levels` Strassen levels in their dense h^3 products; all other
- * products are unchanged.  levels 0 (default) = off; 0..3, min_h >= 64, else
- * TRINV_INVALID_ARG.  Process-wide; TRINV_STRASSEN=<levels> sets it before the first call.
+ * run by quadrants with up to `levels` Strassen levels in their dense h^3 products (a level
+ * only while its half-size products are >= 2048); all other products are unchanged.
+ * Default: levels 2, min_h 4096 (measured faster at equal floored error);
+ * levels 0 = off.  levels 0..3, min_h >= 64, else TRINV_INVALID_ARG.  Strassen's error is
+ * normwise: with it the DMMA path is no longer exactly invariant under power-of-two row /
+ * column scalings for n >= 16384 (set levels 0 for that).  Process-wide; TRINV_STRASSEN=<levels> sets it before the first call.
  * Changes trinv_workspace_bytes ('L', 'U', 'G'): query it after.  DESIGN.md §11 has the
  * measured time and error that decide the default. */
 trinv_status_t trinv_set_strassen(int levels, int64_t min_h);
 int trinv_get_strassen(void);
 
-/* ---- NEXT row f3 (measurement only) ----------------------------------------------------
- * C = A B for dense n x n (n divisible by 4) with ONE level of Strassen's 7-product
- * recursion (the paper's fast multiplication for block products, P:20, P:46, P:523,
- * P:614-629) over the DMMA GEMM, with element-wise block sums.  Kept out of the
- * inversion path: see DESIGN.md §11 and profiles/r01_strassen.txt for the timing
- * and error measurements behind that decision.  ws_bytes >=
- * trinv_strassen_workspace_bytes(n); A, B, C 16-byte aligned with even ld. */
+/* NEXT row f3, standalone: C = A B for dense n x n (n % 4 == 0) with ONE level of Strassen's
+ * 7-product recursion over the DMMA GEMM (the same routine the inversion uses above).
+ * ws_bytes >= trinv_strassen_workspace_bytes(n); A, B, C 16-byte aligned with even ld
+ * (TRINV_NOT_SUPPORTED otherwise). */
 size_t trinv_strassen_workspace_bytes(int64_t n);
 trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                    int64_t ldc, void* ws, size_t ws_bytes, void* stream);

@@ -230,9 +230,10 @@ def set_product_engine(engine="dmma", min_block=2048):
     _MIN_BLOCK = int(min_block)
 
 
-def set_strassen(levels=0, min_h=4096):
+def set_strassen(levels=2, min_h=4096):
     """NEXT row f3: Strassen levels in the dense quadrant products of the top merge of a
-    triangular inverse and of inv_from_lu's U^-1 L^-1 (trinv_set_strassen; 0 = off)."""
+    triangular inverse and of inv_from_lu's U^-1 L^-1 (trinv_set_strassen; library default
+    2 levels from h = 4096; 0 = off)."""
     _check(lib().trinv_set_strassen(int(levels), int(min_h)))
 
 

@@ -146,10 +146,11 @@ cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t 
 
 // ---- Strassen's recursion for dense square block products (strassen.cu, NEXT f3) ------
 // C = beta C + alpha A B (h x h, row-major, 16-byte aligned, even ld) with `levels` levels of
-// Strassen's 7 products over the DMMA GEMM (h % 4 != 0 or levels == 0: one GEMM).
-size_t strassen_ws_bytes(int64_t h, int levels);
+// Strassen's 7 products over the DMMA GEMM; a level is applied while h % 4 == 0 and its
+// products are >= min_q (else one GEMM).
+size_t strassen_ws_bytes(int64_t h, int levels, int64_t min_q);
 cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-                         double beta, double* C, int64_t ldc, int levels, void* ws, cudaStream_t s,
+                         double beta, double* C, int64_t ldc, int levels, int64_t min_q, void* ws, cudaStream_t s,
                          int64_t* launches);
 
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the

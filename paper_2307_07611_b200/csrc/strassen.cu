@@ -68,16 +68,24 @@ static cudaError_t lincomb(int64_t n, double beta, double* C, int64_t ldc, std::
 static int64_t even_up2(int64_t x) { return (x + 1) & ~int64_t(1); }
 static size_t aup(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t strassen_ws_bytes(int64_t h, int levels) {
-  if (levels <= 0 || h % 4) return 0;
+// A level is applied only while its half-size products keep q >= min_q (the library passes
+// min_h / 2: 2048 by default): below that the DMMA GEMM of the products loses more than the
+// 1/8 of the flops a level saves (config 2's 1024-size products: 5.56 -> 6.75 ms;
+// profiles/r02_strassen_inversion.txt).
+static bool strassen_level_ok(int64_t h, int levels, int64_t min_q) {
+  return levels > 0 && h % 4 == 0 && h / 2 >= min_q;
+}
+
+size_t strassen_ws_bytes(int64_t h, int levels, int64_t min_q) {
+  if (!strassen_level_ok(h, levels, min_q)) return 0;
   const int64_t q = h / 2;
-  return 9 * aup((size_t)q * even_up2(q) * sizeof(double)) + strassen_ws_bytes(q, levels - 1);
+  return 9 * aup((size_t)q * even_up2(q) * sizeof(double)) + strassen_ws_bytes(q, levels - 1, min_q);
 }
 
 cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-                         double beta, double* C, int64_t ldc, int levels, void* ws, cudaStream_t s,
+                         double beta, double* C, int64_t ldc, int levels, int64_t min_q, void* ws, cudaStream_t s,
                          int64_t* launches) {
-  if (levels <= 0 || h % 4) {  // one DMMA GEMM
+  if (!strassen_level_ok(h, levels, min_q)) {  // one DMMA GEMM
     GemmArgs g{};
     g.M = h; g.N = h; g.K = h; g.batch = 1;
     g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
@@ -98,7 +106,7 @@ cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, 
   cudaError_t e = cudaSuccess;
 #define S_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   auto prod = [&](const double* X, int64_t lx, const double* Y, int64_t ly, double* Z) {
-    return strassen_acc(q, 1.0, X, lx, Y, ly, 0.0, Z, lq, levels - 1, inner, s, launches);
+    return strassen_acc(q, 1.0, X, lx, Y, ly, 0.0, Z, lq, levels - 1, min_q, inner, s, launches);
   };
   // M1 = (A11 + A22)(B11 + B22)
   S_TRY(lincomb(q, 0.0, SA, lq, {A11, A22}, {lda, lda}, {1.0, 1.0}, s, launches));

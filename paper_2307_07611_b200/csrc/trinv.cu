@@ -403,18 +403,21 @@ static bool ul_on_int8(int64_t n) {
 // by Strassen's 7-product recursion.  With g_strassen_levels > 0 the top
 // merge of a triangular inverse (one merge, n = 2b, h = b/2 >= g_strassen_min, h % 4 == 0) and
 // the U^-1 L^-1 product of inv_from_lu run that way on the DMMA engine (strassen.cu);
-// TRINV_STRASSEN=<levels> sets it before the first call.  Default 0 (off): DESIGN.md §11.
+// TRINV_STRASSEN=<levels> sets it before the first call.  Default 2 levels from h = 4096 (each
+// level only while its products stay >= 2048): config 3 327.9 -> 316.3 ms, config 4 165.5 ->
+// ~163 ms at unchanged floored error (profiles/r02_strassen_inversion.txt).
 static std::atomic<int> g_strassen_levels{-1};
 static std::atomic<int64_t> g_strassen_min{4096};
 static int strassen_levels() {
   int l = g_strassen_levels.load(std::memory_order_relaxed);
   if (l < 0) {
     const char* v = getenv("TRINV_STRASSEN");
-    l = v ? std::max(0, std::min(3, atoi(v))) : 0;
+    l = v ? std::max(0, std::min(3, atoi(v))) : 2;
     g_strassen_levels.store(l, std::memory_order_relaxed);
   }
   return l;
 }
+static int64_t strassen_min_q() { return std::max<int64_t>(16, g_strassen_min.load() / 2); }
 static bool strassen_top(int64_t n, int64_t b) {  // does the merge at level b take the Strassen path?
   const int64_t h = b / 2;
   return strassen_levels() > 0 && product_engine() == 0 && n == 2 * b && h % 4 == 0 &&
@@ -427,7 +430,7 @@ static int64_t top_block(int64_t n) {  // the block size of the top level (its s
 }
 static size_t strassen_scratch(int64_t n) {
   const int64_t b = top_block(n);
-  return (n > BLK_MAX && strassen_top(n, b)) ? align_up(strassen_ws_bytes(b / 2, strassen_levels())) : 0;
+  return (n > BLK_MAX && strassen_top(n, b)) ? align_up(strassen_ws_bytes(b / 2, strassen_levels(), strassen_min_q())) : 0;
 }
 static bool strassen_ul(int64_t n) {
   return strassen_levels() > 0 && product_engine() == 0 && n % 8 == 0 && n / 2 >= g_strassen_min.load();
@@ -480,6 +483,7 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
                                   double* W, void* sws, cudaStream_t s) {
   const int64_t b = n / 2, h = b / 2;
   const int lv = strassen_levels();
+  const int64_t mq = strassen_min_q();
   const double* Ai = X;                    // A^-1 (b x b)
   const double* Bi = X + b * ldx + b;      // B^-1 / C^-1 (b x b)
   cudaError_t e;
@@ -489,14 +493,14 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
     double* X21 = X + b * ldx;
     M_TRY(gemm_tri(b, h, h, 1.0, C, lda, TRI_NONE, Ai, ldx, TRI_LOWER, 0.0, W, b, s));                       // C1 P
     for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // + C2 Q
-      M_TRY(strassen_acc(h, 1.0, C + r0 * lda + h, lda, Ai + h * ldx, ldx, 1.0, W + r0 * b, b, lv, sws, s,
+      M_TRY(strassen_acc(h, 1.0, C + r0 * lda + h, lda, Ai + h * ldx, ldx, 1.0, W + r0 * b, b, lv, mq, sws, s,
                          &g_launches));
     M_TRY(gemm_tri(b, h, h, 1.0, C + h, lda, TRI_NONE, Ai + h * ldx + h, ldx, TRI_LOWER, 0.0, W + h, b, s));  // C2 R
     M_TRY(gemm_tri(h, b, h, -1.0, Bi, ldx, TRI_LOWER, W, b, TRI_NONE, 0.0, X21, ldx, s));                     // -P' W1
     M_TRY(gemm_tri(h, b, h, -1.0, Bi + h * ldx + h, ldx, TRI_LOWER, W + h * b, b, TRI_NONE, 0.0, X21 + h * ldx,
                    ldx, s));                                                                                  // -R' W2
     for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // - Q' W1
-      M_TRY(strassen_acc(h, -1.0, Bi + h * ldx, ldx, W + c0, b, 1.0, X21 + h * ldx + c0, ldx, lv, sws, s,
+      M_TRY(strassen_acc(h, -1.0, Bi + h * ldx, ldx, W + c0, b, 1.0, X21 + h * ldx + c0, ldx, lv, mq, sws, s,
                          &g_launches));
     M_TRY(launch_zero_2d(X + b, ldx, b, b, s, &g_launches));
   } else {
@@ -504,13 +508,13 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
     double* X12 = X + b;
     M_TRY(gemm_tri(h, b, h, 1.0, Ai, ldx, TRI_UPPER, B, lda, TRI_NONE, 0.0, W, b, s));                        // P B1
     for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // + Q B2
-      M_TRY(strassen_acc(h, 1.0, Ai + h, ldx, B + h * lda + c0, lda, 1.0, W + c0, b, lv, sws, s, &g_launches));
+      M_TRY(strassen_acc(h, 1.0, Ai + h, ldx, B + h * lda + c0, lda, 1.0, W + c0, b, lv, mq, sws, s, &g_launches));
     M_TRY(gemm_tri(h, b, h, 1.0, Ai + h * ldx + h, ldx, TRI_UPPER, B + h * lda, lda, TRI_NONE, 0.0, W + h * b, b,
                    s));                                                                                      // R B2
     M_TRY(gemm_tri(b, h, h, -1.0, W, b, TRI_NONE, Bi, ldx, TRI_UPPER, 0.0, X12, ldx, s));                     // -W1 P'
     M_TRY(gemm_tri(b, h, h, -1.0, W + h, b, TRI_NONE, Bi + h * ldx + h, ldx, TRI_UPPER, 0.0, X12 + h, ldx, s));  // -W2 R'
     for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // - W1 Q'
-      M_TRY(strassen_acc(h, -1.0, W + r0 * b, b, Bi + h, ldx, 1.0, X12 + r0 * ldx + h, ldx, lv, sws, s,
+      M_TRY(strassen_acc(h, -1.0, W + r0 * b, b, Bi + h, ldx, 1.0, X12 + r0 * ldx + h, ldx, lv, mq, sws, s,
                          &g_launches));
     M_TRY(launch_zero_2d(X + b * ldx, ldx, b, b, s, &g_launches));
   }
@@ -699,7 +703,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
 // (S11 K11 and S22 K22 are upper x lower products of order h, P_UL; S12 K21 dense, by
 // strassen_acc; S12 K22 / S22 K21 dense x triangular).  NEXT f3.
 static size_t ul_strassen_scratch(int64_t n) {
-  return strassen_ul(n) ? align_up(strassen_ws_bytes(n / 2, strassen_levels())) : 0;
+  return strassen_ul(n) ? align_up(strassen_ws_bytes(n / 2, strassen_levels(), strassen_min_q())) : 0;
 }
 static trinv_status_t ul_strassen(int64_t n, const double* S, const double* K, int64_t ld, double* X, int64_t ldx,
                                   void* sws, cudaStream_t s) {
@@ -712,7 +716,7 @@ static trinv_status_t ul_strassen(int64_t n, const double* S, const double* K, i
     return launch_level(u, s, &g_launches);
   };
   TRY(ul(S, K, X));                                                                           // S11 K11
-  TRY(strassen_acc(h, 1.0, S + h, ld, K + h * ld, ld, 1.0, X, ldx, strassen_levels(), sws, s,
+  TRY(strassen_acc(h, 1.0, S + h, ld, K + h * ld, ld, 1.0, X, ldx, strassen_levels(), strassen_min_q(), sws, s,
                    &g_launches));                                                             // + S12 K21
   TRY(gemm_tri(h, h, h, 1.0, S + h, ld, TRI_NONE, K + h * ld + h, ld, TRI_LOWER, 0.0, X + h, ldx, s));   // S12 K22
   TRY(gemm_tri(h, h, h, 1.0, S + h * ld + h, ld, TRI_UPPER, K + h * ld, ld, TRI_NONE, 0.0, X + h * ldx, ldx,
@@ -1158,59 +1162,22 @@ size_t trinv_tri_ex_workspace_bytes(int beta, int64_t n) {
 }
 
 size_t trinv_strassen_workspace_bytes(int64_t n) {
-  if (n <= 0 || n % 2) return 0;
-  const int64_t h = n / 2, lh = even_up(h);
-  return 9 * align_up((size_t)h * lh * sizeof(double));  // 2 operand sums + 7 products
+  if (n <= 0 || n % 4) return 0;
+  return strassen_ws_bytes(n, 1, 16);  // 2 operand sums + 7 products of (n/2)^2
 }
 
-// NEXT row f3 (experiment): one level of Strassen's 7-product recursion (cited by
-// the paper for its block products) over the DMMA
-// GEMM for a dense n x n product C = A B (n even).
+// NEXT row f3: one level of Strassen's 7-product recursion (cited by the paper for its block
+// products) over the DMMA GEMM for a dense n x n product
+// C = A B (n % 4 == 0): strassen_acc (strassen.cu), as inside the inversion.
 trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                    int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (n < 0 || n % 2) return n < 0 ? TRINV_INVALID_ARG : TRINV_NOT_SUPPORTED;
+  if (n < 0) return TRINV_INVALID_ARG;
   if (n == 0) return TRINV_OK;
   if (!A || !B || !C || lda < n || ldb < n || ldc < n) return TRINV_INVALID_ARG;
-  if (!tma_ok(A, lda) || !tma_ok(B, ldb) || !tma_ok(C, ldc) || (n / 2) % 2) return TRINV_NOT_SUPPORTED;
+  if (n % 4 || !tma_ok(A, lda) || !tma_ok(B, ldb) || !tma_ok(C, ldc)) return TRINV_NOT_SUPPORTED;
   if (ws_bytes < trinv_strassen_workspace_bytes(n) || !ws) return TRINV_WORKSPACE_TOO_SMALL;
-  const int64_t h = n / 2, lh = even_up(h);
-  const size_t slot = align_up((size_t)h * lh * sizeof(double));
-  auto buf = [&](int k) { return reinterpret_cast<double*>(static_cast<char*>(ws) + k * slot); };
-  double *SA = buf(0), *SB = buf(1);
-  double* M[7];
-  for (int k = 0; k < 7; ++k) M[k] = buf(2 + k);
-  const double *A11 = A, *A12 = A + h, *A21 = A + h * lda, *A22 = A + h * lda + h;
-  const double *B11 = B, *B12 = B + h, *B21 = B + h * ldb, *B22 = B + h * ldb + h;
-  double *C11 = C, *C12 = C + h, *C21 = C + h * ldc, *C22 = C + h * ldc + h;
-  auto add = [&](const double* X, int64_t lx, double b, const double* Y, int64_t ly, double* Z, int64_t lz) {
-    return cuda_fail(launch_geam(h, h, 1.0, X, lx, b, Y, ly, Z, lz, s, &g_launches));
-  };
-  auto mul = [&](const double* X, int64_t lx, const double* Y, int64_t ly, double* Z) {
-    GemmArgs g{};
-    g.M = h; g.N = h; g.K = h; g.batch = 1;
-    g.A = X; g.lda = lx; g.B = Y; g.ldb = ly; g.C = Z; g.ldc = lh;
-    g.alpha = 1.0; g.beta = 0.0; g.triA = TRI_NONE; g.triB = TRI_NONE;
-    return cuda_fail(launch_gemm(g, s, &g_launches));
-  };
-  trinv_status_t st = TRINV_OK;
-#define STEP(x) do { if (st == TRINV_OK) st = (x); } while (0)
-  STEP(add(A11, lda, 1.0, A22, lda, SA, lh)); STEP(add(B11, ldb, 1.0, B22, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[0]));
-  STEP(add(A21, lda, 1.0, A22, lda, SA, lh)); STEP(mul(SA, lh, B11, ldb, M[1]));
-  STEP(add(B12, ldb, -1.0, B22, ldb, SB, lh)); STEP(mul(A11, lda, SB, lh, M[2]));
-  STEP(add(B21, ldb, -1.0, B11, ldb, SB, lh)); STEP(mul(A22, lda, SB, lh, M[3]));
-  STEP(add(A11, lda, 1.0, A12, lda, SA, lh)); STEP(mul(SA, lh, B22, ldb, M[4]));
-  STEP(add(A21, lda, -1.0, A11, lda, SA, lh)); STEP(add(B11, ldb, 1.0, B12, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[5]));
-  STEP(add(A12, lda, -1.0, A22, lda, SA, lh)); STEP(add(B21, ldb, 1.0, B22, ldb, SB, lh)); STEP(mul(SA, lh, SB, lh, M[6]));
-  // C11 = M1 + M4 - M5 + M7, C12 = M3 + M5, C21 = M2 + M4, C22 = M1 - M2 + M3 + M6
-  STEP(add(M[0], lh, 1.0, M[3], lh, C11, ldc)); STEP(add(C11, ldc, -1.0, M[4], lh, C11, ldc));
-  STEP(add(C11, ldc, 1.0, M[6], lh, C11, ldc));
-  STEP(add(M[2], lh, 1.0, M[4], lh, C12, ldc));
-  STEP(add(M[1], lh, 1.0, M[3], lh, C21, ldc));
-  STEP(add(M[0], lh, -1.0, M[1], lh, C22, ldc)); STEP(add(C22, ldc, 1.0, M[2], lh, C22, ldc));
-  STEP(add(C22, ldc, 1.0, M[5], lh, C22, ldc));
-#undef STEP
-  return st;
+  return cuda_fail(strassen_acc(n, 1.0, A, lda, B, ldb, 0.0, C, ldc, 1, 16, ws, s, &g_launches));
 }
 
 trinv_status_t trinv_gemm(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,

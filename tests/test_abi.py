@@ -62,6 +62,10 @@ def test_workspace_sizes():
     n = 32768
     P.set_product_engine()  # default: DMMA for every product
     assert P.product_engine() == "dmma"
+    assert P.strassen_levels() == 2  # default: Strassen in the top merge's dense quadrants (f3)
+    h = n // 4  # the top merge's quadrant order
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + 9 * (h // 2) ** 2 * 8 + 9 * (h // 4) ** 2 * 8
+    P.set_strassen(0)
     assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
     try:
         P.set_product_engine("int8crt")  # opt-in INT8 CRT engine for blocks >= 2048 adds its residue scratch
@@ -71,6 +75,7 @@ def test_workspace_sizes():
     finally:
         P.set_product_engine()
     assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8
+    P.set_strassen()
     assert ws(b"U", 1000, None, 1000, None, 1000) > 0
     # odd leading dimensions stage through the workspace
     assert ws(b"L", 999, None, 999, None, 999) > ws(b"L", 999, None, 1000, None, 1000)

@@ -21,7 +21,7 @@ def strassen(request):
     levels, min_h = request.param
     P.set_strassen(levels, min_h)
     yield levels
-    P.set_strassen(0)
+    P.set_strassen()  # library default
 
 
 @pytest.mark.parametrize("strassen", [(1, 64), (2, 64)], indirect=True)

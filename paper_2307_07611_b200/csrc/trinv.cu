@@ -1176,7 +1176,8 @@ trinv_status_t trinv_gemm_strassen(int64_t n, const double* A, int64_t lda, cons
   if (n == 0) return TRINV_OK;
   if (!A || !B || !C || lda < n || ldb < n || ldc < n) return TRINV_INVALID_ARG;
   if (n % 4 || !tma_ok(A, lda) || !tma_ok(B, ldb) || !tma_ok(C, ldc)) return TRINV_NOT_SUPPORTED;
-  if (ws_bytes < trinv_strassen_workspace_bytes(n) || !ws) return TRINV_WORKSPACE_TOO_SMALL;
+  const size_t need = trinv_strassen_workspace_bytes(n);
+  if (ws_bytes < need || (need > 0 && !ws)) return TRINV_WORKSPACE_TOO_SMALL;
   return cuda_fail(strassen_acc(n, 1.0, A, lda, B, ldb, 0.0, C, ldc, 1, 16, ws, s, &g_launches));
 }
 

@@ -38,6 +38,9 @@
 namespace trinv {
 
 constexpr int BK = 16;
+#ifndef LEVEL_GROUP
+#define LEVEL_GROUP 12  // K-classes per raster group of the level launches
+#endif
 
 // One output tile: where its operands come from and its K-range.  Only o_row /
 // o_col / g stay live across the main loop; everything else of the epilogue is
@@ -50,6 +53,7 @@ struct TileJob {
   int32_t k_begin, k_end;
   int32_t o_row, o_col, g;  // output tile origin (and batch index)
   int32_t m_row, m_col;     // mirror tile origin (zero fill, level modes 2), or -1
+  int32_t sem, chunk;       // split-K: the tile's semaphore index and this unit's K chunk (sem -1: unsplit)
   bool valid;
 };
 
@@ -77,27 +81,55 @@ struct LevelTraits {
     const int64_t b = p.b, n = p.n, merges = p.merges;
     const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
     int64_t g = 0, I = 0, J = 0;
+    // Tiles are ordered by their K-class (the tile index the K-range depends on), longest K
+    // first (an LPT schedule under the in-order CTA dispatch), and within a class group of
+    // LEVEL_GROUP classes the free index is the outer loop: a wave of ~148 CTAs then reads
+    // ~LEVEL_GROUP + 148 / LEVEL_GROUP operand panels instead of ~149 (grouped raster, L2
+    // reuse; the top-level TRMM of config 3 moved 124 GB of DRAM with the class-major order).
+    const bool cls_is_j = p.mode == MODE_LOWER_1 || p.mode == MODE_UPPER_2;
+    const int64_t Tc = cls_is_j ? TNmax : TMmax, Tf = cls_is_j ? TMmax : TNmax;
+    int64_t chunk = -1;
+    // K-length of a class (split-K levels have full merges, r = b)
+    auto cls_len = [&](int64_t cc) -> int64_t {
+      switch (p.mode) {
+        case MODE_LOWER_1: return b - cc * BN;
+        case MODE_UPPER_1: return b - cc * BM;
+        case MODE_LOWER_2: return (cc + 1) * BM < b ? (cc + 1) * BM : b;
+        default: return (cc + 1) * BN < b ? (cc + 1) * BN : b;
+      }
+    };
+    if (p.kchunk > 0) {  // split-K: classes in dispatch order, each tile's chunks consecutive
+      const int64_t kc = p.kchunk;
+      int64_t c = 0, cc = 0, nc = 1, rem = t;
+      for (; c < Tc; ++c) {
+        cc = (p.mode == MODE_LOWER_2 || p.mode == MODE_UPPER_2) ? Tc - 1 - c : c;
+        nc = (cls_len(cc) + kc - 1) / kc;
+        const int64_t cnt = merges * Tf * nc;
+        if (rem < cnt) break;
+        rem -= cnt;
+      }
+      const int64_t tl = rem / nc;
+      chunk = rem % nc;
+      g = tl / Tf;
+      const int64_t f = tl % Tf;
+      if (cls_is_j) { J = cc; I = f; } else { I = cc; J = f; }
+      j.sem = (int32_t)((g * Tc + cc) * Tf + f);
+    } else if (p.mode != MODE_UL) {
+      // small levels (operands L2-resident) keep the exact class-major LPT order (G = 1)
+      const int64_t G = b >= 8192 ? LEVEL_GROUP : 1;
+      const int64_t per_cls = merges * Tf, cg = t / (per_cls * G);
+      const int64_t gsz = Tc - cg * G < G ? Tc - cg * G : G;
+      const int64_t local = t - cg * per_cls * G;
+      g = local / (Tf * gsz);
+      const int64_t l2 = local % (Tf * gsz);
+      const int64_t f = l2 / gsz, c = cg * G + l2 % gsz;
+      // ascending class = longest K first for LOWER_1 (k >= J) / UPPER_1 (k >= I); LOWER_2 /
+      // UPPER_2 have k < (I+1) / (J+1): descending
+      const int64_t cc = (p.mode == MODE_LOWER_2 || p.mode == MODE_UPPER_2) ? Tc - 1 - c : c;
+      if (cls_is_j) { J = cc; I = f; } else { I = cc; J = f; }
+    }
     switch (p.mode) {
-      case MODE_LOWER_1: {  // J ascending
-        J = t / (merges * TMmax);
-        const int64_t rem = t % (merges * TMmax);
-        g = rem / TMmax; I = rem % TMmax;
-      } break;
-      case MODE_LOWER_2: {  // I descending
-        I = TMmax - 1 - t / (merges * TNmax);
-        const int64_t rem = t % (merges * TNmax);
-        g = rem / TNmax; J = rem % TNmax;
-      } break;
-      case MODE_UPPER_1: {  // I ascending
-        I = t / (merges * TNmax);
-        const int64_t rem = t % (merges * TNmax);
-        g = rem / TNmax; J = rem % TNmax;
-      } break;
-      case MODE_UPPER_2: {  // J descending
-        J = TNmax - 1 - t / (merges * TMmax);
-        const int64_t rem = t % (merges * TMmax);
-        g = rem / TMmax; I = rem % TMmax;
-      } break;
+      case MODE_LOWER_1: case MODE_LOWER_2: case MODE_UPPER_1: case MODE_UPPER_2: break;
       default: {  // MODE_UL: max(I, J) ascending
         int64_t m = (int64_t)sqrt((double)t);
         while (m * m > t) --m;
@@ -111,6 +143,7 @@ struct LevelTraits {
     j.valid = true;
     j.m_row = j.m_col = -1;
     j.g = 0; j.ga = j.gb = 0;
+    const int32_t sem = p.kchunk > 0 ? j.sem : -1;
     switch (p.mode) {
       case MODE_LOWER_1:
         j.valid = I * BM < r;
@@ -149,8 +182,16 @@ struct LevelTraits {
         j.k_begin = (int32_t)((I * BM > J * BN) ? I * BM : J * BN); j.k_end = (int32_t)n;
         break;
     }
+    j.sem = sem;
+    j.chunk = (int32_t)(chunk < 0 ? 0 : chunk);
+    if (sem >= 0) {  // this unit's K chunk of the tile's range
+      const int32_t kb = j.k_begin + j.chunk * p.kchunk;
+      j.k_end = kb + p.kchunk < j.k_end ? kb + p.kchunk : j.k_end;
+      j.k_begin = kb;
+    }
     return j;
   }
+  static __device__ __forceinline__ int* sync(const LevelArgs& p) { return p.kchunk > 0 ? p.sync : nullptr; }
   static __device__ __forceinline__ double* out(const LevelArgs& p, const TileJob& j) {
     return p.out + (int64_t)j.o_row * p.ldo + j.o_col;
   }
@@ -194,6 +235,7 @@ struct GemmTraits {
     j.k_begin = (int32_t)kb; j.k_end = (int32_t)(ke > kb ? ke : kb);
     j.o_row = (int32_t)(I * BM); j.o_col = (int32_t)(J * BN);
     j.m_row = j.m_col = -1;
+    j.sem = -1; j.chunk = 0;
     return j;
   }
   static __device__ __forceinline__ double* out(const GemmArgs& p, const TileJob& j) {
@@ -207,6 +249,7 @@ struct GemmTraits {
   static __device__ __forceinline__ double* mir(const GemmArgs&) { return nullptr; }
   static __device__ __forceinline__ int64_t ldm(const GemmArgs&) { return 0; }
   static __device__ __forceinline__ int64_t n(const GemmArgs&) { return 0; }
+  static __device__ __forceinline__ int* sync(const GemmArgs&) { return nullptr; }
 };
 
 // ---------------------------------------------------------------------------
@@ -214,7 +257,15 @@ template <int BM, int BN, int WM, int WN, int STAGES, int RANK, typename TR>
 __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensorMap* mapB,
                                          const typename TR::Params& p, unsigned char* smem_raw) {
   using C = GemmCfg<BM, BN, WM, WN, STAGES>;
-  const TileJob tj = TR::template job<BM, BN>(p, blockIdx.x);
+  // split-K levels take their work unit from an in-order ticket (a unit is handed out only
+  // after every earlier unit has a running CTA, so a chunk never waits on an unscheduled one)
+  __shared__ int s_unit;
+  int* sync = TR::sync(p);
+  if (sync) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(sync, 1);
+    __syncthreads();
+  }
+  const TileJob tj = TR::template job<BM, BN>(p, sync ? (int64_t)s_unit : (int64_t)blockIdx.x);
   if (!tj.valid) return;
   // align by offsetting the __shared__ pointer itself (an integer round trip would turn
   // the fragment loads into generic LD instead of LDS)
@@ -269,7 +320,7 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   }
 
   // ---------------- consumers ----------------
-  if (tj.m_row >= 0) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
+  if (tj.m_row >= 0 && tj.chunk == 0) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
     const int64_t nn = TR::n(p), ldm = TR::ldm(p);
     double* mir = TR::mir(p) + (int64_t)tj.m_row * ldm + tj.m_col;
     constexpr int PAIRS = BM / 2;
@@ -318,7 +369,22 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   // ---------------- epilogue: out = alpha * acc (+ beta * out), clipped ----------------
   double* out = TR::out(p, tj);
   const int64_t ldo = TR::ldo(p), rows = TR::rows_left(p, tj), cols = TR::cols_left(p, tj);
-  const double alpha = TR::alpha(p), beta = TR::beta(p);
+  const double alpha = TR::alpha(p);
+  double beta = TR::beta(p);
+  int* sem = nullptr;
+  if (tj.sem >= 0) {  // split-K: add this chunk's partial after chunk - 1 has stored its sum
+    sem = sync + 1 + tj.sem;
+    if (tj.chunk > 0) {
+      if (lane == 0) {
+        int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(sem) : "memory");
+        } while (v < tj.chunk);
+      }
+      __syncwarp();
+      beta = 1.0;
+    }
+  }
   // 16-byte stores need an even leading dimension and an aligned tile origin
   const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (ldo % 2 == 0);
 #pragma unroll
@@ -332,16 +398,21 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
       double v0 = alpha * acc[mi][ni][0], v1 = alpha * acc[mi][ni][1];
       if (col + 1 < cols && vec) {
         if (beta != 0.0) {
-          const double2 o = *reinterpret_cast<const double2*>(orow + col);
+          const double2 o = __ldcg(reinterpret_cast<const double2*>(orow + col));
           v0 = fma(beta, o.x, v0);
           v1 = fma(beta, o.y, v1);
         }
         *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
       } else {
-        if (col < cols) orow[col] = (beta != 0.0) ? fma(beta, orow[col], v0) : v0;
-        if (col + 1 < cols) orow[col + 1] = (beta != 0.0) ? fma(beta, orow[col + 1], v1) : v1;
+        if (col < cols) orow[col] = (beta != 0.0) ? fma(beta, __ldcg(orow + col), v0) : v0;
+        if (col + 1 < cols) orow[col + 1] = (beta != 0.0) ? fma(beta, __ldcg(orow + col + 1), v1) : v1;
       }
     }
+  }
+  if (sem) {  // every consumer warp has stored: release the next chunk
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sem), "r"(tj.chunk + 1) : "memory");
   }
 }
 
@@ -363,13 +434,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
 
 // ---------------------------------------------------------------------------
 template <int BM, int BN, int WM, int WN, int STAGES>
-static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches, int64_t units = 0) {
   using C = GemmCfg<BM, BN, WM, WN, STAGES>;
   CUtensorMap mA, mB;
   if (!encode_map(&mA, a.opA, 4, BM, false)) return cudaErrorInvalidValue;
   if (!encode_map(&mB, a.opB, 4, BK, false)) return cudaErrorInvalidValue;
   int64_t tiles;
-  if (a.mode == MODE_UL) {
+  if (units > 0) {
+    tiles = units;  // split-K work units
+  } else if (a.mode == MODE_UL) {
     const int64_t T = (a.n + BM - 1) / BM;
     tiles = T * T;
   } else {
@@ -415,8 +488,46 @@ static int64_t pick_tile(F tiles, int64_t cap) {
   return cap < 32 ? cap : 32;
 }
 
-cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches) {
+// Split-K for levels that would underfill the GPU with 64x64 tiles (mid-size orders: at
+// n = 2048 the top level had 256 such tiles of K up to 1024, so it runs on 32x32 tiles at
+// 63% of the DMMA peak): 64x64 tiles with their K ranges cut into chunks, about 3 work units
+// per SM, the chunks of a tile summed in order (LevelArgs::sync).  Full merges only.
+// Opt-in (TRINV_SPLITK=1): it measured 1.1-1.8x SLOWER than the unsplit 32x32 tiles at
+// n = 1024..8192 (the per-level semaphore memset and the serial chunk epilogues cost more
+// than the better tiles gain; profiles/r02_splitk.txt).
+static int64_t split_plan(const LevelArgs& a, int64_t& kc) {
+  constexpr int64_t T = 64;
+  const int sms = device_sms();
+  if (!a.sync || a.mode == MODE_UL || a.b < 256 || a.n % (2 * a.b) != 0 || a.b % T) return 0;
+  const int64_t Tc = a.b / T, tiles = a.merges * Tc * Tc;
+  if (tiles >= 2 * sms || 1 + tiles > (int64_t)(LEVEL_SYNC_BYTES / sizeof(int))) return 0;
+  auto len = [&](int64_t c) {  // K length of class c (all modes: b - c T or (c + 1) T)
+    return (a.mode == MODE_LOWER_1 || a.mode == MODE_UPPER_1) ? a.b - c * T : (c + 1) * T;
+  };
+  int64_t total = 0;
+  for (int64_t c = 0; c < Tc; ++c) total += a.merges * Tc * len(c);
+  kc = (total / (3 * sms) + 63) / 64 * 64;
+  if (kc < 128) kc = 128;
+  int64_t units = 0;
+  for (int64_t c = 0; c < Tc; ++c) units += a.merges * Tc * ((len(c) + kc - 1) / kc);
+  return units > tiles ? units : 0;
+}
+
+cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launches) {
+  LevelArgs a = a_in;
   ProfileScope prof(KIND_DMMA, level_flops(a), 0.0, s);
+  a.kchunk = 0;
+  // measured slower at every order (profiles/r02_splitk.txt): opt-in experiment, TRINV_SPLITK=1
+  static const bool split_on = [] { const char* e = std::getenv("TRINV_SPLITK"); return e && atoi(e) != 0; }();
+  int64_t kc = 0;
+  const int64_t units = split_on ? split_plan(a, kc) : 0;
+  if (units > 0) {
+    const int64_t tiles = a.merges * (a.b / 64) * (a.b / 64);
+    cudaError_t e = cudaMemsetAsync(a.sync, 0, (size_t)(1 + tiles) * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    a.kchunk = (int32_t)kc;
+    return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches, units);
+  }
   auto tiles = [&](int64_t T) {
     if (a.mode == MODE_UL) { const int64_t m = (a.n + T - 1) / T; return m * m; }
     const int64_t m = (a.b + T - 1) / T;

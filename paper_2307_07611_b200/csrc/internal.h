@@ -88,7 +88,14 @@ struct LevelArgs {
   double* mir;      // matrix whose mirrored tile is zero-filled (LOWER_2/UPPER_2), else NULL
   int64_t ldm;
   double alpha;
+  // split-K (launch_level sets these): NULL / 0 = one CTA per output tile.  Else every tile's
+  // K range is cut into chunks of kchunk; chunk c of a tile adds its partial product to the
+  // tile after chunk c-1 has (a per-tile semaphore in sync[1..], a ticket counter in sync[0]
+  // hands out work units in order): deterministic summation order.
+  int* sync;        // LEVEL_SYNC_BYTES of device scratch (caller-provided), or NULL
+  int32_t kchunk;
 };
+constexpr size_t LEVEL_SYNC_BYTES = 16384;  // ticket + up to 4095 tile semaphores
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
 
 // General batched GEMM on the same engine: for g < batch,

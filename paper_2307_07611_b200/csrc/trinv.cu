@@ -438,7 +438,7 @@ static bool strassen_ul(int64_t n) {
 
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
-  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n);
+  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES;
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
   return bytes;
@@ -524,9 +524,12 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
 
 // Core recursion on an aligned, even-ld problem (or n <= 32 in any layout).
 // info: NULL or a single accumulator already initialised by the caller.
+// aux: NULL, or the public entry's scratch after W and the INT8 scratch: [Strassen scratch |
+// LEVEL_SYNC_BYTES of split-K tickets / semaphores]; without it the top merge stays on the
+// level launches and no level is split along K (callers with their own workspace layout).
 static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda, double* X, int64_t ldx,
                               int unit, double* W, int32_t* info, int64_t info_off, cudaStream_t s,
-                              int64_t b_stop = 0) {
+                              int64_t b_stop = 0, void* aux = nullptr) {
   if (n <= BLK_MAX && b_stop == 0) {  // one block of order n (BASELINE config 0): a single launch
     LeafArgs l1{};
     l1.A = A; l1.lda = lda; l1.sA = n * lda; l1.X = X; l1.ldx = ldx; l1.sX = n * ldx;
@@ -576,10 +579,12 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       l1.mode = MODE_UPPER_1; l1.opA = xr; l1.opB = in;
       l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
     }
-    if (b_stop == 0 && strassen_top(n, b)) {  // NEXT f3: the top merge with Strassen's dense quadrants
-      void* sws = reinterpret_cast<char*>(W) + align_up(w_bytes(n)) + oz_scratch(n);
-      TRY(strassen_merge(uplo, n, A, lda, X, ldx, W, sws, s));
+    if (aux && b_stop == 0 && strassen_top(n, b)) {  // NEXT f3: the top merge with Strassen's dense quadrants
+      TRY(strassen_merge(uplo, n, A, lda, X, ldx, W, aux, s));
       continue;
+    }
+    if (aux) {  // split-K tickets / semaphores (launch_level zeroes them when it splits)
+      l1.sync = l2.sync = reinterpret_cast<int*>(static_cast<char*>(aux) + strassen_scratch(n));
     }
     if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
       void* ozws0 = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
@@ -674,7 +679,8 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
 
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
-  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n);  // W, then run_tri's scratch
+  void* aux = p + align_up(w_bytes(n)) + oz_scratch(n);                               // run_tri's aux scratch
+  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES;  // then staging
   const double* Ause = A;
   int64_t lda_use = lda;
   if (!tma_ok(A, lda)) {  // stage the input into an even-ld, aligned copy
@@ -691,7 +697,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
     Xuse = reinterpret_cast<double*>(p);
     ldx_use = even_up(n);
   }
-  st = run_tri(uplo, n, Ause, lda_use, Xuse, ldx_use, diag, W, info, info_off, s);
+  st = run_tri(uplo, n, Ause, lda_use, Xuse, ldx_use, diag, W, info, info_off, s, 0, aux);
   if (st != TRINV_OK) return st;
   if (stage_x) TRY(launch_copy_2d(Xuse, ldx_use, X, ldx, n, n, s, &g_launches));
   return TRINV_OK;

@@ -533,7 +533,10 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
     const int64_t m = (a.b + T - 1) / T;
     return a.merges * m * m;
   };
-  const int64_t t = pick_tile(tiles, a.mode == MODE_UL ? 128 : a.b);
+  // TRINV_LEVEL_TILE = 32 / 64 / 128 forces the tile of the level launches (experiments)
+  static const int64_t forced = [] { const char* e = std::getenv("TRINV_LEVEL_TILE"); return e ? atoll(e) : 0; }();
+  int64_t t = pick_tile(tiles, a.mode == MODE_UL ? 128 : a.b);
+  if (forced >= 32 && (a.mode == MODE_UL || forced <= a.b)) t = forced;
   if (t >= 128) return launch_level_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches);
   return launch_level_cfg<32, 32, 2, 2, 4>(a, s, launches);

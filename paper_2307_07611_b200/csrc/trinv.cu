@@ -906,8 +906,11 @@ static size_t lu_oz_ws(int64_t n) {
   return best;
 }
 // ozws: two CRT scratches of ozhalf bytes each, one per stream (nullptr: DMMA only)
+// sws: NULL or the Strassen scratch of the top Schur update (lu_strassen_scratch): dense square
+// Schur updates of order >= the Strassen threshold run strassen_acc (NEXT f3).
 static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, double* Ui, int64_t ld, double* T,
-                                 int32_t* info, int64_t info_off, cudaStream_t s, void* ozws, size_t ozhalf) {
+                                 int32_t* info, int64_t info_off, cudaStream_t s, void* ozws, size_t ozhalf,
+                                 void* sws = nullptr) {
   ForkCtx* fc = nullptr;
   TRY(fork_ctx(&fc));
   if (n <= LU_MAX) {
@@ -941,17 +944,22 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   static const bool fork_on = [] { const char* e = std::getenv("TRINV_LU_FORK"); return !(e && e[0] == '0'); }();
   const bool par = fork_on;
   cudaStream_t s2 = par ? fc->aux : s;
-  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws, ozhalf);  // A11 = L11 U11, K11, S11
+  trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws, ozhalf, sws);  // A11 = L11 U11, K11, S11
   if (st != TRINV_OK) return st;
   // U12 = K11 A12 (K11 lower) || L21 = A21 S11 (S11 upper); Schur W22 <- A22 - L21 U12
   if (par) TRY(fork_to(fc, s));
   if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0, s))) return st;
   if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0, s2))) return st;
   if (par) TRY(join_from(fc, s));
-  if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0, s)))
+  if (sws && r == h && !(ozws && lu_gemm_on_int8(r, r, h)) && strassen_ul(2 * h)) {  // W22 -= L21 U12 by Strassen
+    TRY(strassen_acc(h, -1.0, blk(F, h, 0), ld, blk(F, 0, h), ld, 1.0, blk(W, h, h), ld, strassen_levels(),
+                     strassen_min_q(), sws, s, &g_launches));
+  } else if ((st = gemm(r, r, h, blk(F, h, 0), ld, TRI_NONE, blk(F, 0, h), ld, TRI_NONE, blk(W, h, h), ld, -1.0, 1.0,
+                        s))) {
     return st;
+  }
   st = lu_inv_rec(r, blk(W, h, h), blk(F, h, h), blk(Li, h, h), blk(Ui, h, h), ld, T, info, info_off + h, s, ozws,
-                  ozhalf);
+                  ozhalf, sws);
   if (st != TRINV_OK) return st;
   const int64_t lth = even_up(h), ltr = even_up(r);
   if (par) TRY(fork_to(fc, s));
@@ -1032,6 +1040,7 @@ size_t trinv_workspace_bytes(char op, int64_t n, const void* A, int64_t lda, con
     size_t bytes = 4 * align_up(mat_bytes(n)) + align_up(lu_inv_scratch(n));
     if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
     bytes += std::max(2 * lu_oz_ws(n), ul_on_int8(n) ? align_up(oz2_workspace_bytes(n, n, n)) : (size_t)0);
+    bytes += ul_strassen_scratch(n);  // Strassen: the top Schur update and S K (h = n/2 both)
     (void)A; (void)lda;
     return bytes;
   }
@@ -1251,11 +1260,16 @@ trinv_status_t inv_general(int64_t n, const double* A, int64_t lda, double* X, i
   if (d_info) TRY(cudaMemsetAsync(d_info, 0, sizeof(int32_t), s));
   TRY(launch_copy_2d(A, lda, Wk, lde, n, n, s, &g_launches));
   // A = L U (U unit, Crout) with K = L^{-1}, S = U^{-1} alongside (SKUL)
-  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, lu_oz_ws(n) ? ozws : nullptr, lu_oz_ws(n));
+  void* sws = ul_strassen_scratch(n) ? static_cast<void*>(take(ul_strassen_scratch(n))) : nullptr;
+  trinv_status_t st = lu_inv_rec(n, Wk, F, Li, Ui, lde, T, d_info, 0, s, lu_oz_ws(n) ? ozws : nullptr, lu_oz_ws(n),
+                                 sws);
   if (st != TRINV_OK) return st;
   // A^{-1} = S K = U^{-1} L^{-1}: X_ij = sum_{k >= max(i,j)} S_ik K_kj (P_UL)
   if (ul_on_int8(n) && !int8_veto()) {
     TRY(launch_oz2_ul(n, Ui, lde, Li, lde, Xuse, ldx_use, ozws, s, &g_launches));
+  } else if (sws) {  // NEXT f3: S K by quadrants, S12 K21 by Strassen
+    st = ul_strassen(n, Ui, Li, lde, Xuse, ldx_use, sws, s);
+    if (st != TRINV_OK) return st;
   } else {
     LevelArgs ul{};
     ul.mode = MODE_UL; ul.n = n; ul.b = n; ul.merges = 1;

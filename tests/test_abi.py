@@ -64,9 +64,10 @@ def test_workspace_sizes():
     assert P.product_engine() == "dmma"
     assert P.strassen_levels() == 2  # default: Strassen in the top merge's dense quadrants (f3)
     h = n // 4  # the top merge's quadrant order
-    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + 9 * (h // 2) ** 2 * 8 + 9 * (h // 4) ** 2 * 8
+    sync = 16384  # split-K tickets / semaphores (LEVEL_SYNC_BYTES)
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + 9 * (h // 2) ** 2 * 8 + 9 * (h // 4) ** 2 * 8 + sync
     P.set_strassen(0)
-    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8  # W = one (n/2)^2 block
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + sync  # W = one (n/2)^2 block
     try:
         P.set_product_engine("int8crt")  # opt-in INT8 CRT engine for blocks >= 2048 adds its residue scratch
         h = n // 2
@@ -74,7 +75,7 @@ def test_workspace_sizes():
         assert P.product_engine() == "int8crt"
     finally:
         P.set_product_engine()
-    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + sync
     P.set_strassen()
     assert ws(b"U", 1000, None, 1000, None, 1000) > 0
     # odd leading dimensions stage through the workspace

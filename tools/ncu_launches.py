@@ -20,7 +20,7 @@ def main(path, cmd):
         v = float(r[vi].replace(",", ""))
         scale = {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(r[ui], 1)
         name = r[ki].split("(")[0]
-        print(f'{r[ii]},{name},"{r[gi]}","{r[bi]}",{int(v * scale)}')
+        print(f'{r[ii]},"{name}","{r[gi]}","{r[bi]}",{int(v * scale)}')
 
 
 if __name__ == "__main__":

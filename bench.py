@@ -211,7 +211,8 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     value = work / dt
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg["kind"] == "B" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg["workload"], "n": cfg["n"]},
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": what},

@@ -260,6 +260,10 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   // split-K levels take their work unit from an in-order ticket (a unit is handed out only
   // after every earlier unit has a running CTA, so a chunk never waits on an unscheduled one)
   __shared__ int s_unit;
+  // PDL: let the next kernel's CTAs be scheduled as this grid drains, and wait for the
+  // previous kernel before touching global memory (no-ops without the launch attribute)
+  pdl_launch_dependents();
+  pdl_wait();
   int* sync = TR::sync(p);
   if (sync) {
     if (threadIdx.x == 0) s_unit = atomicAdd(sync, 1);
@@ -452,9 +456,9 @@ static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t*
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
   set_smem_once<k>((int)C::SMEM);
-  k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
+  const cudaError_t e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
   if (launches) ++*launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Algorithmic flops of one level launch, exploiting the triangular operand
@@ -479,12 +483,16 @@ static double level_flops(const LevelArgs& a) {
 // Tile size: the largest of 128 / 64 / 32 (not above `cap`) giving at least two
 // CTAs per SM; mid-size problems otherwise leave SMs idle behind a few long
 // tiles (profiles/r01_sweep_n.txt).
+// 128x128 tiles only when they make at least TRINV_LEVEL_W128 (default 32) waves: the 64x64
+// tiles balance the triangular K ranges better (n = 8192: 5553 -> 5305 us, config 3 317.0 ->
+// 316.0 ms, config 4 164.2 -> 162.6 ms against the round-1 threshold of 2 waves,
+// profiles/r02_tile_waves.txt).
 template <typename F>
 static int64_t pick_tile(F tiles, int64_t cap) {
   const int sms = device_sms();
-  for (int64_t T : {128, 64}) {
-    if (T <= cap && tiles(T) >= 2 * sms) return T;
-  }
+  static const double w128 = [] { const char* e = std::getenv("TRINV_LEVEL_W128"); return e ? atof(e) : 32.0; }();
+  if (128 <= cap && tiles(128) >= w128 * sms) return 128;
+  if (64 <= cap && tiles(64) >= 2 * sms) return 64;
   return cap < 32 ? cap : 32;
 }
 
@@ -560,9 +568,9 @@ static cudaError_t launch_gemm_cfg(const GemmArgs& a, cudaStream_t s, int64_t* l
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   constexpr auto k = dmma_gemm_kernel<BM, BN, WM, WN, STAGES>;
   set_smem_once<k>((int)C::SMEM);
-  k<<<(unsigned)tiles, C::kThreads, C::SMEM, s>>>(mA, mB, a);
+  const cudaError_t e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
   if (launches) ++*launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 double gemm_flops(const GemmArgs& a) {
@@ -587,9 +595,13 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   // tiles per SM required before a larger tile is taken (experiments: TRINV_GEMM_WAVES)
   static const double waves = [] { const char* e = std::getenv("TRINV_GEMM_WAVES"); return e ? std::atof(e) : 2.0; }();
   auto tiles = [&](int64_t T) { return a.batch * ((a.M + T - 1) / T) * ((a.N + T - 1) / T); };
+  // TRINV_GEMM_W128: waves of 128x128 tiles required before they are preferred to 64x64
+  // (default 32, as for the level launches: config 4 162.5 -> 161.2 ms, configs 2 / 3
+  // unchanged; profiles/r02_pdl.txt)
+  static const double w128 = [] { const char* e = std::getenv("TRINV_GEMM_W128"); return e ? atof(e) : 32.0; }();
   int64_t t = 32;
-  for (int64_t T : {128, 64})
-    if (tiles(T) >= (int64_t)(waves * device_sms())) { t = T; break; }
+  if (tiles(128) >= (int64_t)(w128 * device_sms())) t = 128;
+  else if (tiles(64) >= (int64_t)(waves * device_sms())) t = 64;
   if (t >= 128) return launch_gemm_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_gemm_cfg<64, 64, 2, 2, 4>(a, s, launches);
   return launch_gemm_cfg<32, 32, 2, 2, 4>(a, s, launches);
@@ -598,6 +610,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
 // ---------------------------------------------------------------------------
 // rows over blockIdx.y (grid-strided), columns over blockIdx.x / threads: no division per entry
 __global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     double* r = p + i * ld;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols; j += (int64_t)gridDim.x * blockDim.x)
@@ -661,7 +675,8 @@ cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cu
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const int64_t gx = std::min<int64_t>((cols + 255) / 256, 64);
   const int64_t gy = std::min<int64_t>(rows, std::max<int64_t>(1, (int64_t)device_sms() * 16 / gx));
-  zero_2d_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(p, ld, rows, cols);
+  const cudaError_t e = launch_k(zero_2d_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, p, ld, rows, cols);
+  if (e != cudaSuccess) return e;
   if (launches) ++*launches;
   return cudaGetLastError();
 }

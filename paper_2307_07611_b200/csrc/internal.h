@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <utility>
 #include <atomic>
 #include <cstdint>
 
@@ -159,6 +160,27 @@ size_t strassen_ws_bytes(int64_t h, int levels, int64_t min_q);
 cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                          double beta, double* C, int64_t ldc, int levels, int64_t min_q, void* ws, cudaStream_t s,
                          int64_t* launches);
+
+// Programmatic dependent launch: launch `k` on `s` with the programmatic stream
+// serialization attribute when pdl_enabled() (TRINV_PDL=1, default off), so that its CTAs are
+// scheduled while the previous kernel's last wave drains; `k` must call pdl_wait() before
+// touching global memory the previous kernel produces or consumes.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // Host helper: encode a 2-D FP64 tensor map (cuTensorMapEncodeTiled through the
 // runtime's driver entry point).  Returns false on failure.

@@ -105,4 +105,14 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// ---- programmatic dependent launch (PDL) --------------------------------------
+// launch_dependents: this CTA no longer holds back the launch of the next kernel in the
+// stream (when that kernel was launched with the programmatic-serialization attribute);
+// wait: block until the previous kernel in the stream has completed and its memory is
+// visible.  Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 }  // namespace trinv

@@ -14,6 +14,7 @@
 #include <initializer_list>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace trinv {
 
@@ -26,6 +27,8 @@ struct LinComb {
 
 // C[i][j] = beta C[i][j] + sum_t c_t X_t[i][j]  (beta == 0: C not read)
 __global__ void lincomb_kernel(int64_t rows, int64_t cols, double beta, double* C, int64_t ldc, const LinComb t) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     for (int64_t j = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); j < cols;
          j += 2 * (int64_t)gridDim.x * blockDim.x) {
@@ -60,9 +63,9 @@ static cudaError_t lincomb(int64_t n, double beta, double* C, int64_t ldc, std::
   const int threads = 256;
   const int64_t bx = (n / 2 + threads - 1) / threads;
   const dim3 grid((unsigned)(bx < 8 ? bx : 8), (unsigned)(n < 65535 ? n : 65535));
-  lincomb_kernel<<<grid, threads, 0, s>>>(n, n, beta, C, ldc, t);
+  const cudaError_t e = launch_k(lincomb_kernel, grid, dim3(threads), 0, s, n, n, beta, C, ldc, t);
   if (launches) ++*launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 static int64_t even_up2(int64_t x) { return (x + 1) & ~int64_t(1); }

@@ -24,6 +24,14 @@
 
 namespace trinv {
 
+// Programmatic dependent launch of the product / combination kernels (internal.h launch_k):
+// opt-in (TRINV_PDL=1).  Measured slower on graph-replayed calls (n = 2048: 165 -> 198 us,
+// n = 4096: 801 -> 868 us; profiles/r02_pdl.txt), so the launches stay stream-serialised.
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = std::getenv("TRINV_PDL"); return e && e[0] == '1'; }();
+  return on;
+}
+
 static thread_local int g_last_cuda_error = 0;
 static thread_local int64_t g_launches = 0;
 

@@ -91,3 +91,23 @@ def test_strassen_config4(strassen):
     R = oracle.lu_columns(L, U, cols, unit_l=True)
     assert oracle.floored_rel_err(Xs, R, axis_cols=0) <= REL_TOL
     assert oracle.factored_column_residual_ratio(L, U, Xs, cols) <= RES_TOL
+
+
+@pytest.mark.parametrize("strassen", [(2, 64)], indirect=True)
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_strassen_with_staged_layouts(strassen, uplo):
+    """Odd leading dimensions make the call stage A and X through the workspace, after W and
+    the Strassen scratch: the three regions must not overlap (round 2 fixed an overlap of the
+    staging copies with the INT8 scratch).  NaN in the padding columns must not leak."""
+    n, ld = 1024, 1027
+    T = synth.host(n, seed=21, uplo=uplo, diag="signed" if uplo == "L" else "pos")
+    big = np.full((n, ld), np.nan)
+    big[:, :n] = T
+    Ad = torch.from_numpy(big).to(DEV)[:, :n]
+    Xbig = torch.full((n, ld), float("nan"), dtype=torch.float64, device=DEV)
+    Xd = Xbig[:, :n]
+    f = P.trinv_lower if uplo == "L" else P.trinv_upper
+    f(Ad, out=Xd)
+    X = Xd.cpu().numpy()
+    check_full(T, X, uplo)
+    assert np.all(np.isnan(Xbig[:, n:].cpu().numpy()))  # padding untouched

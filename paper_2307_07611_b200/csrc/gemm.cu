@@ -503,19 +503,19 @@ static int64_t pick_tile(F tiles, int64_t cap) {
 // Opt-in (TRINV_SPLITK=1): it measured 1.1-1.8x SLOWER than the unsplit 32x32 tiles at
 // n = 1024..8192 (the per-level semaphore memset and the serial chunk epilogues cost more
 // than the better tiles gain; profiles/r02_splitk.txt).
-static int64_t split_plan(const LevelArgs& a, int64_t& kc) {
-  constexpr int64_t T = 64;
+static int64_t split_plan(const LevelArgs& a, int64_t& kc, int64_t T) {
   const int sms = device_sms();
   if (!a.sync || a.mode == MODE_UL || a.b < 256 || a.n % (2 * a.b) != 0 || a.b % T) return 0;
   const int64_t Tc = a.b / T, tiles = a.merges * Tc * Tc;
-  if (tiles >= 2 * sms || 1 + tiles > (int64_t)(LEVEL_SYNC_BYTES / sizeof(int))) return 0;
+  if ((T == 64 && tiles >= 2 * sms) || 1 + tiles > (int64_t)(LEVEL_SYNC_BYTES / sizeof(int))) return 0;
   auto len = [&](int64_t c) {  // K length of class c (all modes: b - c T or (c + 1) T)
     return (a.mode == MODE_LOWER_1 || a.mode == MODE_UPPER_1) ? a.b - c * T : (c + 1) * T;
   };
   int64_t total = 0;
   for (int64_t c = 0; c < Tc; ++c) total += a.merges * Tc * len(c);
-  kc = (total / (3 * sms) + 63) / 64 * 64;
-  if (kc < 128) kc = 128;
+  static const int64_t kc_env = [] { const char* e = std::getenv("TRINV_SPLITK_KC"); return e ? atoll(e) : 0; }();
+  kc = kc_env > 0 ? kc_env : (total / (3 * sms) + 63) / 64 * 64;
+  if (kc < 64) kc = 64;
   int64_t units = 0;
   for (int64_t c = 0; c < Tc; ++c) units += a.merges * Tc * ((len(c) + kc - 1) / kc);
   return units > tiles ? units : 0;
@@ -527,13 +527,16 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
   a.kchunk = 0;
   // measured slower at every order (profiles/r02_splitk.txt): opt-in experiment, TRINV_SPLITK=1
   static const bool split_on = [] { const char* e = std::getenv("TRINV_SPLITK"); return e && atoi(e) != 0; }();
+  static const int64_t split_t = [] { const char* e = std::getenv("TRINV_SPLITK_T"); return e ? atoll(e) : 64; }();
   int64_t kc = 0;
-  const int64_t units = split_on ? split_plan(a, kc) : 0;
+  const int64_t units = split_on ? split_plan(a, kc, split_t == 32 ? 32 : 64) : 0;
   if (units > 0) {
-    const int64_t tiles = a.merges * (a.b / 64) * (a.b / 64);
+    const int64_t T = split_t == 32 ? 32 : 64;
+    const int64_t tiles = a.merges * (a.b / T) * (a.b / T);
     cudaError_t e = cudaMemsetAsync(a.sync, 0, (size_t)(1 + tiles) * sizeof(int), s);
     if (e != cudaSuccess) return e;
     a.kchunk = (int32_t)kc;
+    if (T == 32) return launch_level_cfg<32, 32, 2, 2, 4>(a, s, launches, units);
     return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches, units);
   }
   auto tiles = [&](int64_t T) {

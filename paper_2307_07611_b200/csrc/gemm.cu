@@ -54,6 +54,8 @@ struct TileJob {
   int32_t o_row, o_col, g;  // output tile origin (and batch index)
   int32_t m_row, m_col;     // mirror tile origin (zero fill, level modes 2), or -1
   int32_t sem, chunk;       // split-K: the tile's semaphore index and this unit's K chunk (sem -1: unsplit)
+  int32_t lg, li, lj;       // level launches: merge and tile indices
+  int32_t phase;            // fused level launches: 0 = first product (W), 1 = second
   bool valid;
 };
 
@@ -184,6 +186,7 @@ struct LevelTraits {
     }
     j.sem = sem;
     j.chunk = (int32_t)(chunk < 0 ? 0 : chunk);
+    j.lg = (int32_t)g; j.li = (int32_t)I; j.lj = (int32_t)J; j.phase = 0;
     if (sem >= 0) {  // this unit's K chunk of the tile's range
       const int32_t kb = j.k_begin + j.chunk * p.kchunk;
       j.k_end = kb + p.kchunk < j.k_end ? kb + p.kchunk : j.k_end;
@@ -192,6 +195,8 @@ struct LevelTraits {
     return j;
   }
   static __device__ __forceinline__ int* sync(const LevelArgs& p) { return p.kchunk > 0 ? p.sync : nullptr; }
+  static constexpr bool kFused = false;
+  static __device__ __forceinline__ void wait_k(const LevelArgs&, const TileJob&, int32_t, int32_t) {}
   static __device__ __forceinline__ double* out(const LevelArgs& p, const TileJob& j) {
     return p.out + (int64_t)j.o_row * p.ldo + j.o_col;
   }
@@ -250,6 +255,74 @@ struct GemmTraits {
   static __device__ __forceinline__ int64_t ldm(const GemmArgs&) { return 0; }
   static __device__ __forceinline__ int64_t n(const GemmArgs&) { return 0; }
   static __device__ __forceinline__ int* sync(const GemmArgs&) { return nullptr; }
+  static constexpr bool kFused = false;
+  static __device__ __forceinline__ void wait_k(const GemmArgs&, const TileJob&, int32_t, int32_t) {}
+};
+
+// ---------------------------------------------------------------------------
+// Fused level launches: both products of one level in ONE launch.  Work units are the
+// first product's tiles (W, longest K first) followed by the second product's tiles, handed
+// out by an in-order ticket (a unit is given to a CTA only after every earlier unit has a
+// running CTA, so no unit waits on an unscheduled one).  A W tile publishes a per-tile flag
+// (= the launch's epoch) after its stores; the producer warp of a second-product tile waits
+// for the flag of each W tile its K range enters before issuing the TMA loads of that K
+// block, so second-product tiles start while the first product drains.
+struct FusedArgs {
+  LevelArgs p[2];
+  int64_t units1;  // tiles of the first product
+  int* ticket;     // zeroed once per call
+  int* flags;      // per W tile of merge g, tile (I, J): (g TM + I) TN + J
+  int32_t epoch;   // flag value meaning "stored" (unique per fused launch of the call)
+};
+struct FusedTraits {
+  using Params = FusedArgs;
+  static constexpr bool kFused = true;
+  template <int BM, int BN>
+  static __device__ __forceinline__ TileJob job(const FusedArgs& p, int64_t t) {
+    const int ph = t < p.units1 ? 0 : 1;
+    TileJob j = LevelTraits::template job<BM, BN>(p.p[ph], ph ? t - p.units1 : t);
+    j.phase = ph;
+    return j;
+  }
+  static __device__ __forceinline__ const LevelArgs& L(const FusedArgs& p, const TileJob& j) { return p.p[j.phase]; }
+  static __device__ __forceinline__ double* out(const FusedArgs& p, const TileJob& j) { return LevelTraits::out(L(p, j), j); }
+  static __device__ __forceinline__ int64_t ldo(const FusedArgs& p) { return p.p[0].ldo; }  // unused: see ldo_j
+  static __device__ __forceinline__ int64_t ldo_j(const FusedArgs& p, const TileJob& j) { return L(p, j).ldo; }
+  static __device__ __forceinline__ int64_t rows_left(const FusedArgs& p, const TileJob& j) {
+    return LevelTraits::rows_left(L(p, j), j);
+  }
+  static __device__ __forceinline__ int64_t cols_left(const FusedArgs& p, const TileJob& j) {
+    return LevelTraits::cols_left(L(p, j), j);
+  }
+  static __device__ __forceinline__ double alpha_j(const FusedArgs& p, const TileJob& j) { return L(p, j).alpha; }
+  static __device__ __forceinline__ double beta(const FusedArgs&) { return 0.0; }
+  static __device__ __forceinline__ double* mir_j(const FusedArgs& p, const TileJob& j) { return L(p, j).mir; }
+  static __device__ __forceinline__ int64_t ldm_j(const FusedArgs& p, const TileJob& j) { return L(p, j).ldm; }
+  static __device__ __forceinline__ int64_t n(const FusedArgs& p) { return p.p[0].n; }
+  static __device__ __forceinline__ int* sync(const FusedArgs& p) { return p.ticket; }
+  // producer of a second-product tile: before the K block at k, wait for the W tile it reads
+  template <int T>
+  static __device__ __forceinline__ void wait_k(const FusedArgs& p, const TileJob& j, int32_t k, int32_t k_prev) {
+    if (j.phase == 0 || (k_prev >= 0 && k / T == k_prev / T)) return;
+    const LevelArgs& a = p.p[1];
+    const int64_t TMt = (a.b + T - 1) / T;
+    const bool lower = a.mode == MODE_LOWER_2;  // W is B (rows k) for lower, A (columns k) for upper
+    const int64_t idx = lower ? ((int64_t)j.lg * TMt + k / T) * TMt + j.lj : ((int64_t)j.lg * TMt + j.li) * TMt + k / T;
+    const int* f = p.flags + idx;
+    int v;
+    long long spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (++spins > (1ll << 30)) __trap();  // a missing flag must fail loudly, not hang the GPU
+    } while (v != p.epoch);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> TMA reads
+  }
+  template <int T>
+  static __device__ __forceinline__ int* publish_flag(const FusedArgs& p, const TileJob& j) {
+    if (j.phase != 0) return nullptr;
+    const int64_t TMt = (p.p[0].b + T - 1) / T;
+    return p.flags + ((int64_t)j.lg * TMt + j.li) * TMt + j.lj;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -270,6 +343,10 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
     __syncthreads();
   }
   const TileJob tj = TR::template job<BM, BN>(p, sync ? (int64_t)s_unit : (int64_t)blockIdx.x);
+  if constexpr (TR::kFused) {  // the phase's operand maps: [A1, B1, A2, B2]
+    mapA += 2 * tj.phase;
+    mapB += 2 * tj.phase;
+  }
   if (!tj.valid) return;
   // align by offsetting the __shared__ pointer itself (an integer round trip would turn
   // the fragment loads into generic LD instead of LDS)
@@ -300,8 +377,9 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
         const int s = kt % STAGES;
         const int use = kt / STAGES;
         if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         const int32_t k = tj.k_begin + kt * BK;
+        if constexpr (TR::kFused) TR::template wait_k<BM>(p, tj, k, kt > 0 ? k - BK : -1);
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         double* sa = sA + (size_t)s * BM * BK;
 #pragma unroll
         for (int kb = 0; kb < BK / 4; ++kb) {
@@ -325,8 +403,12 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
 
   // ---------------- consumers ----------------
   if (tj.m_row >= 0 && tj.chunk == 0) {  // mirror-tile zero fill (row a7): BN rows x BM columns of the opposite triangle
-    const int64_t nn = TR::n(p), ldm = TR::ldm(p);
-    double* mir = TR::mir(p) + (int64_t)tj.m_row * ldm + tj.m_col;
+    int64_t ldm;
+    double* mir0;
+    if constexpr (TR::kFused) { ldm = TR::ldm_j(p, tj); mir0 = TR::mir_j(p, tj); }
+    else { ldm = TR::ldm(p); mir0 = TR::mir(p); }
+    const int64_t nn = TR::n(p);
+    double* mir = mir0 + (int64_t)tj.m_row * ldm + tj.m_col;
     constexpr int PAIRS = BM / 2;
     for (int e = threadIdx.x; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
       const int64_t row = e / PAIRS, col = 2 * (e % PAIRS);
@@ -372,8 +454,11 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
 
   // ---------------- epilogue: out = alpha * acc (+ beta * out), clipped ----------------
   double* out = TR::out(p, tj);
-  const int64_t ldo = TR::ldo(p), rows = TR::rows_left(p, tj), cols = TR::cols_left(p, tj);
-  const double alpha = TR::alpha(p);
+  int64_t ldo;
+  double alpha;
+  if constexpr (TR::kFused) { ldo = TR::ldo_j(p, tj); alpha = TR::alpha_j(p, tj); }
+  else { ldo = TR::ldo(p); alpha = TR::alpha(p); }
+  const int64_t rows = TR::rows_left(p, tj), cols = TR::cols_left(p, tj);
   double beta = TR::beta(p);
   int* sem = nullptr;
   if (tj.sem >= 0) {  // split-K: add this chunk's partial after chunk - 1 has stored its sum
@@ -418,6 +503,14 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
     asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
     if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sem), "r"(tj.chunk + 1) : "memory");
   }
+  if constexpr (TR::kFused) {  // a W tile of a fused launch: publish it for the second product
+    int* flag = TR::template publish_flag<BM>(p, tj);
+    if (flag) {
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+      if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(p.epoch) : "memory");
+    }
+  }
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES>
@@ -426,6 +519,16 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
                       const LevelArgs p) {
   extern __shared__ unsigned char smem_raw[];
   run_tile<BM, BN, WM, WN, STAGES, 2, LevelTraits>(&mapA, &mapB, p, smem_raw);
+}
+
+struct FusedMaps {
+  CUtensorMap m[4];  // A1, B1, A2, B2
+};
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+    dmma_fused_level_kernel(const __grid_constant__ FusedMaps maps, const FusedArgs p) {
+  extern __shared__ unsigned char smem_raw[];
+  run_tile<BM, BN, WM, WN, STAGES, 2, FusedTraits>(&maps.m[0], &maps.m[1], p, smem_raw);
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES>
@@ -459,6 +562,31 @@ static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t*
   const cudaError_t e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// Both products of one level in one launch (FusedTraits).  ticket / flags: zeroed by the
+// caller once per call; `epoch` unique among the fused launches of the call (1, 2, ...).
+template <int T, int WM, int WN, int STAGES>
+static cudaError_t launch_fused_cfg(const LevelArgs& l1, const LevelArgs& l2, int* ticket, int* flags, int epoch,
+                                    cudaStream_t s, int64_t* launches) {
+  using C = GemmCfg<T, T, WM, WN, STAGES>;
+  FusedMaps maps;
+  if (!encode_map(&maps.m[0], l1.opA, 4, T, false) || !encode_map(&maps.m[1], l1.opB, 4, BK, false) ||
+      !encode_map(&maps.m[2], l2.opA, 4, T, false) || !encode_map(&maps.m[3], l2.opB, 4, BK, false))
+    return cudaErrorInvalidValue;
+  const int64_t tiles = l1.merges * ((l1.b + T - 1) / T) * ((l1.b + T - 1) / T);
+  FusedArgs f{};
+  f.p[0] = l1; f.p[1] = l2;
+  f.p[0].kchunk = f.p[1].kchunk = 0;
+  f.units1 = tiles;
+  f.ticket = ticket;
+  f.flags = flags;
+  f.epoch = epoch;
+  constexpr auto k = dmma_fused_level_kernel<T, T, WM, WN, STAGES>;
+  set_smem_once<k>((int)C::SMEM);
+  k<<<(unsigned)(2 * tiles), C::kThreads, C::SMEM, s>>>(maps, f);
+  if (launches) ++*launches;
+  return cudaGetLastError();
 }
 
 // Algorithmic flops of one level launch, exploiting the triangular operand
@@ -519,6 +647,27 @@ static int64_t split_plan(const LevelArgs& a, int64_t& kc, int64_t T) {
   int64_t units = 0;
   for (int64_t c = 0; c < Tc; ++c) units += a.merges * Tc * ((len(c) + kc - 1) / kc);
   return units > tiles ? units : 0;
+}
+
+bool level_fusable(const LevelArgs& l1) {
+  static const bool on = [] { const char* e = std::getenv("TRINV_FUSED"); return !(e && e[0] == '0'); }();
+  if (!on || !l1.sync || l1.mode == MODE_UL) return false;
+  const int sms = device_sms();
+  auto tiles = [&](int64_t T) { const int64_t m = (l1.b + T - 1) / T; return l1.merges * m * m; };
+  const int64_t T = pick_tile(tiles, l1.b);
+  return T >= 32 && tiles(T) <= (int64_t)LEVEL_FLAG_MAX && tiles(T) < 64 * sms;
+}
+
+cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epoch, cudaStream_t s,
+                               int64_t* launches) {
+  ProfileScope prof(KIND_DMMA, level_flops(l1) + level_flops(l2), 0.0, s);
+  auto tiles = [&](int64_t T) { const int64_t m = (l1.b + T - 1) / T; return l1.merges * m * m; };
+  const int64_t T = pick_tile(tiles, l1.b);
+  int* ticket = l1.sync + epoch;           // one ticket per fused launch of the call
+  int* flags = l1.sync + LEVEL_TICKETS;    // flags carry the epoch
+  if (T >= 128) return launch_fused_cfg<128, 2, 4, 5>(l1, l2, ticket, flags, epoch, s, launches);
+  if (T >= 64) return launch_fused_cfg<64, 2, 2, 4>(l1, l2, ticket, flags, epoch, s, launches);
+  return launch_fused_cfg<32, 2, 2, 4>(l1, l2, ticket, flags, epoch, s, launches);
 }
 
 cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launches) {

@@ -96,7 +96,14 @@ struct LevelArgs {
   int* sync;        // LEVEL_SYNC_BYTES of device scratch (caller-provided), or NULL
   int32_t kchunk;
 };
-constexpr size_t LEVEL_SYNC_BYTES = 16384;  // ticket + up to 4095 tile semaphores
+constexpr size_t LEVEL_SYNC_BYTES = 65536;  // split-K: ticket + tile semaphores; fused: tickets + W-tile flags
+constexpr int LEVEL_TICKETS = 64;            // fused launches: one ticket per level of a call
+constexpr int LEVEL_FLAG_MAX = 16384 - LEVEL_TICKETS;
+// Both products of a level in one launch (gemm.cu FusedTraits): l1 = W = first product, l2 =
+// second; l1.sync = the call's LEVEL_SYNC_BYTES, zeroed once per call; epoch in 1..63.
+bool level_fusable(const LevelArgs& l1);
+cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epoch, cudaStream_t s,
+                               int64_t* launches);
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t s, int64_t* launches);
 
 // General batched GEMM on the same engine: for g < batch,

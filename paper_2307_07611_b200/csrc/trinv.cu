@@ -570,8 +570,10 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       TRY(launch_leaf(uplo, lt, s, &g_launches));
     }
   }
-  // (a4-a7) levels: two grouped DMMA launches per level.
+  // (a4-a7) levels: two grouped DMMA launches per level, or one fused launch (both products,
+  // the second's tiles gated per W tile: launch_level_fused) when the call has the sync scratch.
   const int64_t b_end = b_stop > 0 ? b_stop : n;
+  int fused_epoch = 0;
   for (int64_t b = bw; b < b_end && b < n; b *= 2) {
     const int64_t merges = merges_at(n, b);
     const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, merges * b, b, b};
@@ -653,6 +655,11 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
         }
       }
       if (two) TRY(join_from(fc, s_main));
+      continue;
+    }
+    if (l1.sync && level_fusable(l1) && fused_epoch < LEVEL_TICKETS - 1 && !(product_engine() != 0)) {
+      if (fused_epoch == 0) TRY(cudaMemsetAsync(l1.sync, 0, LEVEL_SYNC_BYTES, s));  // once per call
+      TRY(launch_level_fused(l1, l2, ++fused_epoch, s, &g_launches));
       continue;
     }
     TRY(launch_level(l1, s, &g_launches));

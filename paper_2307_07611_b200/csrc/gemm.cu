@@ -650,7 +650,9 @@ static int64_t split_plan(const LevelArgs& a, int64_t& kc, int64_t T) {
 }
 
 bool level_fusable(const LevelArgs& l1) {
-  static const bool on = [] { const char* e = std::getenv("TRINV_FUSED"); return !(e && e[0] == '0'); }();
+  // opt-in (TRINV_FUSED=1): measured slower (n = 2048 165 -> 217 us, the gated second-product
+  // tiles hold SM slots while they wait; profiles/r02_fused_levels.txt)
+  static const bool on = [] { const char* e = std::getenv("TRINV_FUSED"); return e && e[0] == '1'; }();
   if (!on || !l1.sync || l1.mode == MODE_UL) return false;
   const int sms = device_sms();
   auto tiles = [&](int64_t T) { const int64_t m = (l1.b + T - 1) / T; return l1.merges * m * m; };

@@ -25,49 +25,27 @@ struct LinComb {
   int k;
 };
 
-// C[i][j] = beta C[i][j] + sum_t c_t X_t[i][j]  (beta == 0: C not read).  One CTA per row
-// (grid-strided), 16-byte accesses, 4 column pairs in flight per thread (the round-2 ncu
-// capture of the 2-pairs-per-thread version showed 59% long-scoreboard stalls at 0.5 of HBM).
-__global__ void __launch_bounds__(256) lincomb_kernel(int64_t rows, int64_t cols, double beta, double* C, int64_t ldc,
-                                                      const LinComb t) {
+// C[i][j] = beta C[i][j] + sum_t c_t X_t[i][j]  (beta == 0: C not read).  One column pair per
+// thread, rows over blockIdx.y: 0.5 of HBM on a 2048^2 combination incl. the launch ramp
+// (profiles/r02_ncu_lincomb_v1.txt); a one-CTA-per-row variant with 4 pairs per thread took
+// 31 instead of 18 us (config 3: 11 -> 21 ms) and was reverted.
+__global__ void lincomb_kernel(int64_t rows, int64_t cols, double beta, double* C, int64_t ldc, const LinComb t) {
   pdl_launch_dependents();
   pdl_wait();
-  const int64_t pairs = cols / 2;
-  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
-    const double2* x[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) x[q] = reinterpret_cast<const double2*>(t.x[q < t.k ? q : 0] + i * t.ld[q < t.k ? q : 0]);
-    double2* c = reinterpret_cast<double2*>(C + i * ldc);
-    for (int64_t j0 = threadIdx.x; j0 < pairs; j0 += 4 * blockDim.x) {
-      double2 acc[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t j = j0 + u * blockDim.x;
-        acc[u] = make_double2(0.0, 0.0);
-        if (j < pairs && beta != 0.0) {
-          acc[u] = __ldcg(c + j);
-          if (beta != 1.0) { acc[u].x *= beta; acc[u].y *= beta; }
-        }
-      }
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    for (int64_t j = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); j < cols;
+         j += 2 * (int64_t)gridDim.x * blockDim.x) {
+      double2 acc = beta == 0.0 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(C + i * ldc + j);
+      if (beta != 0.0 && beta != 1.0) { acc.x *= beta; acc.y *= beta; }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (q < t.k) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int64_t j = j0 + u * blockDim.x;
-            if (j < pairs) {
-              const double2 v = __ldcg(x[q] + j);
-              acc[u].x = fma(t.c[q], v.x, acc[u].x);
-              acc[u].y = fma(t.c[q], v.y, acc[u].y);
-            }
-          }
+          const double2 v = *reinterpret_cast<const double2*>(t.x[q] + i * t.ld[q] + j);
+          acc.x = fma(t.c[q], v.x, acc.x);
+          acc.y = fma(t.c[q], v.y, acc.y);
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t j = j0 + u * blockDim.x;
-        if (j < pairs) c[j] = acc[u];
-      }
+      *reinterpret_cast<double2*>(C + i * ldc + j) = acc;
     }
   }
 }
@@ -86,7 +64,8 @@ static cudaError_t lincomb(int64_t n, double beta, double* C, int64_t ldc, std::
     t.c[t.k] = *ci;
   }
   const int threads = 256;
-  const dim3 grid((unsigned)(n < 65535 ? n : 65535));
+  const int64_t bx = (n / 2 + threads - 1) / threads;
+  const dim3 grid((unsigned)(bx < 8 ? bx : 8), (unsigned)(n < 65535 ? n : 65535));
   const cudaError_t e = launch_k(lincomb_kernel, grid, dim3(threads), 0, s, n, n, beta, C, ldc, t);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();

@@ -96,8 +96,12 @@ def _split_worker(rank, world, port, n, uplo, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,uplo", [(2, 300, "L"), (3, 257, "U"), (2, 128, "U")])
+@pytest.mark.parametrize("world,n,uplo", [(2, 300, "L"), (3, 257, "U"), (2, 128, "U"), (4, 520, "L"),
+                                          (5, 700, "U")])
 def test_gloo_split_single_matrix(world, n, uplo):
+    """One matrix over `world` ranks: phase 1 recurses on halves of the group (sub-groups of
+    1..3 ranks, the broadcast / gather sources translated to global ranks), phase 3 splits the
+    off-diagonal block into 2G panels; rank 0 gets X equal to the oracle's."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -48,7 +48,8 @@ def _worker(rank, world, port, n, uplo, q, transport="nccl"):
 
 
 @pytest.mark.parametrize("transport", ["nccl", "p2p"])
-@pytest.mark.parametrize("world,n,uplo", [(2, 1024, "L"), (2, 1500, "U"), (3, 2048, "L"), (3, 1000, "U")])
+@pytest.mark.parametrize("world,n,uplo", [(2, 1024, "L"), (2, 1500, "U"), (3, 2048, "L"), (3, 1000, "U"),
+                                          (4, 2048, "U")])
 def test_split_two_ranks_one_gpu(world, n, uplo, transport):
     """transport "nccl": process-group broadcast + gather (gloo here); "p2p": the kernels
     read A^-1 / B^-1 from and store the X21 panels into rank 0's X through CUDA IPC

@@ -54,6 +54,7 @@ struct TileJob {
   int32_t o_row, o_col, g;  // output tile origin (and batch index)
   int32_t m_row, m_col;     // mirror tile origin (zero fill, level modes 2), or -1
   int32_t sem, chunk;       // split-K: the tile's semaphore index and this unit's K chunk (sem -1: unsplit)
+  int32_t nch, unit0;       // split-K: chunks of the tile, unit index of its chunk 0
   int32_t lg, li, lj;       // level launches: merge and tile indices
   int32_t phase;            // fused level launches: 0 = first product (W), 1 = second
   bool valid;
@@ -112,6 +113,8 @@ struct LevelTraits {
       }
       const int64_t tl = rem / nc;
       chunk = rem % nc;
+      j.nch = (int32_t)nc;
+      j.unit0 = (int32_t)(t - chunk);
       g = tl / Tf;
       const int64_t f = tl % Tf;
       if (cls_is_j) { J = cc; I = f; } else { I = cc; J = f; }
@@ -197,6 +200,8 @@ struct LevelTraits {
   static __device__ __forceinline__ int* sync(const LevelArgs& p) { return p.kchunk > 0 ? p.sync : nullptr; }
   static constexpr bool kFused = false;
   static __device__ __forceinline__ void wait_k(const LevelArgs&, const TileJob&, int32_t, int32_t) {}
+  static __device__ __forceinline__ int split_mode(const LevelArgs& p) { return p.split_mode; }
+  static __device__ __forceinline__ double* partial(const LevelArgs& p) { return p.partial; }
   static __device__ __forceinline__ double* out(const LevelArgs& p, const TileJob& j) {
     return p.out + (int64_t)j.o_row * p.ldo + j.o_col;
   }
@@ -257,6 +262,8 @@ struct GemmTraits {
   static __device__ __forceinline__ int* sync(const GemmArgs&) { return nullptr; }
   static constexpr bool kFused = false;
   static __device__ __forceinline__ void wait_k(const GemmArgs&, const TileJob&, int32_t, int32_t) {}
+  static __device__ __forceinline__ int split_mode(const GemmArgs&) { return 0; }
+  static __device__ __forceinline__ double* partial(const GemmArgs&) { return nullptr; }
 };
 
 // ---------------------------------------------------------------------------
@@ -300,6 +307,8 @@ struct FusedTraits {
   static __device__ __forceinline__ int64_t ldm_j(const FusedArgs& p, const TileJob& j) { return L(p, j).ldm; }
   static __device__ __forceinline__ int64_t n(const FusedArgs& p) { return p.p[0].n; }
   static __device__ __forceinline__ int* sync(const FusedArgs& p) { return p.ticket; }
+  static __device__ __forceinline__ int split_mode(const FusedArgs&) { return 0; }
+  static __device__ __forceinline__ double* partial(const FusedArgs&) { return nullptr; }
   // producer of a second-product tile: before the K block at k, wait for the W tile it reads
   template <int T>
   static __device__ __forceinline__ void wait_k(const FusedArgs& p, const TileJob& j, int32_t k, int32_t k_prev) {
@@ -461,7 +470,49 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   const int64_t rows = TR::rows_left(p, tj), cols = TR::cols_left(p, tj);
   double beta = TR::beta(p);
   int* sem = nullptr;
-  if (tj.sem >= 0) {  // split-K: add this chunk's partial after chunk - 1 has stored its sum
+  bool fixup = false;
+  fixup = tj.sem >= 0 && TR::split_mode(p) == 2;
+  if (fixup) {  // split-K fix-up: store alpha * partial in this unit's slot, the last chunk sums
+    constexpr int TS = BM * BN;
+    double* slot = TR::partial(p) + (int64_t)(tj.unit0 + tj.chunk) * TS;
+#pragma unroll
+    for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < C::FN; ++ni) {
+        const int row = wm * C::WTM + mi * 8 + lr, col = wn * C::WTN + ni * 8 + 2 * lc;
+        __stcg(reinterpret_cast<double2*>(slot + row * BN + col),
+               make_double2(alpha * acc[mi][ni][0], alpha * acc[mi][ni][1]));
+      }
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+    __shared__ int s_last;
+    int* cnt = sync + 1 + tj.sem;
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(cnt, 1);
+      s_last = prev == tj.nch - 1;
+      if (s_last) *cnt = 0;  // ready for the next split launch of the call
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+    if (!s_last) return;
+    __threadfence();  // acquire side: the other chunks' partials are visible (read via L2 below)
+    const double* base = TR::partial(p) + (int64_t)tj.unit0 * TS;
+#pragma unroll
+    for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < C::FN; ++ni) {
+        const int row = wm * C::WTM + mi * 8 + lr, col = wn * C::WTN + ni * 8 + 2 * lc;
+        double2 sum = __ldcg(reinterpret_cast<const double2*>(base + row * BN + col));
+        for (int c = 1; c < tj.nch; ++c) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(base + (int64_t)c * TS + row * BN + col));
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+        acc[mi][ni][0] = sum.x;
+        acc[mi][ni][1] = sum.y;
+      }
+  }
+  const double alpha_out = fixup ? 1.0 : alpha;  // the partials already carry alpha
+  if (tj.sem >= 0 && !fixup) {  // split-K: add this chunk's partial after chunk - 1 has stored its sum
     sem = sync + 1 + tj.sem;
     if (tj.chunk > 0) {
       if (lane == 0) {
@@ -484,7 +535,7 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
 #pragma unroll
     for (int ni = 0; ni < C::FN; ++ni) {
       const int64_t col = wn * C::WTN + ni * 8 + 2 * lc;
-      double v0 = alpha * acc[mi][ni][0], v1 = alpha * acc[mi][ni][1];
+      double v0 = alpha_out * acc[mi][ni][0], v1 = alpha_out * acc[mi][ni][1];
       if (col + 1 < cols && vec) {
         if (beta != 0.0) {
           const double2 o = __ldcg(reinterpret_cast<const double2*>(orow + col));
@@ -649,6 +700,11 @@ static int64_t split_plan(const LevelArgs& a, int64_t& kc, int64_t T) {
   return units > tiles ? units : 0;
 }
 
+bool level_split_fixup() {  // TRINV_SPLITK=2: split-K with the last-chunk fix-up (needs LEVEL_PARTIAL_BYTES)
+  static const bool on = [] { const char* e = std::getenv("TRINV_SPLITK"); return e && atoi(e) == 2; }();
+  return on;
+}
+
 bool level_fusable(const LevelArgs& l1) {
   // opt-in (TRINV_FUSED=1): measured slower (n = 2048 165 -> 217 us, the gated second-product
   // tiles hold SM slots while they wait; profiles/r02_fused_levels.txt)
@@ -679,8 +735,14 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
   // measured slower at every order (profiles/r02_splitk.txt): opt-in experiment, TRINV_SPLITK=1
   static const bool split_on = [] { const char* e = std::getenv("TRINV_SPLITK"); return e && atoi(e) != 0; }();
   static const int64_t split_t = [] { const char* e = std::getenv("TRINV_SPLITK_T"); return e ? atoll(e) : 64; }();
+  static const int split_mode = [] { const char* e = std::getenv("TRINV_SPLITK"); return e ? atoi(e) : 0; }();
   int64_t kc = 0;
-  const int64_t units = split_on ? split_plan(a, kc, split_t == 32 ? 32 : 64) : 0;
+  int64_t units = split_on ? split_plan(a, kc, split_t == 32 ? 32 : 64) : 0;
+  if (units > 0 && split_mode == 2) {  // fix-up mode needs the partial scratch for every unit
+    const int64_t T = split_t == 32 ? 32 : 64;
+    if (!a.partial || (size_t)units * T * T * sizeof(double) > LEVEL_PARTIAL_BYTES) units = 0;
+    a.split_mode = 2;
+  }
   if (units > 0) {
     const int64_t T = split_t == 32 ? 32 : 64;
     const int64_t tiles = a.merges * (a.b / T) * (a.b / T);

@@ -95,12 +95,19 @@ struct LevelArgs {
   // hands out work units in order): deterministic summation order.
   int* sync;        // LEVEL_SYNC_BYTES of device scratch (caller-provided), or NULL
   int32_t kchunk;
+  // split_mode 2 ("fix-up"): no chunk waits.  Every chunk stores alpha * its partial in
+  // partial[unit]; a per-tile arrival counter (sync[1 + tile], left at 0 again) elects the
+  // last chunk to finish, which sums the tile's partials in chunk order into the output.
+  int32_t split_mode;
+  double* partial;  // LEVEL_PARTIAL_BYTES of device scratch, or NULL
 };
+constexpr size_t LEVEL_PARTIAL_BYTES = (size_t)48 << 20;  // split-K fix-up partial tiles
 constexpr size_t LEVEL_SYNC_BYTES = 65536;  // split-K: ticket + tile semaphores; fused: tickets + W-tile flags
 constexpr int LEVEL_TICKETS = 64;            // fused launches: one ticket per level of a call
 constexpr int LEVEL_FLAG_MAX = 16384 - LEVEL_TICKETS;
 // Both products of a level in one launch (gemm.cu FusedTraits): l1 = W = first product, l2 =
 // second; l1.sync = the call's LEVEL_SYNC_BYTES, zeroed once per call; epoch in 1..63.
+bool level_split_fixup();
 bool level_fusable(const LevelArgs& l1);
 cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epoch, cudaStream_t s,
                                int64_t* launches);

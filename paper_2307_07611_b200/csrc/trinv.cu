@@ -444,9 +444,11 @@ static bool strassen_ul(int64_t n) {
   return strassen_levels() > 0 && product_engine() == 0 && n % 8 == 0 && n / 2 >= g_strassen_min.load();
 }
 
+static size_t partial_bytes() { return level_split_fixup() ? LEVEL_PARTIAL_BYTES : 0; }
+
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
-  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES;
+  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes();
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
   return bytes;
@@ -595,6 +597,9 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
     }
     if (aux) {  // split-K tickets / semaphores (launch_level zeroes them when it splits)
       l1.sync = l2.sync = reinterpret_cast<int*>(static_cast<char*>(aux) + strassen_scratch(n));
+      if (partial_bytes())
+        l1.partial = l2.partial =
+            reinterpret_cast<double*>(static_cast<char*>(aux) + strassen_scratch(n) + LEVEL_SYNC_BYTES);
     }
     if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
       void* ozws0 = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
@@ -695,7 +700,7 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
   void* aux = p + align_up(w_bytes(n)) + oz_scratch(n);                               // run_tri's aux scratch
-  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES;  // then staging
+  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes();  // then staging
   const double* Ause = A;
   int64_t lda_use = lda;
   if (!tma_ok(A, lda)) {  // stage the input into an even-ld, aligned copy

@@ -4,69 +4,68 @@
 //
 // strassen_acc computes C = beta C + alpha A B for square h x h operands with `levels`
 // levels of the recursion over the DMMA GEMM engine (gemm.cu): per level the 10 operand
-// sums and the 4 output combinations are single fused passes (lincomb_kernel, HBM-bound),
-// the 7 half-size products recurse (level 0: one DMMA GEMM with alpha / beta).  The
+// sums (one pass over each operand's four quadrants) and the 4 output combinations (one
+// pass over M1..M7) run in mix_kernel (HBM-bound), the 7 half-size products recurse (level 0: one DMMA GEMM with alpha / beta).  The
 // products of the recursion are summed in FP64, so its error is normwise (it grows with
 // the levels, Higham's bound) where the DMMA GEMM's is componentwise: DESIGN.md §11 keeps
 // or drops it on the measured floored-relative error and time of whole inversions.
 #include <cuda_runtime.h>
-
-#include <initializer_list>
 
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace trinv {
 
-struct LinComb {
-  const double* x[4];
-  int64_t ld[4];
-  double c[4];
-  int k;
+// Several combinations of the same inputs in ONE pass: out_o = beta out_o + sum_i c[o][i] in_i
+// for up to 7 inputs and 5 outputs (the 5 operand sums of A from its 4 quadrants, likewise for
+// B, and the 4 output quadrants from M1..M7): 33 instead of 50 quadrant-sized HBM transfers
+// per Strassen level (round 2; the first version ran 14 two-input passes).
+struct Mix {
+  const double* in[7];
+  int64_t ldin[7];
+  double* out[5];
+  int64_t ldout[5];
+  double c[5][7];
+  int nin, nout;
 };
-
-// C[i][j] = beta C[i][j] + sum_t c_t X_t[i][j]  (beta == 0: C not read).  One column pair per
-// thread, rows over blockIdx.y: 0.5 of HBM on a 2048^2 combination incl. the launch ramp
-// (profiles/r02_ncu_lincomb_v1.txt); a one-CTA-per-row variant with 4 pairs per thread took
-// 31 instead of 18 us (config 3: 11 -> 21 ms) and was reverted.
-__global__ void lincomb_kernel(int64_t rows, int64_t cols, double beta, double* C, int64_t ldc, const LinComb t) {
+template <int NIN, int NOUT>
+__global__ void __launch_bounds__(256) mix_kernel(int64_t rows, int64_t cols, double beta, const Mix m) {
   pdl_launch_dependents();
   pdl_wait();
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     for (int64_t j = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); j < cols;
          j += 2 * (int64_t)gridDim.x * blockDim.x) {
-      double2 acc = beta == 0.0 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(C + i * ldc + j);
-      if (beta != 0.0 && beta != 1.0) { acc.x *= beta; acc.y *= beta; }
+      double2 v[NIN];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q < t.k) {
-          const double2 v = *reinterpret_cast<const double2*>(t.x[q] + i * t.ld[q] + j);
-          acc.x = fma(t.c[q], v.x, acc.x);
-          acc.y = fma(t.c[q], v.y, acc.y);
+      for (int q = 0; q < NIN; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(m.in[q] + i * m.ldin[q] + j));
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        double2* dst = reinterpret_cast<double2*>(m.out[o] + i * m.ldout[o] + j);
+        double2 acc = make_double2(0.0, 0.0);
+        if (beta != 0.0) {
+          acc = *dst;
+          acc.x *= beta;
+          acc.y *= beta;
         }
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) {
+          if (m.c[o][q] != 0.0) {
+            acc.x = fma(m.c[o][q], v[q].x, acc.x);
+            acc.y = fma(m.c[o][q], v[q].y, acc.y);
+          }
+        }
+        *dst = acc;
       }
-      *reinterpret_cast<double2*>(C + i * ldc + j) = acc;
     }
   }
 }
 
-static cudaError_t lincomb(int64_t n, double beta, double* C, int64_t ldc, std::initializer_list<const double*> xs,
-                           std::initializer_list<int64_t> lds, std::initializer_list<double> cs, cudaStream_t s,
-                           int64_t* launches) {
-  LinComb t{};
-  t.k = 0;
-  auto xi = xs.begin();
-  auto li = lds.begin();
-  auto ci = cs.begin();
-  for (; xi != xs.end(); ++xi, ++li, ++ci, ++t.k) {
-    t.x[t.k] = *xi;
-    t.ld[t.k] = *li;
-    t.c[t.k] = *ci;
-  }
+template <int NIN, int NOUT>
+static cudaError_t mix(int64_t n, double beta, const Mix& m, cudaStream_t s, int64_t* launches) {
   const int threads = 256;
   const int64_t bx = (n / 2 + threads - 1) / threads;
   const dim3 grid((unsigned)(bx < 8 ? bx : 8), (unsigned)(n < 65535 ? n : 65535));
-  const cudaError_t e = launch_k(lincomb_kernel, grid, dim3(threads), 0, s, n, n, beta, C, ldc, t);
+  const cudaError_t e = launch_k(mix_kernel<NIN, NOUT>, grid, dim3(threads), 0, s, n, n, beta, m);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -82,10 +81,12 @@ static bool strassen_level_ok(int64_t h, int levels, int64_t min_q) {
   return levels > 0 && h % 4 == 0 && h / 2 >= min_q;
 }
 
+constexpr int STRASSEN_TEMPS = 17;  // 5 operand sums of A, 5 of B, M1..M7
+
 size_t strassen_ws_bytes(int64_t h, int levels, int64_t min_q) {
   if (!strassen_level_ok(h, levels, min_q)) return 0;
   const int64_t q = h / 2;
-  return 9 * aup((size_t)q * even_up2(q) * sizeof(double)) + strassen_ws_bytes(q, levels - 1, min_q);
+  return STRASSEN_TEMPS * aup((size_t)q * even_up2(q) * sizeof(double)) + strassen_ws_bytes(q, levels - 1, min_q);
 }
 
 cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
@@ -101,50 +102,71 @@ cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, 
   const int64_t q = h / 2, lq = even_up2(q);
   const size_t slot = aup((size_t)q * lq * sizeof(double));
   char* w = static_cast<char*>(ws);
-  double* SA = reinterpret_cast<double*>(w);
-  double* SB = reinterpret_cast<double*>(w + slot);
+  auto buf = [&](int k) { return reinterpret_cast<double*>(w + k * slot); };
+  double *SA1 = buf(0), *SA2 = buf(1), *SA5 = buf(2), *SA6 = buf(3), *SA7 = buf(4);
+  double *SB1 = buf(5), *SB3 = buf(6), *SB4 = buf(7), *SB6 = buf(8), *SB7 = buf(9);
   double* M[7];
-  for (int k = 0; k < 7; ++k) M[k] = reinterpret_cast<double*>(w + (2 + k) * slot);
-  void* inner = w + 9 * slot;
+  for (int k = 0; k < 7; ++k) M[k] = buf(10 + k);
+  void* inner = w + STRASSEN_TEMPS * slot;
   const double *A11 = A, *A12 = A + q, *A21 = A + q * lda, *A22 = A + q * lda + q;
   const double *B11 = B, *B12 = B + q, *B21 = B + q * ldb, *B22 = B + q * ldb + q;
   double *C11 = C, *C12 = C + q, *C21 = C + q * ldc, *C22 = C + q * ldc + q;
   cudaError_t e = cudaSuccess;
 #define S_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  // operand sums, one pass per operand: inputs (X11, X12, X21, X22)
+  Mix ma{};
+  ma.nin = 4; ma.nout = 5;
+  const double* ain[4] = {A11, A12, A21, A22};
+  double* aout[5] = {SA1, SA2, SA5, SA6, SA7};
+  const double ac[5][4] = {{1, 0, 0, 1},    // A11 + A22  (M1)
+                           {0, 0, 1, 1},    // A21 + A22  (M2)
+                           {1, 1, 0, 0},    // A11 + A12  (M5)
+                           {-1, 0, 1, 0},   // A21 - A11  (M6)
+                           {0, 1, 0, -1}};  // A12 - A22  (M7)
+  Mix mb = ma;
+  const double* bin[4] = {B11, B12, B21, B22};
+  double* bout[5] = {SB1, SB3, SB4, SB6, SB7};
+  const double bc[5][4] = {{1, 0, 0, 1},    // B11 + B22  (M1)
+                           {0, 1, 0, -1},   // B12 - B22  (M3)
+                           {-1, 0, 1, 0},   // B21 - B11  (M4)
+                           {1, 1, 0, 0},    // B11 + B12  (M6)
+                           {0, 0, 1, 1}};   // B21 + B22  (M7)
+  for (int i = 0; i < 4; ++i) {
+    ma.in[i] = ain[i]; ma.ldin[i] = lda;
+    mb.in[i] = bin[i]; mb.ldin[i] = ldb;
+  }
+  for (int o = 0; o < 5; ++o) {
+    ma.out[o] = aout[o]; ma.ldout[o] = lq;
+    mb.out[o] = bout[o]; mb.ldout[o] = lq;
+    for (int i = 0; i < 4; ++i) { ma.c[o][i] = ac[o][i]; mb.c[o][i] = bc[o][i]; }
+  }
+  S_TRY((mix<4, 5>(q, 0.0, ma, s, launches)));
+  S_TRY((mix<4, 5>(q, 0.0, mb, s, launches)));
   auto prod = [&](const double* X, int64_t lx, const double* Y, int64_t ly, double* Z) {
     return strassen_acc(q, 1.0, X, lx, Y, ly, 0.0, Z, lq, levels - 1, min_q, inner, s, launches);
   };
-  // M1 = (A11 + A22)(B11 + B22)
-  S_TRY(lincomb(q, 0.0, SA, lq, {A11, A22}, {lda, lda}, {1.0, 1.0}, s, launches));
-  S_TRY(lincomb(q, 0.0, SB, lq, {B11, B22}, {ldb, ldb}, {1.0, 1.0}, s, launches));
-  S_TRY(prod(SA, lq, SB, lq, M[0]));
-  // M2 = (A21 + A22) B11
-  S_TRY(lincomb(q, 0.0, SA, lq, {A21, A22}, {lda, lda}, {1.0, 1.0}, s, launches));
-  S_TRY(prod(SA, lq, B11, ldb, M[1]));
-  // M3 = A11 (B12 - B22)
-  S_TRY(lincomb(q, 0.0, SB, lq, {B12, B22}, {ldb, ldb}, {1.0, -1.0}, s, launches));
-  S_TRY(prod(A11, lda, SB, lq, M[2]));
-  // M4 = A22 (B21 - B11)
-  S_TRY(lincomb(q, 0.0, SB, lq, {B21, B11}, {ldb, ldb}, {1.0, -1.0}, s, launches));
-  S_TRY(prod(A22, lda, SB, lq, M[3]));
-  // M5 = (A11 + A12) B22
-  S_TRY(lincomb(q, 0.0, SA, lq, {A11, A12}, {lda, lda}, {1.0, 1.0}, s, launches));
-  S_TRY(prod(SA, lq, B22, ldb, M[4]));
-  // M6 = (A21 - A11)(B11 + B12)
-  S_TRY(lincomb(q, 0.0, SA, lq, {A21, A11}, {lda, lda}, {1.0, -1.0}, s, launches));
-  S_TRY(lincomb(q, 0.0, SB, lq, {B11, B12}, {ldb, ldb}, {1.0, 1.0}, s, launches));
-  S_TRY(prod(SA, lq, SB, lq, M[5]));
-  // M7 = (A12 - A22)(B21 + B22)
-  S_TRY(lincomb(q, 0.0, SA, lq, {A12, A22}, {lda, lda}, {1.0, -1.0}, s, launches));
-  S_TRY(lincomb(q, 0.0, SB, lq, {B21, B22}, {ldb, ldb}, {1.0, 1.0}, s, launches));
-  S_TRY(prod(SA, lq, SB, lq, M[6]));
-  // C11 += M1 + M4 - M5 + M7, C12 += M3 + M5, C21 += M2 + M4, C22 += M1 - M2 + M3 + M6 (x alpha)
-  S_TRY(lincomb(q, beta, C11, ldc, {M[0], M[3], M[4], M[6]}, {lq, lq, lq, lq}, {alpha, alpha, -alpha, alpha}, s,
-                launches));
-  S_TRY(lincomb(q, beta, C12, ldc, {M[2], M[4]}, {lq, lq}, {alpha, alpha}, s, launches));
-  S_TRY(lincomb(q, beta, C21, ldc, {M[1], M[3]}, {lq, lq}, {alpha, alpha}, s, launches));
-  S_TRY(lincomb(q, beta, C22, ldc, {M[0], M[1], M[2], M[5]}, {lq, lq, lq, lq}, {alpha, -alpha, alpha, alpha}, s,
-                launches));
+  S_TRY(prod(SA1, lq, SB1, lq, M[0]));   // M1 = (A11 + A22)(B11 + B22)
+  S_TRY(prod(SA2, lq, B11, ldb, M[1]));  // M2 = (A21 + A22) B11
+  S_TRY(prod(A11, lda, SB3, lq, M[2]));  // M3 = A11 (B12 - B22)
+  S_TRY(prod(A22, lda, SB4, lq, M[3]));  // M4 = A22 (B21 - B11)
+  S_TRY(prod(SA5, lq, B22, ldb, M[4]));  // M5 = (A11 + A12) B22
+  S_TRY(prod(SA6, lq, SB6, lq, M[5]));   // M6 = (A21 - A11)(B11 + B12)
+  S_TRY(prod(SA7, lq, SB7, lq, M[6]));   // M7 = (A12 - A22)(B21 + B22)
+  // C11 = beta C11 + alpha (M1 + M4 - M5 + M7), C12 = .. (M3 + M5), C21 = .. (M2 + M4),
+  // C22 = .. (M1 - M2 + M3 + M6): one pass over M1..M7
+  Mix mc{};
+  mc.nin = 7; mc.nout = 4;
+  double* cout[4] = {C11, C12, C21, C22};
+  const double cc[4][7] = {{1, 0, 0, 1, -1, 0, 1},
+                           {0, 0, 1, 0, 1, 0, 0},
+                           {0, 1, 0, 1, 0, 0, 0},
+                           {1, -1, 1, 0, 0, 1, 0}};
+  for (int i = 0; i < 7; ++i) { mc.in[i] = M[i]; mc.ldin[i] = lq; }
+  for (int o = 0; o < 4; ++o) {
+    mc.out[o] = cout[o]; mc.ldout[o] = ldc;
+    for (int i = 0; i < 7; ++i) mc.c[o][i] = alpha * cc[o][i];
+  }
+  S_TRY((mix<7, 4>(q, beta, mc, s, launches)));
 #undef S_TRY
   return cudaSuccess;
 }

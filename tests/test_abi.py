@@ -64,8 +64,9 @@ def test_workspace_sizes():
     assert P.product_engine() == "dmma"
     assert P.strassen_levels() == 2  # default: Strassen in the top merge's dense quadrants (f3)
     h = n // 4  # the top merge's quadrant order
-    sync = 16384  # split-K tickets / semaphores (LEVEL_SYNC_BYTES)
-    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + 9 * (h // 2) ** 2 * 8 + 9 * (h // 4) ** 2 * 8 + sync
+    sync = 65536  # split-K tickets / semaphores, fused-level flags (LEVEL_SYNC_BYTES)
+    # Strassen scratch: 17 quadrant temps (5 + 5 operand sums, M1..M7) per level, 2 levels
+    assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + 17 * (h // 2) ** 2 * 8 + 17 * (h // 4) ** 2 * 8 + sync
     P.set_strassen(0)
     assert ws(b"L", n, None, n, None, n) == (n // 2) ** 2 * 8 + sync  # W = one (n/2)^2 block
     try:

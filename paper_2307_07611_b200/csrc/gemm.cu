@@ -763,6 +763,8 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
   if (forced >= 32 && (a.mode == MODE_UL || forced <= a.b)) t = forced;
   if (t >= 128) return launch_level_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches);
+  // 32x32 tiles: 2x2 consumer warps of 16x16.  One warp of 32x32, 1x2 warps of 32x16 and 6
+  // stages were measured slower or equal (profiles/r02_t32_layouts.txt).
   return launch_level_cfg<32, 32, 2, 2, 4>(a, s, launches);
 }
 

@@ -289,38 +289,38 @@ __device__ __forceinline__ void mchunk(int q, int& i, int& c) {
 }
 
 // Stage 1 step pair for the lower recurrence (k, k+1) and the upper one (k, k-1).
-template <int K>
+template <int K, int S = MS>
 __device__ __forceinline__ void m_lower_step(const double* T, double (&x)[16]) {
-  const double xk = x[K] * T[K * (MS + 1)];  // the diagonal slot holds r_K
+  const double xk = x[K] * T[K * (S + 1)];  // the diagonal slot holds r_K
   x[K] = xk;
-  x[K + 1] = fma(-T[(K + 1) * MS + K], xk, x[K + 1]);
-  const double xk1 = x[K + 1] * T[(K + 1) * (MS + 1)];
+  x[K + 1] = fma(-T[(K + 1) * S + K], xk, x[K + 1]);
+  const double xk1 = x[K + 1] * T[(K + 1) * (S + 1)];
   x[K + 1] = xk1;
 #pragma unroll
   for (int i = K + 2; i < 16; ++i) {
-    const double2 t = *reinterpret_cast<const double2*>(T + i * MS + K);
+    const double2 t = *reinterpret_cast<const double2*>(T + i * S + K);
     x[i] = fma(-t.x, xk, x[i]);
     x[i] = fma(-t.y, xk1, x[i]);
   }
 }
-template <int K>
+template <int K, int S = MS>
 __device__ __forceinline__ void m_upper_step(const double* T, double (&x)[16]) {  // K odd: rows K, K-1
-  const double xk = x[K] * T[K * (MS + 1)];
+  const double xk = x[K] * T[K * (S + 1)];
   x[K] = xk;
-  x[K - 1] = fma(-T[(K - 1) * MS + K], xk, x[K - 1]);
-  const double xk1 = x[K - 1] * T[(K - 1) * (MS + 1)];
+  x[K - 1] = fma(-T[(K - 1) * S + K], xk, x[K - 1]);
+  const double xk1 = x[K - 1] * T[(K - 1) * (S + 1)];
   x[K - 1] = xk1;
 #pragma unroll
   for (int i = 0; i < K - 1; ++i) {
-    const double2 t = *reinterpret_cast<const double2*>(T + i * MS + K - 1);  // (T_i,K-1, T_iK)
+    const double2 t = *reinterpret_cast<const double2*>(T + i * S + K - 1);  // (T_i,K-1, T_iK)
     x[i] = fma(-t.y, xk, x[i]);
     x[i] = fma(-t.x, xk1, x[i]);
   }
 }
-template <bool UPPER, int... P>
+template <bool UPPER, int S = MS, int... P>
 __device__ __forceinline__ void m_steps(const double* T, double (&x)[16], std::integer_sequence<int, P...>) {
-  if constexpr (UPPER) (m_upper_step<15 - 2 * P>(T, x), ...);
-  else (m_lower_step<2 * P>(T, x), ...);
+  if constexpr (UPPER) (m_upper_step<15 - 2 * P, S>(T, x), ...);
+  else (m_lower_step<2 * P, S>(T, x), ...);
 }
 
 // acc[I][J] (8x8 tiles of a 16x16 product) += A[16][16] B[16][16], both in the slot
@@ -512,6 +512,68 @@ static void launch_mma32(char uplo, const LeafArgs& a, int sms, cudaStream_t s) 
 }
 
 // ---------------------------------------------------------------------------
+// n <= 16 (any layout): a half-warp per matrix, two per warp, lane c = column c of the inverse
+// by the same 16-wide recurrence (lower: P:221-247 right-looking; upper: CRIT's back
+// substitution), orders below 16 padded with the identity (inv([T 0; 0 I]) =
+// [T^-1 0; 0 I], nothing of the padding is stored).  Rows move one per instruction (16 lanes
+// x 8 B = one 128-byte line per half-warp); the next pair of matrices is loaded into
+// registers while the current pair is inverted.  Round 1 ran these orders through the
+// one-warp-per-matrix plain kernel at 0.12 of HBM (n = 16); now 0.61 (5x).
+constexpr int HS = 18;  // slot row stride (doubles): 16-byte aligned rows for the pair loads
+template <bool UPPER>
+__global__ void __launch_bounds__(256) leaf16_kernel(const LeafArgs a) {
+  __shared__ __align__(16) double slots[8][2][16 * HS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, c = lane & 15;
+  double* T = slots[warp][h];
+  const int64_t npairs = (a.batch + 1) / 2;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp, TW = (int64_t)gridDim.x * 8;
+  const unsigned hmask = 0xffffu << (16 * h);
+  auto load = [&](int64_t pr, double (&v)[16]) {
+    const int64_t b = 2 * pr + h;
+    const int nb = b >= a.batch ? 0 : (b == a.batch - 1 ? a.n_last : a.n);
+    const double* src = a.A + (b < a.batch ? b : 0) * a.sA;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const bool ref = i < nb && c < nb && (UPPER ? c >= i : c <= i) && !(a.unit && c == i);
+      v[i] = ref ? src[(int64_t)i * a.lda + c] : (i == c ? 1.0 : 0.0);
+    }
+  };
+  double v[16];
+  if (gw < npairs) load(gw, v);
+  for (int64_t pr = gw; pr < npairs; pr += TW) {
+    const int64_t b = 2 * pr + h;
+    const int nb = b >= a.batch ? 0 : (b == a.batch - 1 ? a.n_last : a.n);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) T[i * HS + c] = v[i];
+    __syncwarp();
+    if (pr + TW < npairs) load(pr + TW, v);  // the next pair's rows in flight during the inversion
+    const double d = T[c * (HS + 1)];
+    const bool zero = c < nb && d == 0.0;
+    const unsigned zmask = (__ballot_sync(0xffffffffu, zero) & hmask) >> (16 * h);
+    __syncwarp();
+    T[c * (HS + 1)] = 1.0 / d;  // IEEE division: X_jj == 1/T_jj bitwise (C4); unit / padding: 1
+    __syncwarp();
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+    m_steps<UPPER, HS>(T, x, std::make_integer_sequence<int, 8>{});
+    __syncwarp();  // the slot is rewritten by the next pair
+    if (b < a.batch) {
+      double* dst = a.X + b * a.sX;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nb && c < nb) dst[(int64_t)i * a.ldx + c] = (UPPER ? i > c : i < c) ? 0.0 : x[i];
+      if (c == 0) {
+        const int fz = zmask ? __ffs(zmask) - 1 : -1;
+        if (a.info_mode == 1) a.info[b] = zmask ? fz + 1 : 0;
+        else if (a.info_mode == 2 && zmask)
+          info_min_nonzero(a.info, static_cast<int32_t>(a.info_off + b * a.info_stride + fz + 1));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Plain-load kernel for any layout (odd n / ld, unaligned pointers): one warp
 // per matrix, rows loaded coalesced into a smem slot, result stored directly.
 template <bool UPPER>
@@ -619,6 +681,13 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
     if (br == 16) launched = launch_band<8, 3, 16>(uplo, a, sms, s);
     else if (br == 8) launched = launch_band<8, 4, 8>(uplo, a, sms, s);
     else launched = launch_band<8, 4, 4>(uplo, a, sms, s);
+  }
+  if (!launched && a.n <= 16 && a.n_last <= 16) {  // half-warp per matrix
+    const int64_t ctas_needed = ((a.batch + 1) / 2 + 7) / 8;
+    const int grid = (int)(ctas_needed < (int64_t)sms * 8 ? ctas_needed : (int64_t)sms * 8);
+    if (uplo == 'L') leaf16_kernel<false><<<grid, 256, 0, s>>>(a);
+    else leaf16_kernel<true><<<grid, 256, 0, s>>>(a);
+    launched = true;
   }
   if (!launched) {
     const int64_t ctas_needed = (a.batch + 3) / 4;

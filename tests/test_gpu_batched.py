@@ -48,7 +48,7 @@ def test_orders_and_uplo(n, uplo):
     assert np.all(opp == 0.0)
 
 
-@pytest.mark.parametrize("uplo,n", [("L", 32), ("U", 32), ("U", 48), ("L", 64)])
+@pytest.mark.parametrize("uplo,n", [("L", 32), ("U", 32), ("U", 48), ("L", 64), ("L", 16), ("U", 13)])
 def test_unit_ignores_diag_and_nan_other_triangle(uplo, n):
     B = 1000
     A = synth.host(n, batch=B, uplo=uplo)

@@ -79,7 +79,7 @@ struct GemmCfg {
 struct LevelTraits {
   using Params = LevelArgs;
   template <int BM, int BN>
-  static __device__ __forceinline__ TileJob job(const LevelArgs& p, int64_t t) {
+  static __host__ __device__ __forceinline__ TileJob job(const LevelArgs& p, int64_t t) {
     TileJob j{};
     const int64_t b = p.b, n = p.n, merges = p.merges;
     const int64_t TMmax = (b + BM - 1) / BM, TNmax = (b + BN - 1) / BN;
@@ -591,6 +591,257 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Stream-K level launches (mid-size levels).  With one CTA per tile a level whose tiles fit
+// in one or two waves is as long as its longest-K tile (the triangular K ranges span 1..b/BK
+// iterations), and every CTA pays the pipeline fill once per tile.  Here a persistent grid of
+// P CTAs splits the level's total K-iterations (sum over its tiles, in the LPT tile order of
+// LevelTraits::job, of ceil(K range / BK)) into P contiguous ranges of W iterations: CTA c
+// runs [c W, (c+1) W), crossing tile boundaries with one continuous TMA ring.  A tile cut by
+// a range boundary is finished by the CTA that ran its first iterations (the "owner", whose
+// piece is the last one of its range): the CTAs holding the tile's later iterations run them
+// FIRST in their ranges, store the raw partial sum in their slot and release a flag; the
+// owner adds the partials in CTA order (a fixed, schedule-determined summation order) and
+// stores alpha * sum (+ the mirror-tile zero fill).  Only owners wait, only on higher CTAs,
+// whose pieces come first in their ranges: with all P CTAs resident nothing waits long, and
+// the last CTA never waits.  Flags are 0 between launches (each owner clears the flags it
+// consumed; the call zeroes them once before its first level).
+constexpr int SK_MAX_P = 320;
+struct SkArgs {
+  int32_t W;            // K-iterations per CTA
+  int32_t total;        // K-iterations of the level
+  int* flags;           // [P]: 1 = CTA c's leading partial is stored
+  double* partial;      // [P][BM * BN] raw partial sums
+  int32_t t0[SK_MAX_P];    // tile of CTA c's first iteration
+  int32_t off0[SK_MAX_P];  // that iteration's index inside the tile
+};
+template <int BM, int BN>
+__host__ __device__ __forceinline__ int32_t sk_nk(const TileJob& j) {
+  return j.valid ? (j.k_end - j.k_begin + BK - 1) / BK : 0;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, MINB)
+    dmma_sk_level_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         const LevelArgs p, const __grid_constant__ SkArgs sk) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  const int c = blockIdx.x;
+  const int32_t todo = min(sk.W, sk.total - c * sk.W);
+  if (todo <= 0) return;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* sA = reinterpret_cast<double*>(base);                              // [STAGES][BK/4][BM][4]
+  double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);  // [STAGES][BN/4][BK][4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::kConsumerWarps) {
+    // ---------------- TMA producer: the CTA's iterations, tile after tile, one ring ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&mapA);
+      tma_prefetch_desc(&mapB);
+      int32_t it = 0, t = sk.t0[c], off = sk.off0[c], rem = todo;
+      while (rem > 0) {
+        const TileJob tj = LevelTraits::template job<BM, BN>(p, t);
+        const int32_t len = min(sk_nk<BM, BN>(tj) - off, rem);
+        for (int32_t kt = off; kt < off + len; ++kt, ++it) {
+          const int s = it % STAGES;
+          const int use = it / STAGES;
+          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+          const int32_t k = tj.k_begin + kt * BK;
+          mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+          double* sa = sA + (size_t)s * BM * BK;
+#pragma unroll
+          for (int kb = 0; kb < BK / 4; ++kb) tma_load_2d(sa + kb * BM * 4, &mapA, tj.a_col + k + 4 * kb, tj.a_row, &full[s]);
+          double* sb = sB + (size_t)s * BK * BN;
+#pragma unroll
+          for (int nb = 0; nb < BN / 4; ++nb) tma_load_2d(sb + nb * BK * 4, &mapB, tj.b_col + nb * 4, tj.b_row + k, &full[s]);
+        }
+        if (len > 0) rem -= len;
+        ++t;
+        off = 0;
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int wm = warp / WN, wn = warp % WN;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int a_base = (wm * C::WTM + lr) * 4 + lc;
+  const int b_base = ((wn * C::WTN + lr) >> 2) * BK * 4 + lc * 4 + (lr & 3);
+  int32_t it = 0, t = sk.t0[c], off = sk.off0[c], rem = todo;
+  while (rem > 0) {
+    const TileJob tj = LevelTraits::template job<BM, BN>(p, t);
+    const int32_t nk = sk_nk<BM, BN>(tj);
+    const int32_t len = min(nk - off, rem);
+    if (len <= 0) { ++t; off = 0; continue; }
+    double acc[C::FM][C::FN][2];
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int32_t kt = 0; kt < len; ++kt, ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      const double* a_st = sA + (size_t)s * BM * BK + a_base;
+      const double* b_st = sB + (size_t)s * BK * BN + b_base;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double af[C::FM], bf[C::FN];
+#pragma unroll
+        for (int mi = 0; mi < C::FM; ++mi) af[mi] = a_st[kk * BM * 4 + mi * 32];
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) bf[ni] = b_st[kk * 16 + ni * 2 * BK * 4];
+#pragma unroll
+        for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < C::FN; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    constexpr int TS = BM * BN;
+    if (off > 0) {
+      // a later piece of a tile begun by an earlier CTA (always this CTA's first segment)
+      double* slot = sk.partial + (int64_t)c * TS;
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) {
+          const int row = wm * C::WTM + mi * 8 + lr, col = wn * C::WTN + ni * 8 + 2 * lc;
+          __stcg(reinterpret_cast<double2*>(slot + row * BN + col), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+        }
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+      if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flags + c), "r"(1) : "memory");
+    } else {
+      if (len < nk) {  // owner: add the later pieces, CTA c+1, c+2, ... in order
+        int32_t rest = nk - len;
+        for (int q = 1; rest > 0; ++q, rest -= sk.W) {
+          if (lane == 0) {
+            const int* f = sk.flags + c + q;
+            int v;
+            long long spins = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+              if (++spins > (1ll << 31)) __trap();  // a missing piece must fail loudly, not hang
+            } while (v == 0);
+          }
+          __syncwarp();
+          const double* slot = sk.partial + (int64_t)(c + q) * TS;
+#pragma unroll
+          for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < C::FN; ++ni) {
+              const int row = wm * C::WTM + mi * 8 + lr, col = wn * C::WTN + ni * 8 + 2 * lc;
+              const double2 v = __ldcg(reinterpret_cast<const double2*>(slot + row * BN + col));
+              acc[mi][ni][0] += v.x;
+              acc[mi][ni][1] += v.y;
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");  // all warps have read
+        if (threadIdx.x == 0) {
+          rest = nk - len;
+          for (int q = 1; rest > 0; ++q, rest -= sk.W) sk.flags[c + q] = 0;
+        }
+      }
+      if (tj.m_row >= 0) {  // mirror-tile zero fill (row a7)
+        double* mir = p.mir + (int64_t)tj.m_row * p.ldm + tj.m_col;
+        constexpr int PAIRS = BM / 2;
+        for (int e = threadIdx.x; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
+          const int64_t row = e / PAIRS, col = 2 * (e % PAIRS);
+          if (tj.m_row + row < p.n) {
+            double* q = mir + row * p.ldm + col;
+            if (tj.m_col + col + 1 < p.n) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
+            else if (tj.m_col + col < p.n) *q = 0.0;
+          }
+        }
+      }
+      double* out = LevelTraits::out(p, tj);
+      const int64_t rows = LevelTraits::rows_left(p, tj), cols = LevelTraits::cols_left(p, tj);
+      const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (p.ldo % 2 == 0);
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi) {
+        const int64_t row = wm * C::WTM + mi * 8 + lr;
+        if (row >= rows) continue;
+        double* orow = out + row * p.ldo;
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) {
+          const int64_t col = wn * C::WTN + ni * 8 + 2 * lc;
+          const double v0 = p.alpha * acc[mi][ni][0], v1 = p.alpha * acc[mi][ni][1];
+          if (col + 1 < cols && vec) {
+            *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
+          } else {
+            if (col < cols) orow[col] = v0;
+            if (col + 1 < cols) orow[col + 1] = v1;
+          }
+        }
+      }
+    }
+    rem -= len;
+    ++t;
+    off = 0;
+  }
+}
+
+// Host side of the stream-K plan: per-CTA first tile / offset from the same tile map.
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB>
+static cudaError_t launch_level_sk_cfg(const LevelArgs& a, int ctas_per_sm, int w_min, cudaStream_t s,
+                                       int64_t* launches) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  const int64_t tiles = a.merges * ((a.b + BM - 1) / BM) * ((a.b + BN - 1) / BN);
+  static thread_local SkArgs sk;  // ~2.6 KB: kept off the stack
+  int64_t total = 0;
+  for (int64_t t = 0; t < tiles; ++t) total += sk_nk<BM, BN>(LevelTraits::template job<BM, BN>(a, t));
+  if (total <= 0) return cudaSuccess;
+  constexpr auto k = dmma_sk_level_kernel<BM, BN, WM, WN, STAGES, MINB>;
+  set_smem_once<k>((int)C::SMEM);
+  // every CTA must be resident (owners wait on later CTAs): at most the occupancy per SM
+  static const int occ = [] {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, C::kThreads, C::SMEM) != cudaSuccess) o = 1;
+    return o < 1 ? 1 : o;
+  }();
+  if (ctas_per_sm > occ) ctas_per_sm = occ;
+  int64_t P = (int64_t)ctas_per_sm * device_sms();
+  if (P > SK_MAX_P) P = SK_MAX_P;
+  if (P > (int64_t)(SK_PARTIAL_BYTES / (BM * BN * sizeof(double)))) P = SK_PARTIAL_BYTES / (BM * BN * sizeof(double));
+  if (P > (total + w_min - 1) / w_min) P = (total + w_min - 1) / w_min;
+  if (P < 1) P = 1;
+  const int64_t W = (total + P - 1) / P;
+  P = (total + W - 1) / W;
+  sk.W = (int32_t)W;
+  sk.total = (int32_t)total;
+  sk.flags = a.sk_flags;
+  sk.partial = a.sk_partial;
+  int64_t cum = 0, cta = 0;
+  for (int64_t t = 0; t < tiles && cta < P; ++t) {
+    const int64_t nk = sk_nk<BM, BN>(LevelTraits::template job<BM, BN>(a, t));
+    while (cta < P && cta * W < cum + nk) {  // CTA cta starts inside tile t
+      sk.t0[cta] = (int32_t)t;
+      sk.off0[cta] = (int32_t)(cta * W - cum);
+      ++cta;
+    }
+    cum += nk;
+  }
+  CUtensorMap mA, mB;
+  if (!encode_map(&mA, a.opA, 4, BM, false)) return cudaErrorInvalidValue;
+  if (!encode_map(&mB, a.opB, 4, BK, false)) return cudaErrorInvalidValue;
+  const cudaError_t e = launch_k(k, dim3((unsigned)P), dim3(C::kThreads), C::SMEM, s, mA, mB, a, sk);
+  if (launches) ++*launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 template <int BM, int BN, int WM, int WN, int STAGES>
 static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches, int64_t units = 0) {
   using C = GemmCfg<BM, BN, WM, WN, STAGES>;
@@ -700,6 +951,15 @@ static int64_t split_plan(const LevelArgs& a, int64_t& kc, int64_t T) {
   return units > tiles ? units : 0;
 }
 
+// Stream-K level launches: opt-in (TRINV_SK=1).  Measured slower than one CTA per tile at
+// n = 1024..8192 for every tile shape tried (profiles/r02_stream_k.txt): the big-tile CTAs
+// reach 80% tensor-pipe activity but the per-SM iteration cost is uneven (active cycles
+// max / mean 1.22 at n = 2048's top level), and the small levels lose their parallelism.
+bool level_sk_enabled() {
+  static const bool on = [] { const char* e = std::getenv("TRINV_SK"); return e && atoi(e) != 0; }();
+  return on;
+}
+
 bool level_split_fixup() {  // TRINV_SPLITK=2: split-K with the last-chunk fix-up (needs LEVEL_PARTIAL_BYTES)
   static const bool on = [] { const char* e = std::getenv("TRINV_SPLITK"); return e && atoi(e) == 2; }();
   return on;
@@ -761,6 +1021,22 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
   static const int64_t forced = [] { const char* e = std::getenv("TRINV_LEVEL_TILE"); return e ? atoll(e) : 0; }();
   int64_t t = pick_tile(tiles, a.mode == MODE_UL ? 128 : a.b);
   if (forced >= 32 && (a.mode == MODE_UL || forced <= a.b)) t = forced;
+  // stream-K for the levels that fit in a few waves of 64x64 tiles (TRINV_SK=0: off;
+  // TRINV_SK_TILE 32 / 64, TRINV_SK_CPS CTAs per SM, TRINV_SK_WMIN minimum iterations per CTA,
+  // TRINV_SK_WAVES: levels with fewer 64x64 tiles than this many per SM)
+  const bool sk_on = level_sk_enabled();
+  static const int sk_tile = [] { const char* e = std::getenv("TRINV_SK_TILE"); return e ? atoi(e) : 64; }();
+  static const int sk_cps = [] { const char* e = std::getenv("TRINV_SK_CPS"); return e ? atoi(e) : 2; }();
+  static const int64_t sk_bmin = [] { const char* e = std::getenv("TRINV_SK_BMIN"); return e ? atoll(e) : 256; }();
+  static const int sk_wmin = [] { const char* e = std::getenv("TRINV_SK_WMIN"); return e ? atoi(e) : 8; }();
+  static const double sk_waves = [] { const char* e = std::getenv("TRINV_SK_WAVES"); return e ? atof(e) : 8.0; }();
+  if (sk_on && a.sk_flags && a.sk_partial && a.mode != MODE_UL && t < 128 && forced == 0 && a.b >= sk_bmin &&
+      a.b >= 128 && tiles(64) < (int64_t)(sk_waves * device_sms())) {
+    if (sk_tile == 128) return launch_level_sk_cfg<128, 128, 2, 4, 5, 1>(a, 1, sk_wmin, s, launches);
+    if (sk_tile == 12864) return launch_level_sk_cfg<128, 64, 4, 2, 4, 1>(a, 1, sk_wmin, s, launches);
+    if (sk_tile == 6448) return launch_level_sk_cfg<64, 64, 2, 4, 4, 1>(a, 1, sk_wmin, s, launches);
+    return launch_level_sk_cfg<64, 64, 2, 2, 4, 2>(a, sk_cps, sk_wmin, s, launches);
+  }
   if (t >= 128) return launch_level_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches);
   // 32x32 tiles: 2x2 consumer warps of 16x16.  One warp of 32x32, 1x2 warps of 32x16 and 6

@@ -100,7 +100,14 @@ struct LevelArgs {
   // last chunk to finish, which sums the tile's partials in chunk order into the output.
   int32_t split_mode;
   double* partial;  // LEVEL_PARTIAL_BYTES of device scratch, or NULL
+  // stream-K launches of the mid-size levels (gemm.cu dmma_sk_level_kernel): SK_FLAG_INTS flags,
+  // zero before the call's first level (left zero by every launch), and SK_PARTIAL_BYTES of
+  // per-CTA partial tiles; NULL = one CTA per tile.
+  int* sk_flags;
+  double* sk_partial;
 };
+constexpr int SK_FLAG_INTS = 512;
+constexpr size_t SK_PARTIAL_BYTES = (size_t)160 * 128 * 128 * sizeof(double);
 constexpr size_t LEVEL_PARTIAL_BYTES = (size_t)48 << 20;  // split-K fix-up partial tiles
 constexpr size_t LEVEL_SYNC_BYTES = 65536;  // split-K: ticket + tile semaphores; fused: tickets + W-tile flags
 constexpr int LEVEL_TICKETS = 64;            // fused launches: one ticket per level of a call
@@ -108,6 +115,7 @@ constexpr int LEVEL_FLAG_MAX = 16384 - LEVEL_TICKETS;
 // Both products of a level in one launch (gemm.cu FusedTraits): l1 = W = first product, l2 =
 // second; l1.sync = the call's LEVEL_SYNC_BYTES, zeroed once per call; epoch in 1..63.
 bool level_split_fixup();
+bool level_sk_enabled();  // TRINV_SK=1: stream-K launches of the mid-size levels (opt-in)
 bool level_fusable(const LevelArgs& l1);
 cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epoch, cudaStream_t s,
                                int64_t* launches);

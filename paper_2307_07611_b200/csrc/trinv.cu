@@ -445,10 +445,13 @@ static bool strassen_ul(int64_t n) {
 }
 
 static size_t partial_bytes() { return level_split_fixup() ? LEVEL_PARTIAL_BYTES : 0; }
+// stream-K scratch of the mid-size level launches: flags + per-CTA partial tiles
+static size_t sk_bytes() { return level_sk_enabled() ? align_up(SK_FLAG_INTS * sizeof(int)) + SK_PARTIAL_BYTES : 0; }
 
 static size_t tri_ws(int64_t n, const void* A, int64_t lda, const void* X, int64_t ldx) {
   if (n <= BLK_MAX) return 0;  // a single block: no products, any layout
-  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes();
+  size_t bytes = align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes() +
+                 sk_bytes();
   if (!tma_ok(A, lda)) bytes += align_up(mat_bytes(n));
   if (!tma_ok(X, ldx)) bytes += align_up(mat_bytes(n));
   return bytes;
@@ -576,6 +579,7 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
   // the second's tiles gated per W tile: launch_level_fused) when the call has the sync scratch.
   const int64_t b_end = b_stop > 0 ? b_stop : n;
   int fused_epoch = 0;
+  bool sk_zeroed = false;
   for (int64_t b = bw; b < b_end && b < n; b *= 2) {
     const int64_t merges = merges_at(n, b);
     const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, merges * b, b, b};
@@ -600,6 +604,15 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
       if (partial_bytes())
         l1.partial = l2.partial =
             reinterpret_cast<double*>(static_cast<char*>(aux) + strassen_scratch(n) + LEVEL_SYNC_BYTES);
+      char* skp = static_cast<char*>(aux) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes();
+      if (sk_bytes()) {
+        l1.sk_flags = l2.sk_flags = reinterpret_cast<int*>(skp);
+        l1.sk_partial = l2.sk_partial = reinterpret_cast<double*>(skp + align_up(SK_FLAG_INTS * sizeof(int)));
+      }
+      if (sk_bytes() && !sk_zeroed) {  // stream-K flags: zero once per call, every launch leaves them zero
+        TRY(cudaMemsetAsync(skp, 0, SK_FLAG_INTS * sizeof(int), s));
+        sk_zeroed = true;
+      }
     }
     if (oz_level_ok(n, b) && !int8_veto()) {  // both products of every merge on the INT8 tensor cores
       void* ozws0 = reinterpret_cast<char*>(W) + align_up(w_bytes(n));
@@ -700,7 +713,8 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
   char* p = static_cast<char*>(ws);
   double* W = reinterpret_cast<double*>(p);
   void* aux = p + align_up(w_bytes(n)) + oz_scratch(n);                               // run_tri's aux scratch
-  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes();  // then staging
+  p += align_up(w_bytes(n)) + oz_scratch(n) + strassen_scratch(n) + LEVEL_SYNC_BYTES + partial_bytes() +
+       sk_bytes();  // then staging
   const double* Ause = A;
   int64_t lda_use = lda;
   if (!tma_ok(A, lda)) {  // stage the input into an even-ld, aligned copy

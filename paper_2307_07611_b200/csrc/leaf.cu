@@ -241,6 +241,163 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// n = 32, two matrices per warp (opt-in TRINV_LEAF32=pair, measured slower): half-warp h inverts matrix
+// 2p + h, lane c computes columns c and c + 16 of its inverse by the same right-looking
+// recurrence (CRIT P:568-581), column c in x[32], column c + 16 in y[16] (its
+// rows 16..31; its first 16 steps multiply by x_k = 0 and are skipped, an exact no-op).
+// Why: the one-warp-per-matrix kernel above is shared-memory (LSU) bound — every 16-byte
+// broadcast of T costs two wavefronts (one per half-warp), both serving the same matrix.
+// Here the two half-warps read the same offset of their own matrices' slots, so each
+// wavefront serves a different matrix: half the LSU wavefronts per matrix, and 37% fewer
+// FP64 instructions (no work on column c + 16's structural zeros).  Stores: one 128-byte
+// line per half-warp per instruction (PSTORE: whole 256-byte rows after one shuffle per row).
+// Staging as above (16-row TMA bands, 768 doubles per matrix), NS pair-slots per warp, one
+// mbarrier per pair-slot.  Measured: l1tex 96% -> 64%, LSU wavefronts 546 -> 292 per matrix,
+// FP64 pipe 42% -> 30%, same DRAM bytes, but 0.333 ms against 0.303 ms (the band kernel is
+// at 0.95 of the copy bandwidth on the bytes DRAM moves: the LSU was not what bounds it).
+template <bool UPPER, int BR, int K>
+__device__ __forceinline__ void leaf32p_step(const double* T, const double* rr, double (&x)[LEAF], double (&y)[16]) {
+  const double2 r = *reinterpret_cast<const double2*>(rr + K);
+  const double sub = tri_sub<UPPER, BR>(T, K);
+  const double xk = x[K] * r.x;
+  x[K] = xk;
+  x[K + 1] = fma(-sub, xk, x[K + 1]);
+  const double xk1 = x[K + 1] * r.y;
+  x[K + 1] = xk1;
+  double yk = 0.0, yk1 = 0.0;
+  if constexpr (K >= 16) {
+    yk = y[K - 16] * r.x;
+    y[K - 16] = yk;
+    y[K - 15] = fma(-sub, yk, y[K - 15]);
+    yk1 = y[K - 15] * r.y;
+    y[K - 15] = yk1;
+  }
+#pragma unroll
+  for (int i = K + 2; i < LEAF; ++i) {
+    const double2 t = tri_pair<UPPER, BR>(T, i, K);
+    x[i] = fma(-t.x, xk, x[i]);
+    x[i] = fma(-t.y, xk1, x[i]);
+    if constexpr (K >= 16) {
+      y[i - 16] = fma(-t.x, yk, y[i - 16]);
+      y[i - 16] = fma(-t.y, yk1, y[i - 16]);
+    }
+  }
+}
+template <bool UPPER, int BR, int... P>
+__device__ __forceinline__ void leaf32p_steps(const double* T, const double* rr, double (&x)[LEAF], double (&y)[16],
+                                              std::integer_sequence<int, P...>) {
+  (leaf32p_step<UPPER, BR, 2 * P>(T, rr, x, y), ...);
+}
+
+template <bool UPPER, int WARPS, int NS, bool PSTORE>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    leaf32_pair_kernel(const __grid_constant__ BandMaps<16> maps, const LeafArgs a) {
+  constexpr int BR = 16;
+  using BD = Band<BR>;
+  constexpr int SLOT = BD::SLOT;  // doubles per matrix
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, c = lane & 15;
+  double* slots = reinterpret_cast<double*>(smem_raw) + (size_t)warp * NS * 2 * SLOT;
+  double* rr = reinterpret_cast<double*>(smem_raw) + (size_t)WARPS * NS * 2 * SLOT + (warp * 2 + h) * LEAF;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem_raw + ((size_t)WARPS * NS * 2 * SLOT + WARPS * 2 * LEAF) * 8) + warp * NS;
+
+  const int64_t npairs = (a.batch + 1) / 2;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t TW = (int64_t)gridDim.x * WARPS;
+  if (gw >= npairs) return;
+  const int64_t count = (npairs - gw + TW - 1) / TW;
+
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  if (lane == 0 && warp == 0)
+    for (int w = 0; w < BD::NBAND; ++w) tma_prefetch_desc(&maps.m[w]);
+  __syncwarp();
+
+  auto issue_load = [&](int64_t t) {  // lane 0 only
+    const int64_t p = gw + t * TW;
+    const int nm = 2 * p + 1 < a.batch ? 2 : 1;
+    double* slot = slots + (t % NS) * 2 * SLOT;
+    uint64_t* bar = &bars[t % NS];
+    mbar_arrive_expect_tx(bar, nm * SLOT * 8);
+    for (int m = 0; m < nm; ++m) {
+      const int b = (int)(2 * p + m);
+#pragma unroll
+      for (int g = 0; g < BD::NBAND; ++g) {
+        if (!UPPER) tma_load_3d(slot + m * SLOT + BD::loff(g), &maps.m[g], 0, BR * g, b, bar);
+        else tma_load_3d(slot + m * SLOT + BD::uoff(g), &maps.m[BD::NBAND - 1 - g], BR * g, BR * g, b, bar);
+      }
+    }
+  };
+  if (lane == 0)
+    for (int64_t t = 0; t < NS && t < count; ++t) issue_load(t);
+
+  for (int64_t t = 0; t < count; ++t) {
+    const int64_t b = 2 * (gw + t * TW) + h;  // this half-warp's matrix
+    const bool live = b < a.batch;
+    const double* T = slots + (t % NS) * 2 * SLOT + h * SLOT;
+    mbar_wait(&bars[t % NS], (uint32_t)((t / NS) & 1));
+
+    // a1: reciprocals of rows c and c + 16 (T' order for the upper case), zero-diagonal mask
+    const double d0 = tri_diag<UPPER, BR>(T, c), d1 = tri_diag<UPPER, BR>(T, c + 16);
+    const unsigned z0 = __ballot_sync(0xffffffffu, live && !a.unit && d0 == 0.0);
+    const unsigned z1 = __ballot_sync(0xffffffffu, live && !a.unit && d1 == 0.0);
+    const unsigned zmask = ((z0 >> (16 * h)) & 0xffffu) | (((z1 >> (16 * h)) & 0xffffu) << 16);
+    rr[UPPER ? LEAF - 1 - c : c] = a.unit ? 1.0 : 1.0 / d0;  // IEEE division: X_jj == 1/T_jj bitwise (C4)
+    rr[UPPER ? 15 - c : c + 16] = a.unit ? 1.0 : 1.0 / d1;
+    __syncwarp();
+    double x[LEAF], y[16];
+#pragma unroll
+    for (int i = 0; i < LEAF; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = (i == c) ? 1.0 : 0.0;
+    leaf32p_steps<UPPER, BR>(T, rr, x, y, std::make_integer_sequence<int, LEAF / 2>{});
+    __syncwarp();  // every lane has finished reading the slot and rr
+    if (t + NS < count && lane == 0) {
+      fence_proxy_async_smem();
+      issue_load(t + NS);
+    }
+    if (PSTORE) {
+      // whole 256-byte rows: one instruction writes row i of matrix 2p (lanes 0-15: columns
+      // c, lanes 16-31: columns 16 + c, received from lane c), the next row i of matrix 2p+1
+      const int64_t b0 = 2 * (gw + t * TW);
+      double* d0p = a.X + b0 * a.sX;
+      double* d1p = a.X + (b0 + 1 < a.batch ? b0 + 1 : b0) * a.sX;
+      const bool live1 = b0 + 1 < a.batch;
+      const int col = UPPER ? LEAF - 1 - lane : lane;  // column of the row this lane writes
+#pragma unroll
+      for (int i = 0; i < LEAF; ++i) {
+        const double xv = (i < c) ? 0.0 : x[i];
+        const double yv = (i < 16 + c) ? 0.0 : y[i < 16 ? 0 : i - 16];
+        const double other = __shfl_xor_sync(0xffffffffu, h ? xv : yv, 16);  // half 0 gets x of matrix 1, half 1 y of matrix 0
+        const int64_t row = (int64_t)(UPPER ? LEAF - 1 - i : i) * a.ldx;
+        d0p[row + col] = h ? other : xv;
+        if (live1) d1p[row + col] = h ? yv : other;
+      }
+    } else if (live) {
+      double* dst = a.X + b * a.sX;
+      const int c0 = UPPER ? LEAF - 1 - c : c, c1 = UPPER ? 15 - c : c + 16;
+#pragma unroll
+      for (int i = 0; i < LEAF; ++i) {
+        const int64_t row = (int64_t)(UPPER ? LEAF - 1 - i : i) * a.ldx;
+        dst[row + c0] = (i < c) ? 0.0 : x[i];
+        dst[row + c1] = (i < 16 + c) ? 0.0 : y[i < 16 ? 0 : i - 16];
+      }
+    }
+    if (live) {
+      if (c == 0) {
+        const int fz = zmask ? __ffs(zmask) - 1 : -1;
+        if (a.info_mode == 1) a.info[b] = zmask ? fz + 1 : 0;
+        else if (a.info_mode == 2 && zmask)
+          info_min_nonzero(a.info, static_cast<int32_t>(a.info_off + b * a.info_stride + fz + 1));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // n = 32 with the off-diagonal block on the FP64 tensor cores (opt-in, TRINV_LEAF32=mma;
 // measured slower than the band kernel, see launch_leaf).
 // The scalar recurrence above reads every T_ik (i > k) once per lane: ~250 16-byte
@@ -637,6 +794,26 @@ static bool launch_band(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
   }
   return true;
 }
+template <int W, int NS, bool PSTORE = false>
+static bool launch_pair(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
+  BandMaps<16> maps;
+  for (int w = 1; w <= 2; ++w)
+    if (!encode_batch_map(&maps.m[w - 1], a, 16 * w, 16)) return false;
+  constexpr size_t smem = ((size_t)W * NS * 2 * Band<16>::SLOT + W * 2 * LEAF) * 8 + W * NS * 8;
+  const int64_t ctas_needed = ((a.batch + 1) / 2 + W - 1) / W;
+  const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
+  if (uplo == 'L') {
+    constexpr auto k = leaf32_pair_kernel<false, W, NS, PSTORE>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(maps, a);
+  } else {
+    constexpr auto k = leaf32_pair_kernel<true, W, NS, PSTORE>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(maps, a);
+  }
+  return true;
+}
+
 cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.batch <= 0) return cudaSuccess;
   const int sms = device_sms();
@@ -660,8 +837,24 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   // default 1063) halves the shared-memory wavefronts but is latency-bound and measured
   // 3-12% slower (profiles/r02_leaf_variants.txt).
   static const bool mma = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "mma"); }();
+  static const bool pair = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "pair"); }();
   static const int mcfg = [] { const char* e = std::getenv("TRINV_LEAF32_CFG"); return e ? std::atoi(e) : 1063; }();
+  static const int pcfg = [] { const char* e = std::getenv("TRINV_LEAF32_PCFG"); return e ? std::atoi(e) : 82; }();
   bool launched = false;
+  // two matrices per warp (TRINV_LEAF32=pair; TRINV_LEAF32_PCFG = [100 full-row stores +] warps x
+  // pair-slots): half the LSU wavefronts and 37% fewer FP64 instructions per matrix, yet 10%
+  // slower than the band kernel in every shape (profiles/r02_leaf_pair.txt)
+  if (pair && br == 16 && tma && full32 && a.batch < (int64_t)1 << 31) {
+    switch (pcfg) {
+      case 43: launched = launch_pair<4, 3>(uplo, a, sms, s); break;
+      case 62: launched = launch_pair<6, 2>(uplo, a, sms, s); break;
+      case 44: launched = launch_pair<4, 4>(uplo, a, sms, s); break;
+      case 52: launched = launch_pair<5, 2>(uplo, a, sms, s); break;
+      case 182: launched = launch_pair<8, 2, true>(uplo, a, sms, s); break;
+      case 143: launched = launch_pair<4, 3, true>(uplo, a, sms, s); break;
+      default: launched = launch_pair<8, 2>(uplo, a, sms, s); break;
+    }
+  }
   if (mma && tma && full32 && a.lda * 32 < ((int64_t)1 << 31)) {
     switch (mcfg) {
       case 122: launch_mma32<12, 2>(uplo, a, sms, s); break;

@@ -225,7 +225,7 @@ import oracle, synth, paper_2307_07611_b200 as P
 from gpu_common import REL_TOL
 bad = 0
 for uplo in 'LU':
-    A = synth.host(32, batch=5000, uplo=uplo, diag='signed' if uplo == 'L' else 'pos')
+    A = synth.host(32, batch=4999, uplo=uplo, diag='signed' if uplo == 'L' else 'pos')  # odd: a lone last matrix
     X = P.trinv_batched(torch.from_numpy(A).cuda(), uplo).cpu().numpy()
     bad += oracle.floored_rel_err(X, oracle.crit_batched(A, uplo)) > REL_TOL
     opp = np.triu(X, 1) if uplo == 'L' else np.tril(X, -1)
@@ -245,16 +245,17 @@ print('BAD', bad)
 """
 
 
-@pytest.mark.parametrize("cfg", ["1063", "83"])
-def test_mma_leaf_variant_parity(cfg):
-    """The opt-in DMMA-merge n = 32 kernel (TRINV_LEAF32=mma, read once per process, hence
-    a subprocess): pipelined and plain variants against the oracle, lower / upper, unit
-    diagonal with NaN-poisoned unreferenced entries, in place, zero-diagonal info."""
+@pytest.mark.parametrize("mode,cfg", [("mma", "1063"), ("mma", "83"), ("pair", "82"), ("pair", "182"), ("pair", "43")])
+def test_leaf32_variant_parity(mode, cfg):
+    """The opt-in n = 32 kernels (read once per process, hence a subprocess): the DMMA-merge
+    kernel (TRINV_LEAF32=mma, pipelined and plain) and the two-matrices-per-warp kernel
+    (TRINV_LEAF32=pair, half-row and full-row stores) against the oracle, lower / upper, an
+    odd batch, unit diagonal with NaN-poisoned unreferenced entries, in place, zero-diagonal info."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TRINV_LEAF32="mma", TRINV_LEAF32_CFG=cfg)
+    env = dict(os.environ, TRINV_LEAF32=mode, TRINV_LEAF32_CFG=cfg, TRINV_LEAF32_PCFG=cfg)
     r = subprocess.run([sys.executable, "-c", _MMA_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

@@ -1020,7 +1020,7 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
   // TRINV_LEVEL_TILE = 32 / 64 / 128 forces the tile of the level launches (experiments)
   static const int64_t forced = [] { const char* e = std::getenv("TRINV_LEVEL_TILE"); return e ? atoll(e) : 0; }();
   int64_t t = pick_tile(tiles, a.mode == MODE_UL ? 128 : a.b);
-  if (forced >= 32 && (a.mode == MODE_UL || forced <= a.b)) t = forced;
+  if (forced >= 32 && forced <= 128 && (a.mode == MODE_UL || forced <= a.b)) t = forced;
   // stream-K for the levels that fit in a few waves of 64x64 tiles (TRINV_SK=0: off;
   // TRINV_SK_TILE 32 / 64, TRINV_SK_CPS CTAs per SM, TRINV_SK_WMIN minimum iterations per CTA,
   // TRINV_SK_WAVES: levels with fewer 64x64 tiles than this many per SM)
@@ -1037,6 +1037,16 @@ cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launche
     if (sk_tile == 6448) return launch_level_sk_cfg<64, 64, 2, 4, 4, 1>(a, 1, sk_wmin, s, launches);
     return launch_level_sk_cfg<64, 64, 2, 2, 4, 2>(a, sk_cps, sk_wmin, s, launches);
   }
+  if (forced == 6432 && a.mode != MODE_UL && a.b >= 64) return launch_level_cfg<64, 32, 2, 2, 4>(a, s, launches);
+  if (forced == 3264 && a.mode != MODE_UL && a.b >= 64) return launch_level_cfg<32, 64, 2, 2, 4>(a, s, launches);
+  if (forced == 6432 || forced == 3264) t = 32;
+  // 64x32 tiles (2x2 warps of 32x16: 6 fragment loads per 8 DMMA instead of 4 per 4) for the
+  // levels that would run 32x32 tiles but still have >= TRINV_T6432_WAVES (default 3) waves of
+  // 64x32 tiles: n = 2048's top level 88.8 -> 80.8 us (profiles/r02_tile_shapes.txt)
+  static const double w6432 = [] { const char* e = std::getenv("TRINV_T6432_WAVES"); return e ? atof(e) : 3.0; }();
+  if (t == 32 && forced == 0 && w6432 > 0 && a.mode != MODE_UL && a.b >= 64 &&
+      a.merges * ((a.b + 63) / 64) * ((a.b + 31) / 32) >= (int64_t)(w6432 * device_sms()))
+    return launch_level_cfg<64, 32, 2, 2, 4>(a, s, launches);
   if (t >= 128) return launch_level_cfg<128, 128, 2, 4, 5>(a, s, launches);
   if (t >= 64) return launch_level_cfg<64, 64, 2, 2, 4>(a, s, launches);
   // 32x32 tiles: 2x2 consumer warps of 16x16.  One warp of 32x32, 1x2 warps of 32x16 and 6

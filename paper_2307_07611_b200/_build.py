@@ -8,7 +8,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtrinv.so")
 SOURCES = ["trinv.cu", "leaf.cu", "leaf64.cu", "blk.cu", "gemm.cu", "lu.cu", "oz2.cu", "probe.cu", "strassen.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"] + os.environ.get("TRINV_NVCC_EXTRA", "").split()
 
 
 def needs_build():

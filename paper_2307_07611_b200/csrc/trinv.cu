@@ -485,6 +485,58 @@ static cudaError_t gemm_tri(int64_t M, int64_t N, int64_t K, double alpha, const
   g.alpha = alpha; g.beta = beta; g.triA = triA; g.triB = triB;
   return launch_gemm(g, s, &g_launches);
 }
+// C = alpha A B + beta C for square operands of order h, exactly one of them triangular
+// (P_TF = h^3), by its quadrants (the recursion of Eq. PTFmbk): the
+// two dense quadrant products (half the flops) by Strassen's recursion, the four triangular
+// ones by this function again, down to quadrants below the Strassen size (then one
+// triangular DMMA GEMM).  E.g. A lower = [A11 0; A21 A22]:
+//   C1j = beta C1j + alpha A11 B1j,   C2j = beta C2j + alpha (A22 B2j + A21 B1j)   (j = 1, 2).
+// The triangular operand's diagonal quadrants keep their explicit zeros (as gemm_tri needs).
+// sws >= strassen_ws_bytes(h / 2, ...); one stream.  NEXT f3.
+static bool trmm_split_ok(int64_t h) {
+  static const bool on = [] { const char* e = std::getenv("TRINV_TRMM"); return !(e && e[0] == '0'); }();
+  return on && strassen_levels() > 0 && product_engine() == 0 && h % 8 == 0 && h / 2 >= g_strassen_min.load();
+}
+static cudaError_t trmm_sq(int64_t h, double alpha, const double* A, int64_t lda, int triA, const double* B,
+                           int64_t ldb, int triB, double beta, double* C, int64_t ldc, void* sws, cudaStream_t s) {
+  if (!sws || !trmm_split_ok(h)) return gemm_tri(h, h, h, alpha, A, lda, triA, B, ldb, triB, beta, C, ldc, s);
+  const int64_t q = h / 2;
+  auto a = [&](int i, int j) { return A + i * q * lda + j * q; };
+  auto b = [&](int i, int j) { return B + i * q * ldb + j * q; };
+  auto c = [&](int i, int j) { return C + i * q * ldc + j * q; };
+  const int lv = strassen_levels();
+  const int64_t mq = strassen_min_q();
+  cudaError_t e;
+#define T_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  auto dense = [&](const double* X, int64_t lx, const double* Y, int64_t ly, double bt, double* Z) {
+    return strassen_acc(q, alpha, X, lx, Y, ly, bt, Z, ldc, lv, mq, sws, s, &g_launches);
+  };
+  auto tri = [&](const double* X, const double* Y, double bt, double* Z) {
+    return trmm_sq(q, alpha, X, lda, triA, Y, ldb, triB, bt, Z, ldc, sws, s);
+  };
+  for (int j = 0; j < 2; ++j) {
+    if (triA == TRI_LOWER) {         // A = [A11 0; A21 A22]
+      T_TRY(tri(a(0, 0), b(0, j), beta, c(0, j)));
+      T_TRY(tri(a(1, 1), b(1, j), beta, c(1, j)));
+      T_TRY(dense(a(1, 0), lda, b(0, j), ldb, 1.0, c(1, j)));
+    } else if (triA == TRI_UPPER) {  // A = [A11 A12; 0 A22]
+      T_TRY(tri(a(0, 0), b(0, j), beta, c(0, j)));
+      T_TRY(dense(a(0, 1), lda, b(1, j), ldb, 1.0, c(0, j)));
+      T_TRY(tri(a(1, 1), b(1, j), beta, c(1, j)));
+    } else if (triB == TRI_LOWER) {  // B = [B11 0; B21 B22]:  Cj1 = Aj1 B11 + Aj2 B21, Cj2 = Aj2 B22
+      T_TRY(tri(a(j, 0), b(0, 0), beta, c(j, 0)));
+      T_TRY(dense(a(j, 1), lda, b(1, 0), ldb, 1.0, c(j, 0)));
+      T_TRY(tri(a(j, 1), b(1, 1), beta, c(j, 1)));
+    } else {                         // B = [B11 B12; 0 B22]:  Cj1 = Aj1 B11, Cj2 = Aj1 B12 + Aj2 B22
+      T_TRY(tri(a(j, 0), b(0, 0), beta, c(j, 0)));
+      T_TRY(tri(a(j, 1), b(1, 1), beta, c(j, 1)));
+      T_TRY(dense(a(j, 0), lda, b(0, 1), ldb, 1.0, c(j, 1)));
+    }
+  }
+#undef T_TRY
+  return cudaSuccess;
+}
+
 // The single top merge of order n = 2b with the quadrant decomposition (h = b/2):
 //   lower  W = C A^-1,  A^-1 = [P 0; Q R]:  W = [C1 P + C2 Q, C2 R];
 //          X21 = -B^-1 W, B^-1 = [P' 0; Q' R']:  X21 = -[P' W1; Q' W1 + R' W2]
@@ -504,14 +556,18 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
   if (uplo == 'L') {
     const double* C = A + b * lda;  // b x b, input rows b.., cols 0..b
     double* X21 = X + b * ldx;
-    M_TRY(gemm_tri(b, h, h, 1.0, C, lda, TRI_NONE, Ai, ldx, TRI_LOWER, 0.0, W, b, s));                       // C1 P
-    for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // + C2 Q
+    for (int64_t r0 = 0; r0 < b; r0 += h) {                                                             // C1 P
+      M_TRY(trmm_sq(h, 1.0, C + r0 * lda, lda, TRI_NONE, Ai, ldx, TRI_LOWER, 0.0, W + r0 * b, b, sws, s));
       M_TRY(strassen_acc(h, 1.0, C + r0 * lda + h, lda, Ai + h * ldx, ldx, 1.0, W + r0 * b, b, lv, mq, sws, s,
-                         &g_launches));
-    M_TRY(gemm_tri(b, h, h, 1.0, C + h, lda, TRI_NONE, Ai + h * ldx + h, ldx, TRI_LOWER, 0.0, W + h, b, s));  // C2 R
-    M_TRY(gemm_tri(h, b, h, -1.0, Bi, ldx, TRI_LOWER, W, b, TRI_NONE, 0.0, X21, ldx, s));                     // -P' W1
-    M_TRY(gemm_tri(h, b, h, -1.0, Bi + h * ldx + h, ldx, TRI_LOWER, W + h * b, b, TRI_NONE, 0.0, X21 + h * ldx,
-                   ldx, s));                                                                                  // -R' W2
+                         &g_launches));                                                                   // + C2 Q
+      M_TRY(trmm_sq(h, 1.0, C + r0 * lda + h, lda, TRI_NONE, Ai + h * ldx + h, ldx, TRI_LOWER, 0.0, W + r0 * b + h,
+                    b, sws, s));                                                                          // C2 R
+    }
+    for (int64_t c0 = 0; c0 < b; c0 += h) {
+      M_TRY(trmm_sq(h, -1.0, Bi, ldx, TRI_LOWER, W + c0, b, TRI_NONE, 0.0, X21 + c0, ldx, sws, s));    // -P' W1
+      M_TRY(trmm_sq(h, -1.0, Bi + h * ldx + h, ldx, TRI_LOWER, W + h * b + c0, b, TRI_NONE, 0.0,
+                    X21 + h * ldx + c0, ldx, sws, s));                                                    // -R' W2
+    }
     for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // - Q' W1
       M_TRY(strassen_acc(h, -1.0, Bi + h * ldx, ldx, W + c0, b, 1.0, X21 + h * ldx + c0, ldx, lv, mq, sws, s,
                          &g_launches));
@@ -519,13 +575,18 @@ static cudaError_t strassen_merge(char uplo, int64_t n, const double* A, int64_t
   } else {
     const double* B = A + b;  // b x b, input rows 0..b, cols b..
     double* X12 = X + b;
-    M_TRY(gemm_tri(h, b, h, 1.0, Ai, ldx, TRI_UPPER, B, lda, TRI_NONE, 0.0, W, b, s));                        // P B1
-    for (int64_t c0 = 0; c0 < b; c0 += h)                                                                 // + Q B2
-      M_TRY(strassen_acc(h, 1.0, Ai + h, ldx, B + h * lda + c0, lda, 1.0, W + c0, b, lv, mq, sws, s, &g_launches));
-    M_TRY(gemm_tri(h, b, h, 1.0, Ai + h * ldx + h, ldx, TRI_UPPER, B + h * lda, lda, TRI_NONE, 0.0, W + h * b, b,
-                   s));                                                                                      // R B2
-    M_TRY(gemm_tri(b, h, h, -1.0, W, b, TRI_NONE, Bi, ldx, TRI_UPPER, 0.0, X12, ldx, s));                     // -W1 P'
-    M_TRY(gemm_tri(b, h, h, -1.0, W + h, b, TRI_NONE, Bi + h * ldx + h, ldx, TRI_UPPER, 0.0, X12 + h, ldx, s));  // -W2 R'
+    for (int64_t c0 = 0; c0 < b; c0 += h) {
+      M_TRY(trmm_sq(h, 1.0, Ai, ldx, TRI_UPPER, B + c0, lda, TRI_NONE, 0.0, W + c0, b, sws, s));          // P B1
+      M_TRY(strassen_acc(h, 1.0, Ai + h, ldx, B + h * lda + c0, lda, 1.0, W + c0, b, lv, mq, sws, s,
+                         &g_launches));                                                                   // + Q B2
+      M_TRY(trmm_sq(h, 1.0, Ai + h * ldx + h, ldx, TRI_UPPER, B + h * lda + c0, lda, TRI_NONE, 0.0, W + h * b + c0,
+                    b, sws, s));                                                                          // R B2
+    }
+    for (int64_t r0 = 0; r0 < b; r0 += h) {
+      M_TRY(trmm_sq(h, -1.0, W + r0 * b, b, TRI_NONE, Bi, ldx, TRI_UPPER, 0.0, X12 + r0 * ldx, ldx, sws, s));  // -W1 P'
+      M_TRY(trmm_sq(h, -1.0, W + r0 * b + h, b, TRI_NONE, Bi + h * ldx + h, ldx, TRI_UPPER, 0.0,
+                    X12 + r0 * ldx + h, ldx, sws, s));                                                    // -W2 R'
+    }
     for (int64_t r0 = 0; r0 < b; r0 += h)                                                                 // - W1 Q'
       M_TRY(strassen_acc(h, -1.0, W + r0 * b, b, Bi + h, ldx, 1.0, X12 + r0 * ldx + h, ldx, lv, mq, sws, s,
                          &g_launches));
@@ -745,24 +806,28 @@ static trinv_status_t tri_entry(char uplo, int64_t n, const double* A, int64_t l
 static size_t ul_strassen_scratch(int64_t n) {
   return strassen_ul(n) ? align_up(strassen_ws_bytes(n / 2, strassen_levels(), strassen_min_q())) : 0;
 }
+// The diagonal quadrants S11 K11 / S22 K22 are upper x lower products again: the same
+// decomposition recursively while its dense quadrant is of Strassen size, else one MODE_UL
+// launch; S12 K22 / S22 K21 by trmm_sq.
 static trinv_status_t ul_strassen(int64_t n, const double* S, const double* K, int64_t ld, double* X, int64_t ldx,
                                   void* sws, cudaStream_t s) {
   const int64_t h = n / 2;
-  auto ul = [&](const double* Sq, const double* Kq, double* Xq) {
+  auto ul = [&](const double* Sq, const double* Kq, double* Xq) -> trinv_status_t {
+    if (strassen_ul(h)) return ul_strassen(h, Sq, Kq, ld, Xq, ldx, sws, s);
     LevelArgs u{};
     u.mode = MODE_UL; u.n = h; u.b = h; u.merges = 1;
     u.opA = MatRef{Sq, h, h, ld}; u.opB = MatRef{Kq, h, h, ld};
     u.out = Xq; u.ldo = ldx; u.out_rows = h; u.out_cols = h; u.alpha = 1.0;
-    return launch_level(u, s, &g_launches);
+    return cuda_fail(launch_level(u, s, &g_launches));
   };
-  TRY(ul(S, K, X));                                                                           // S11 K11
+  trinv_status_t st = ul(S, K, X);                                                            // S11 K11
+  if (st != TRINV_OK) return st;
   TRY(strassen_acc(h, 1.0, S + h, ld, K + h * ld, ld, 1.0, X, ldx, strassen_levels(), strassen_min_q(), sws, s,
                    &g_launches));                                                             // + S12 K21
-  TRY(gemm_tri(h, h, h, 1.0, S + h, ld, TRI_NONE, K + h * ld + h, ld, TRI_LOWER, 0.0, X + h, ldx, s));   // S12 K22
-  TRY(gemm_tri(h, h, h, 1.0, S + h * ld + h, ld, TRI_UPPER, K + h * ld, ld, TRI_NONE, 0.0, X + h * ldx, ldx,
-               s));                                                                           // S22 K21
-  TRY(ul(S + h * ld + h, K + h * ld + h, X + h * ldx + h));                                   // S22 K22
-  return TRINV_OK;
+  TRY(trmm_sq(h, 1.0, S + h, ld, TRI_NONE, K + h * ld + h, ld, TRI_LOWER, 0.0, X + h, ldx, sws, s));      // S12 K22
+  TRY(trmm_sq(h, 1.0, S + h * ld + h, ld, TRI_UPPER, K + h * ld, ld, TRI_NONE, 0.0, X + h * ldx, ldx, sws,
+              s));                                                                            // S22 K21
+  return ul(S + h * ld + h, K + h * ld + h, X + h * ldx + h);                                 // S22 K22
 }
 
 // ---- NEXT row f4: COMBRIT with beta = 4 at the top level ------------------------------

@@ -34,6 +34,14 @@
  *    synchronises once per call, see trinv_set_product_engine).
  *  - Entry points are re-entrant and thread-safe; they may be called on any
  *    device (the current device is used).
+ *  - Known limitation (round 2, profiles/r02_strassen_concurrency.txt): two
+ *    calls that take a Strassen path (trinv_lower / trinv_upper with n >=
+ *    16384 at the default trinv_set_strassen threshold; inv_from_lu /
+ *    inv_general with n >= 8192; trinv_gemm_strassen)
+ *    must not run at the same time on different streams: measured, an
+ *    occasional 32-row band of one half-size product comes out wrong (root
+ *    cause not found; the library itself never overlaps them).  Serialise such
+ *    calls on one stream, or turn Strassen off (trinv_set_strassen(0)).
  */
 #ifndef TRINV_H
 #define TRINV_H

@@ -34,14 +34,16 @@
  *    synchronises once per call, see trinv_set_product_engine).
  *  - Entry points are re-entrant and thread-safe; they may be called on any
  *    device (the current device is used).
- *  - Known limitation (round 2, profiles/r02_strassen_concurrency.txt): two
+ *  - Concurrency note (round 2, profiles/r02_strassen_concurrency.txt): two
  *    calls that take a Strassen path (trinv_lower / trinv_upper with n >=
  *    16384 at the default trinv_set_strassen threshold; inv_from_lu /
- *    inv_general with n >= 8192; trinv_gemm_strassen)
- *    must not run at the same time on different streams: measured, an
- *    occasional 32-row band of one half-size product comes out wrong (root
- *    cause not found; the library itself never overlaps them).  Serialise such
- *    calls on one stream, or turn Strassen off (trinv_set_strassen(0)).
+ *    inv_general with n >= 8192; trinv_gemm_strassen) running at the same time
+ *    on different streams produced occasional wrong tiles until the library's
+ *    element-wise kernels were given the maximum-L1 carve-out preference; with
+ *    it the reproducer shows no error (tests/test_gpu_concurrency.py), but the
+ *    root cause is not established, so the library itself never overlaps its
+ *    Strassen work with other work, and callers who need certainty can
+ *    serialise such calls or turn Strassen off (trinv_set_strassen(0)).
  */
 #ifndef TRINV_H
 #define TRINV_H

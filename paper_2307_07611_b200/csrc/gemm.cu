@@ -1139,6 +1139,7 @@ cudaError_t launch_geam(int64_t rows, int64_t cols, double alpha, const double* 
   const int64_t total = rows * cols;
   const int64_t blocks = (total + 255) / 256;
   const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
+  prefer_l1_once<geam_kernel>();
   geam_kernel<<<grid, 256, 0, s>>>(rows, cols, alpha, A, lda, beta, B, ldb, C, ldc);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -1170,6 +1171,7 @@ cudaError_t launch_copy_2d(const double* src, int64_t lds, double* dst, int64_t 
   const int64_t per_row = vec ? (cols / 2 + 255) / 256 : (cols + 255) / 256;
   const unsigned gx = (unsigned)(per_row < 1 ? 1 : (per_row < 8 ? per_row : 8));
   const unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
+  prefer_l1_once<copy_2d_kernel>();
   copy_2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, vec);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -1179,6 +1181,7 @@ cudaError_t launch_zero_2d(double* p, int64_t ld, int64_t rows, int64_t cols, cu
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const int64_t gx = std::min<int64_t>((cols + 255) / 256, 64);
   const int64_t gy = std::min<int64_t>(rows, std::max<int64_t>(1, (int64_t)device_sms() * 16 / gx));
+  prefer_l1_once<zero_2d_kernel>();
   const cudaError_t e = launch_k(zero_2d_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, p, ld, rows, cols);
   if (e != cudaSuccess) return e;
   if (launches) ++*launches;

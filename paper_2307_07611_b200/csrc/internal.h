@@ -6,6 +6,7 @@
 #include <utility>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 namespace trinv {
 
@@ -32,6 +33,27 @@ inline void set_smem_once(int bytes) {
   const uint64_t bit = 1ull << (d & 63);
   if (!(done.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
+
+// Element-wise kernels without shared memory (Strassen's combination passes, geam, zero and
+// copy passes) prefer the maximum L1 carve-out, once per kernel and device.  Round 2 finding
+// (DESIGN.md §9b): with the default carve-out, two Strassen products on concurrent streams
+// occasionally produced a wrong tile in a DMMA GEMM that shared its SMs with the other
+// stream's element-wise CTAs; with this preference those CTAs no longer share an SM with
+// the GEMMs' shared-memory-heavy CTAs and the reproducer (tools/strassen_concurrency.py)
+// shows no error.  TRINV_ELEM_CARVEOUT=-1 restores the default (experiments).
+template <auto Kernel>
+inline void prefer_l1_once() {
+  static std::atomic<uint64_t> done{0};
+  static const int pref = [] { const char* e = std::getenv("TRINV_ELEM_CARVEOUT"); return e ? atoi(e) : 0; }();
+  if (pref < 0) return;
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pref);
     done.fetch_or(bit, std::memory_order_release);
   }
 }

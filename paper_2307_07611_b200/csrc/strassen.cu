@@ -14,6 +14,8 @@
 #include "internal.h"
 #include "ptx.cuh"
 
+#include <cstdlib>
+
 namespace trinv {
 
 // Several combinations of the same inputs in ONE pass: out_o = beta out_o + sum_i c[o][i] in_i
@@ -60,8 +62,35 @@ __global__ void __launch_bounds__(256) mix_kernel(int64_t rows, int64_t cols, do
   }
 }
 
+// The same combinations as two-input geam passes (TRINV_STRASSEN_SUMS=geam: the operand sums;
+// experiment for the concurrency finding of DESIGN.md §9b)
+static cudaError_t mix_geam(int64_t n, double beta, const Mix& m, cudaStream_t s, int64_t* launches) {
+  for (int o = 0; o < m.nout; ++o) {
+    bool first = true;
+    for (int q = 0; q < m.nin; ++q) {
+      if (m.c[o][q] == 0.0) continue;
+      cudaError_t e;
+      if (first && beta == 0.0)
+        e = launch_geam(n, n, m.c[o][q], m.in[q], m.ldin[q], 0.0, m.in[q], m.ldin[q], m.out[o], m.ldout[o], s, launches);
+      else if (first)
+        e = launch_geam(n, n, m.c[o][q], m.in[q], m.ldin[q], beta, m.out[o], m.ldout[o], m.out[o], m.ldout[o], s, launches);
+      else
+        e = launch_geam(n, n, 1.0, m.out[o], m.ldout[o], m.c[o][q], m.in[q], m.ldin[q], m.out[o], m.ldout[o], s, launches);
+      if (e != cudaSuccess) return e;
+      first = false;
+    }
+  }
+  return cudaSuccess;
+}
+static bool sums_by_geam() {
+  static const bool on = [] { const char* e = std::getenv("TRINV_STRASSEN_SUMS"); return e && e[0] == 'g'; }();
+  return on;
+}
+
 template <int NIN, int NOUT>
 static cudaError_t mix(int64_t n, double beta, const Mix& m, cudaStream_t s, int64_t* launches) {
+  if (NIN == 4 && sums_by_geam()) return mix_geam(n, beta, m, s, launches);
+  prefer_l1_once<mix_kernel<NIN, NOUT>>();
   const int threads = 256;
   const int64_t bx = (n / 2 + threads - 1) / threads;
   const dim3 grid((unsigned)(bx < 8 ? bx : 8), (unsigned)(n < 65535 ? n : 65535));

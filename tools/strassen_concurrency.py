@@ -11,7 +11,7 @@ import paper_2307_07611_b200 as P  # noqa: E402
 dev = torch.device('cuda:0')
 g = torch.Generator(device=dev).manual_seed(0)
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-for n in (1024, 2048, 4096):
+for n in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1024", "2048", "4096"])]:
     k = 4
     As = [torch.rand((n, n), dtype=torch.float64, device=dev, generator=g) for _ in range(k)]
     Bs = [torch.rand((n, n), dtype=torch.float64, device=dev, generator=g) for _ in range(k)]

@@ -52,3 +52,23 @@ for r in range(reps):
                 wrong.append(f"{name}({err:.1e}, rows {bad_rows.min().item()}..{bad_rows.max().item()} n={bad_rows.numel()})")
         key = " ".join(wrong) if wrong else "only C"
         print(f"rep {r} product {i}: {key}", flush=True)
+        # do the wrong rows of M1 match a product formed with another call's operands?
+        got = ws[i][10 * slot: 10 * slot + q * q * 8].view(torch.float64).view(q, q)
+        e = exp[i][10]
+        rows = ((got - e).abs().max(dim=1).values > 1e-9 * e.abs().max()).nonzero().flatten()
+        if rows.numel():
+            rr = rows[:4]
+            for j in range(k):
+                for nameA, SA in (("SA1", exp[j][0]),):
+                    for nameB, SB in (("SB1", exp[j][5]),):
+                        pass
+                cand = {f"SA1[{j}] SB1[{i}]": exp[j][0][rr] @ exp[i][5], f"SA1[{i}] SB1[{j}]": exp[i][0][rr] @ exp[j][5],
+                        f"M1[{j}]": exp[j][10][rr]}
+                for nm, cv in cand.items():
+                    d = ((got[rr] - cv).abs().max() / cv.abs().max()).item()
+                    if d < 1e-10:
+                        print(f"     rows {rr.tolist()} match {nm}")
+            # partial match per row: which columns wrong
+            r0 = rows[0].item()
+            cols = ((got[r0] - e[r0]).abs() > 1e-9 * e.abs().max()).nonzero().flatten()
+            print(f"     row {r0}: {cols.numel()} wrong columns, {cols.min().item()}..{cols.max().item()}")

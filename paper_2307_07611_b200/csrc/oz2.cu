@@ -766,6 +766,7 @@ cudaError_t launch_oz2_prepare(int64_t M, int64_t N, int64_t K, const double* A,
                        ((which & 2) ? 32.0 * range_sum(N, OZ2_TN, triB == TRI_UPPER, triB == TRI_LOWER) : 0.0);
   ProfileScope aux(KIND_OZAUX, 0.0, bytes, st);
   if (which & 1) {
+    prefer_l1_once<oz2_split_rows_kernel>();  // element-wise: no shared memory
     oz2_split_rows_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, st>>>(
         A, lda, (int)M, (int)K, triA, (strict & 1) != 0, P, oz2_use_pair(M, N, K) ? 256 : OZ2_TM, As, ea);
     if (launches) ++*launches;
@@ -773,6 +774,7 @@ cudaError_t launch_oz2_prepare(int64_t M, int64_t N, int64_t K, const double* A,
   if (which & 2) {
     cudaError_t e = cudaMemsetAsync(maxbits, 0, (size_t)N * 8, st);
     if (e != cudaSuccess) return e;
+    prefer_l1_once<oz2_colmax_kernel>();
     oz2_colmax_kernel<<<dim3((unsigned)((N + 255) / 256), (unsigned)((K + OZ2_CMAX_ROWS - 1) / OZ2_CMAX_ROWS)), 256, 0,
                         st>>>(B, ldb, (int)K, (int)N, triB, (strict & 2) != 0, maxbits);
     oz2_split_cols_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
@@ -851,6 +853,7 @@ cudaError_t launch_oz2_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
   static const Oz2Crt crt = oz2_crt_constants();
   {
     ProfileScope aux(KIND_OZAUX, 0.0, (double)M * N * (beta == 0.0 ? 24.0 : 32.0), st);
+    prefer_l1_once<oz2_reconstruct_kernel>();
     oz2_reconstruct_kernel<<<(unsigned)((total4 + 255) / 256), 256, 0, st>>>(Rs, (int)M, (int)N, ea, eb, P, alpha,
                                                                             beta, C, ldc, crt);
   }

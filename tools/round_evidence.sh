@@ -16,3 +16,8 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 -
 CMD1="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-fp64"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:leaf32_tma -s 3 -c 1 -o gpurun_out/full_leaf32 $CMD1 > gpurun_out/ncu_full_leaf32.log 2>&1; echo "ncu full rc=$?" >> gpurun_out/steps.log
 cat gpurun_out/steps.log
+timeout 900 python tests/accuracy_report.py > gpurun_out/accuracy.txt 2>&1; echo "accuracy rc=$?" >> gpurun_out/steps.log
+: > gpurun_out/sweep_n.txt
+for n in 512 1024 2048 4096 8192; do for op in L U; do python tools/timeline.py $op $n 2>/dev/null | head -1 >> gpurun_out/sweep_n.txt; done; done
+python tools/timeline.py L 2048 2>/dev/null >> gpurun_out/sweep_n.txt
+cat gpurun_out/steps.log

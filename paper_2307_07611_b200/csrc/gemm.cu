@@ -988,6 +988,263 @@ cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epo
   return launch_fused_cfg<32, 2, 2, 4>(l1, l2, ticket, flags, epoch, s, launches);
 }
 
+// ---------------------------------------------------------------------------
+// Level chain (opt-in, measured slower): the lowest levels of a recursion (those that would run
+// 32x32 tiles) in ONE persistent launch.  Their products are latency-bound (n = 2048: the b = 128..512 levels hold
+// 19 us of DMMA work but took 59 us as six launches), so the chain replaces the launch
+// boundaries by dataflow: the tiles of all phases [W_l0, X21_l0, W_l1, X21_l1, ...] form one
+// list in topological order, CTA c takes tiles c, c + G, c + 2G, ... (G = resident CTAs), and
+// before a tile's first TMA load its producer waits for the per-(phase, merge) completion
+// counters the tile depends on:
+//   W of level l, merge g       <- X21 of level l-1, merges 2g and 2g+1 (A^-1, B^-1 complete)
+//   X21 of level l, merge g     <- W of level l, merge g
+// (the blocks below the first chained level come from the preceding blk launch).  A finished
+// tile bumps its counter after its stores (release: __threadfence, then the atomic); a waiting
+// producer acquires, then orders the generic writes before its TMA reads with a proxy fence.
+// Every dependency points at an earlier tile of the list and every CTA is resident, so the
+// wait always ends.  W is laid out by position (the rows of the merge's second half for the
+// lower case, its first half for the upper case, ld = the widest chained level) so that a
+// merge's W never overlaps the W of a merge that is not yet complete.
+constexpr int CHAIN_MAXP = 8;
+struct ChainArgs {
+  LevelArgs ph[CHAIN_MAXP];
+  int32_t tile0[CHAIN_MAXP + 1];  // first global tile of each phase
+  int32_t nphase;
+  int32_t cstride;                // counters per phase (>= merges of the first level)
+  int* cnt;                       // [nphase][cstride] completion counters, zero at launch
+};
+struct ChainMaps {
+  CUtensorMap m[2 * CHAIN_MAXP];  // per phase: A, B
+};
+
+template <int BM, int BN>
+__device__ __forceinline__ TileJob chain_job(const ChainArgs& c, int p, int64_t t) {
+  const LevelArgs& a = c.ph[p];
+  TileJob j = LevelTraits::template job<BM, BN>(a, t);
+  const int32_t s = 2 * j.lg * (int32_t)a.b, b = (int32_t)a.b;
+  switch (a.mode) {  // W by position (see above)
+    case MODE_LOWER_1: j.o_row = s + b + j.li * BM; break;
+    case MODE_UPPER_1: j.o_row = s + j.li * BM; break;
+    case MODE_LOWER_2: j.b_row = s + b; break;
+    default: j.a_row = s + j.li * BM; break;  // MODE_UPPER_2
+  }
+  return j;
+}
+
+__device__ __forceinline__ void chain_wait(const int* ctr, int target) {
+  int v;
+  long long spins = 0;
+  do {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+    if (++spins > (1ll << 28)) __trap();  // a missing tile must fail loudly, not hang the GPU
+  } while (true);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
+    dmma_chain_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ ChainArgs c) {
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* sA = reinterpret_cast<double*>(base);
+  double* sB = reinterpret_cast<double*>(base + (size_t)STAGES * C::A_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t total = c.tile0[c.nphase];
+  if ((int32_t)blockIdx.x >= total) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::kConsumerWarps) {
+    // ---------------- producer: dependencies, then the tile's K blocks into the ring ----------------
+    if (lane == 0) {
+      for (int p = 0; p < c.nphase; ++p) {
+        tma_prefetch_desc(&maps.m[2 * p]);
+        tma_prefetch_desc(&maps.m[2 * p + 1]);
+      }
+      int32_t it = 0;
+      int p = 0;
+      for (int32_t T = blockIdx.x; T < total; T += gridDim.x) {
+        while (T >= c.tile0[p + 1]) ++p;
+        const TileJob tj = chain_job<BM, BN>(c, p, T - c.tile0[p]);
+        if (!tj.valid) continue;
+        const LevelArgs& a = c.ph[p];
+        if (p & 1) {  // X21 of merge g: its W complete
+          const int64_t m = (a.b + BM - 1) / BM;
+          chain_wait(c.cnt + (p - 1) * c.cstride + tj.lg, (int)(m * m));
+        } else if (p > 0) {  // W of merge g: the level below complete on both halves
+          const LevelArgs& q = c.ph[p - 1];
+          const int64_t m = (q.b + BM - 1) / BM;
+          chain_wait(c.cnt + (p - 1) * c.cstride + 2 * tj.lg, (int)(m * m));
+          if (2 * tj.lg + 1 < q.merges) chain_wait(c.cnt + (p - 1) * c.cstride + 2 * tj.lg + 1, (int)(m * m));
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores of other CTAs -> TMA reads
+        const CUtensorMap* mA = &maps.m[2 * p];
+        const CUtensorMap* mB = &maps.m[2 * p + 1];
+        const int nk = (tj.k_end - tj.k_begin + BK - 1) / BK;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int s = it % STAGES;
+          const int use = it / STAGES;
+          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+          const int32_t k = tj.k_begin + kt * BK;
+          mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+          double* sa = sA + (size_t)s * BM * BK;
+#pragma unroll
+          for (int kb = 0; kb < BK / 4; ++kb) tma_load_2d(sa + kb * BM * 4, mA, tj.a_col + k + 4 * kb, tj.a_row, &full[s]);
+          double* sb = sB + (size_t)s * BK * BN;
+#pragma unroll
+          for (int nb = 0; nb < BN / 4; ++nb) tma_load_2d(sb + nb * BK * 4, mB, tj.b_col + nb * 4, tj.b_row + k, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int wm = warp / WN, wn = warp % WN;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int a_base = (wm * C::WTM + lr) * 4 + lc;
+  const int b_base = ((wn * C::WTN + lr) >> 2) * BK * 4 + lc * 4 + (lr & 3);
+  int32_t it = 0;
+  int p = 0;
+  for (int32_t T = blockIdx.x; T < total; T += gridDim.x) {
+    while (T >= c.tile0[p + 1]) ++p;
+    const TileJob tj = chain_job<BM, BN>(c, p, T - c.tile0[p]);
+    const LevelArgs& a = c.ph[p];
+    if (tj.valid) {
+      if (tj.m_row >= 0) {  // mirror-tile zero fill (row a7)
+        double* mir = a.mir + (int64_t)tj.m_row * a.ldm + tj.m_col;
+        constexpr int PAIRS = BM / 2;
+        for (int e = threadIdx.x; e < BN * PAIRS; e += C::kConsumerWarps * 32) {
+          const int64_t row = e / PAIRS, col = 2 * (e % PAIRS);
+          if (tj.m_row + row < a.n) {
+            double* q = mir + row * a.ldm + col;
+            if (tj.m_col + col + 1 < a.n) *reinterpret_cast<double2*>(q) = make_double2(0.0, 0.0);
+            else if (tj.m_col + col < a.n) *q = 0.0;
+          }
+        }
+      }
+      double acc[C::FM][C::FN][2];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const int nk = (tj.k_end - tj.k_begin + BK - 1) / BK;
+      for (int kt = 0; kt < nk; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+        const double* a_st = sA + (size_t)s * BM * BK + a_base;
+        const double* b_st = sB + (size_t)s * BK * BN + b_base;
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+          double af[C::FM], bf[C::FN];
+#pragma unroll
+          for (int mi = 0; mi < C::FM; ++mi) af[mi] = a_st[kk * BM * 4 + mi * 32];
+#pragma unroll
+          for (int ni = 0; ni < C::FN; ++ni) bf[ni] = b_st[kk * 16 + ni * 2 * BK * 4];
+#pragma unroll
+          for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < C::FN; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      double* out = a.out + (int64_t)tj.o_row * a.ldo + tj.o_col;
+      const int64_t rows = a.out_rows - tj.o_row, cols = a.out_cols - tj.o_col;
+      const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (a.ldo % 2 == 0);
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi) {
+        const int64_t row = wm * C::WTM + mi * 8 + lr;
+        if (row >= rows) continue;
+        double* orow = out + row * a.ldo;
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) {
+          const int64_t col = wn * C::WTN + ni * 8 + 2 * lc;
+          const double v0 = a.alpha * acc[mi][ni][0], v1 = a.alpha * acc[mi][ni][1];
+          if (col + 1 < cols && vec) {
+            *reinterpret_cast<double2*>(orow + col) = make_double2(v0, v1);
+          } else {
+            if (col < cols) orow[col] = v0;
+            if (col + 1 < cols) orow[col + 1] = v1;
+          }
+        }
+      }
+    }
+    // the tile (valid or not) is complete: release it to the tiles that depend on its merge
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(C::kConsumerWarps * 32) : "memory");
+    if (threadIdx.x == 0) atomicAdd(c.cnt + p * c.cstride + tj.lg, 1);
+  }
+}
+
+// Opt-in (TRINV_CHAIN=1): measured slower than one launch per product (n = 2048: 151 -> 170-228 us
+// for 1-6 resident CTAs per SM; the chained levels took 78-90 us against 59 us as six launches;
+// profiles/r02_level_chain.txt).  A dependent step inside the persistent grid (poll, proxy fence,
+// TMA fill, compute, release) costs more than a graph-replayed launch boundary.
+bool level_chain_enabled() {
+  static const bool on = [] { const char* e = std::getenv("TRINV_CHAIN"); return e && e[0] == '1'; }();
+  return on;
+}
+
+// Does the level run 32x32 tiles on the per-launch path (the levels the chain takes over)?
+bool level_uses_t32(const LevelArgs& a) {
+  if (a.mode == MODE_UL || a.b < 32) return false;
+  auto tiles = [&](int64_t T) { const int64_t m = (a.b + T - 1) / T; return a.merges * m * m; };
+  static const double w6432 = [] { const char* e = std::getenv("TRINV_T6432_WAVES"); return e ? atof(e) : 3.0; }();
+  if (pick_tile(tiles, a.b) != 32) return false;
+  if (w6432 > 0 && a.b >= 64 && a.merges * ((a.b + 63) / 64) * ((a.b + 31) / 32) >= (int64_t)(w6432 * device_sms()))
+    return false;
+  return true;
+}
+
+cudaError_t launch_level_chain(const LevelArgs* ph, int nphase, int* counters, int cstride, cudaStream_t s,
+                               int64_t* launches) {
+  constexpr int BM = 32, BN = 32, WM = 2, WN = 2, STAGES = 4;
+  using C = GemmCfg<BM, BN, WM, WN, STAGES>;
+  if (nphase <= 0 || nphase > CHAIN_MAXP) return cudaErrorInvalidValue;
+  double fl = 0.0;
+  for (int p = 0; p < nphase; ++p) fl += level_flops(ph[p]);
+  ProfileScope prof(KIND_DMMA, fl, 0.0, s);
+  static thread_local ChainArgs c;
+  static thread_local ChainMaps maps;
+  c.nphase = nphase;
+  c.cstride = cstride;
+  c.cnt = counters;
+  c.tile0[0] = 0;
+  for (int p = 0; p < nphase; ++p) {
+    c.ph[p] = ph[p];
+    const int64_t m = (ph[p].b + BM - 1) / BM;
+    c.tile0[p + 1] = c.tile0[p] + (int32_t)(ph[p].merges * m * m);
+    if (!encode_map(&maps.m[2 * p], ph[p].opA, 4, BM, false)) return cudaErrorInvalidValue;
+    if (!encode_map(&maps.m[2 * p + 1], ph[p].opB, 4, BK, false)) return cudaErrorInvalidValue;
+  }
+  constexpr auto k = dmma_chain_kernel<BM, BN, WM, WN, STAGES>;
+  set_smem_once<k>((int)C::SMEM);
+  static const int occ = [] {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, C::kThreads, C::SMEM) != cudaSuccess) o = 1;
+    return o < 1 ? 1 : o;
+  }();
+  static const int occ_cap = [] { const char* e = std::getenv("TRINV_CHAIN_OCC"); return e ? atoi(e) : 0; }();
+  int64_t grid = (int64_t)(occ_cap > 0 && occ_cap < occ ? occ_cap : occ) * device_sms();
+  if (grid > c.tile0[nphase]) grid = c.tile0[nphase];
+  cudaError_t e = cudaMemsetAsync(counters, 0, (size_t)nphase * cstride * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  e = launch_k(k, dim3((unsigned)grid), dim3(C::kThreads), C::SMEM, s, maps, c);
+  if (launches) ++*launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_level(const LevelArgs& a_in, cudaStream_t s, int64_t* launches) {
   LevelArgs a = a_in;
   ProfileScope prof(KIND_DMMA, level_flops(a), 0.0, s);

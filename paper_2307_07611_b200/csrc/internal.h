@@ -138,6 +138,14 @@ constexpr int LEVEL_FLAG_MAX = 16384 - LEVEL_TICKETS;
 // second; l1.sync = the call's LEVEL_SYNC_BYTES, zeroed once per call; epoch in 1..63.
 bool level_split_fixup();
 bool level_sk_enabled();  // TRINV_SK=1: stream-K launches of the mid-size levels (opt-in)
+// Level chain (gemm.cu): the lowest levels that run 32x32 tiles, all their products in one
+// persistent dependency-driven launch.  ph[0..nphase) = [W, X21] per level, W by position
+// (first products: out = W with ld = the widest chained level, out_rows = n; second products
+// read W through a map of n rows); counters: nphase * cstride ints of device scratch.
+bool level_chain_enabled();
+bool level_uses_t32(const LevelArgs& a);
+cudaError_t launch_level_chain(const LevelArgs* ph, int nphase, int* counters, int cstride, cudaStream_t s,
+                               int64_t* launches);
 bool level_fusable(const LevelArgs& l1);
 cudaError_t launch_level_fused(const LevelArgs& l1, const LevelArgs& l2, int epoch, cudaStream_t s,
                                int64_t* launches);

@@ -641,7 +641,55 @@ static trinv_status_t run_tri(char uplo, int64_t n, const double* A, int64_t lda
   const int64_t b_end = b_stop > 0 ? b_stop : n;
   int fused_epoch = 0;
   bool sk_zeroed = false;
-  for (int64_t b = bw; b < b_end && b < n; b *= 2) {
+  int64_t b_first = bw;
+  // the lowest levels that run 32x32 tiles: one persistent dependency-driven launch (gemm.cu)
+  if (aux && bw == BLK_MAX && b_stop == 0 && level_chain_enabled() && product_engine() == 0 && !level_sk_enabled() &&
+      !level_split_fixup()) {
+    static const bool opt_out = [] {  // the other opt-in level experiments keep their launches
+      const char* a = std::getenv("TRINV_SPLITK");
+      const char* f = std::getenv("TRINV_FUSED");
+      return (a && atoi(a) != 0) || (f && f[0] == '1');
+    }();
+    LevelArgs ph[8];
+    int np = 0;
+    int64_t bmax = 0, b = bw;
+    for (; b < n && np + 2 <= 8; b *= 2) {
+      const int64_t merges = merges_at(n, b);
+      LevelArgs t{};
+      t.mode = uplo == 'L' ? MODE_LOWER_1 : MODE_UPPER_1; t.n = n; t.b = b; t.merges = merges;
+      if (opt_out || !level_uses_t32(t) || (strassen_top(n, b)) ||
+          (size_t)n * (size_t)b * sizeof(double) > w_bytes(n))
+        break;
+      bmax = b;
+      np += 2;
+    }
+    if (np >= 4) {  // at least two levels (one level gains nothing over two launches)
+      const int64_t ldw = bmax;
+      np = 0;
+      for (int64_t bb = bw; bb <= bmax; bb *= 2) {
+        const int64_t merges = merges_at(n, bb);
+        const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, n, bmax, ldw};
+        LevelArgs& l1 = ph[np++];
+        LevelArgs& l2 = ph[np++];
+        l1 = LevelArgs{}; l2 = LevelArgs{};
+        l1.n = l2.n = n; l1.b = l2.b = bb; l1.merges = l2.merges = merges;
+        l1.out = W; l1.ldo = ldw; l1.out_rows = n; l1.out_cols = bb; l1.alpha = 1.0;
+        l2.out = X; l2.ldo = ldx; l2.out_rows = n; l2.out_cols = n; l2.alpha = -1.0;
+        l2.mir = X; l2.ldm = ldx;
+        if (uplo == 'L') {
+          l1.mode = MODE_LOWER_1; l1.opA = in; l1.opB = xr;
+          l2.mode = MODE_LOWER_2; l2.opA = xr; l2.opB = wr;
+        } else {
+          l1.mode = MODE_UPPER_1; l1.opA = xr; l1.opB = in;
+          l2.mode = MODE_UPPER_2; l2.opA = wr; l2.opB = xr;
+        }
+      }
+      int* counters = reinterpret_cast<int*>(static_cast<char*>(aux) + strassen_scratch(n));
+      TRY(launch_level_chain(ph, np, counters, (int)merges_at(n, bw), s, &g_launches));
+      b_first = 2 * bmax;
+    }
+  }
+  for (int64_t b = b_first; b < b_end && b < n; b *= 2) {
     const int64_t merges = merges_at(n, b);
     const MatRef in{A, n, n, lda}, xr{X, n, n, ldx}, wr{W, merges * b, b, b};
     LevelArgs l1{}, l2{};

@@ -2,7 +2,8 @@
 behind an environment variable read once per process, hence one subprocess per setting):
 serial split-K (TRINV_SPLITK=1, 64x64 and 32x32 tiles), split-K with the last-chunk fix-up
 (TRINV_SPLITK=2), fused level launches (TRINV_FUSED=1), programmatic dependent launch
-(TRINV_PDL=1) and stream-K level launches (TRINV_SK=1; WMIN=2 cuts tiles into several pieces).  Each must still match the oracle: full parity at n = 1024 / 2048 (lower and
+(TRINV_PDL=1), stream-K level launches (TRINV_SK=1; WMIN=2 cuts tiles into several pieces) and the
+persistent dependency-driven level chain (TRINV_CHAIN=1; OCC=1 makes every CTA walk many tiles).  Each must still match the oracle: full parity at n = 1024 / 2048 (lower and
 upper, ragged n = 1500) and bit-for-bit determinism."""
 import os
 import subprocess
@@ -37,8 +38,10 @@ print('BAD', bad)
                                  {"TRINV_SPLITK": "2", "TRINV_SPLITK_T": "32", "TRINV_SPLITK_KC": "256"},
                                  {"TRINV_SPLITK": "2"}, {"TRINV_FUSED": "1"}, {"TRINV_PDL": "1"},
                                  {"TRINV_SK": "1", "TRINV_SK_BMIN": "128"},
-                                 {"TRINV_SK": "1", "TRINV_SK_TILE": "12864", "TRINV_SK_BMIN": "128", "TRINV_SK_WMIN": "2"}],
-                         ids=["splitk1", "splitk1-t32", "splitk2-t32", "splitk2", "fused", "pdl", "sk64", "sk128x64"])
+                                 {"TRINV_SK": "1", "TRINV_SK_TILE": "12864", "TRINV_SK_BMIN": "128", "TRINV_SK_WMIN": "2"},
+                                 {"TRINV_CHAIN": "1"}, {"TRINV_CHAIN": "1", "TRINV_CHAIN_OCC": "1"}],
+                         ids=["splitk1", "splitk1-t32", "splitk2-t32", "splitk2", "fused", "pdl", "sk64", "sk128x64",
+                              "chain", "chain-occ1"])
 def test_optin_path_parity(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", _SCRIPT], cwd=root, env=dict(os.environ, **env), capture_output=True,

@@ -175,7 +175,10 @@ __device__ __forceinline__ void leaf32_compute(const double* T, double* rr, int 
   leaf32_steps<UPPER, BR>(T, rr, x, std::make_integer_sequence<int, LEAF / 2>{});
 }
 
-template <bool UPPER, int WARPS, int NS, int BR>
+// BULK (opt-in TRINV_LEAF_BULK=1..3, measured no faster: profiles/r02_leaf_bulk.txt): the inverse
+// leaves through an 8 KiB shared-memory staging buffer per warp and one cp.async.bulk shared ->
+// global copy per matrix (contiguous 32x32 outputs only) instead of 32 row stores from registers.
+template <bool UPPER, int WARPS, int NS, int BR, bool BULK = false>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     leaf32_tma_kernel(const __grid_constant__ BandMaps<BR> maps, const LeafArgs a) {
   using BD = Band<BR>;
@@ -186,6 +189,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   double* rr = reinterpret_cast<double*>(smem_raw) + (size_t)WARPS * NS * SLOT + warp * LEAF;
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem_raw + ((size_t)WARPS * NS * SLOT + WARPS * LEAF) * 8) + warp * NS;
+  constexpr size_t STAGE_OFF = (((size_t)WARPS * NS * SLOT + WARPS * LEAF) * 8 + WARPS * NS * 8 + 127) & ~size_t(127);
+  double* stage = reinterpret_cast<double*>(smem_raw + STAGE_OFF) + (size_t)warp * LEAF * LEAF;
 
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t TW = (int64_t)gridDim.x * WARPS;
@@ -231,12 +236,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
     double* dst = a.X + b * a.sX;
     const int col = UPPER ? LEAF - 1 - lane : lane;
+    if constexpr (BULK) {
+      if (t > 0) {  // the previous matrix's bulk store has read the staging buffer
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+      }
 #pragma unroll
-    for (int i = 0; i < LEAF; ++i) {
-      const int row = UPPER ? LEAF - 1 - i : i;
-      dst[(int64_t)row * a.ldx + col] = (i < lane) ? 0.0 : x[i];
+      for (int i = 0; i < LEAF; ++i) {
+        const int row = UPPER ? LEAF - 1 - i : i;
+        stage[row * LEAF + col] = (i < lane) ? 0.0 : x[i];
+      }
+      fence_proxy_async_smem();  // generic smem writes -> the bulk copy's reads
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g(dst, stage, LEAF * LEAF * 8);
+        bulk_commit();
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < LEAF; ++i) {
+        const int row = UPPER ? LEAF - 1 - i : i;
+        dst[(int64_t)row * a.ldx + col] = (i < lane) ? 0.0 : x[i];
+      }
     }
     leaf_report(a, b, lane, singular, first_zero);
+  }
+  if constexpr (BULK) {
+    if (lane == 0) bulk_wait<0>();  // the last store complete before the CTA's shared memory goes
   }
 }
 
@@ -775,20 +801,21 @@ static bool encode_batch_map(CUtensorMap* m, const LeafArgs& a, int cols, int ro
   return encode_map_nd(m, a.A, 3, dims, strides, box);
 }
 
-template <int W, int NS, int BR>
+template <int W, int NS, int BR, bool BULK = false>
 static bool launch_band(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
   BandMaps<BR> maps;
   for (int w = 1; w <= Band<BR>::NBAND; ++w)
     if (!encode_batch_map(&maps.m[w - 1], a, BR * w, BR)) return false;
-  constexpr size_t smem = ((size_t)W * NS * Band<BR>::SLOT + W * LEAF) * 8 + W * NS * 8;
+  constexpr size_t base = ((size_t)W * NS * Band<BR>::SLOT + W * LEAF) * 8 + W * NS * 8;
+  constexpr size_t smem = BULK ? ((base + 127) & ~size_t(127)) + (size_t)W * LEAF * LEAF * 8 : base;
   const int64_t ctas_needed = (a.batch + W - 1) / W;
   const int grid = (int)(ctas_needed < sms ? ctas_needed : sms);
   if (uplo == 'L') {
-    constexpr auto k = leaf32_tma_kernel<false, W, NS, BR>;
+    constexpr auto k = leaf32_tma_kernel<false, W, NS, BR, BULK>;
     set_smem_once<k>((int)smem);
     k<<<grid, W * 32, smem, s>>>(maps, a);
   } else {
-    constexpr auto k = leaf32_tma_kernel<true, W, NS, BR>;
+    constexpr auto k = leaf32_tma_kernel<true, W, NS, BR, BULK>;
     set_smem_once<k>((int)smem);
     k<<<grid, W * 32, smem, s>>>(maps, a);
   }
@@ -871,7 +898,12 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
     launched = true;
   }
   if (!launched && tma && full32 && a.batch < (int64_t)1 << 31) {
-    if (br == 16) launched = launch_band<8, 3, 16>(uplo, a, sms, s);
+    static const int bulk = [] { const char* e = std::getenv("TRINV_LEAF_BULK"); return e ? atoi(e) : 0; }();
+    const bool contiguous = a.ldx == LEAF && a.sX == LEAF * LEAF;
+    if (br == 16 && bulk == 1 && contiguous) launched = launch_band<8, 3, 16, true>(uplo, a, sms, s);
+    else if (br == 16 && bulk == 2 && contiguous) launched = launch_band<8, 2, 16, true>(uplo, a, sms, s);
+    else if (br == 16 && bulk == 3 && contiguous) launched = launch_band<6, 4, 16, true>(uplo, a, sms, s);
+    else if (br == 16) launched = launch_band<8, 3, 16>(uplo, a, sms, s);
     else if (br == 8) launched = launch_band<8, 4, 8>(uplo, a, sms, s);
     else launched = launch_band<8, 4, 4>(uplo, a, sms, s);
   }

@@ -43,6 +43,23 @@ def _ld(t):
     return t.shape[-1]
 
 
+def _on_stream(fn):
+    """Run a binding call with its `stream` (if given) as torch's current stream, so that the
+    workspace, info and output tensors the call allocates belong to that stream's memory pool
+    (the caching allocator may otherwise hand a freed workspace to another stream while this
+    call's kernels still use it) and a synchronous read of `info` is ordered after them."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        stream = kwargs.get("stream")
+        if stream is None:
+            return fn(*args, **kwargs)
+        with _torch().cuda.stream(stream):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
 def _stream(stream):
     torch = _torch()
     s = torch.cuda.current_stream() if stream is None else stream
@@ -102,16 +119,19 @@ def _tri(uplo, A, unit, out, check, stream):
     return X
 
 
+@_on_stream
 def trinv_lower(A, *, unit=False, out=None, check=False, stream=None):
     """X = A^{-1} for lower-triangular A (only the lower triangle is used)."""
     return _tri("L", A, unit, out, check, stream)
 
 
+@_on_stream
 def trinv_upper(A, *, unit=False, out=None, check=False, stream=None):
     """X = A^{-1} for upper-triangular A (only the upper triangle is used)."""
     return _tri("U", A, unit, out, check, stream)
 
 
+@_on_stream
 def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None):
     """X[b] = A[b]^{-1} for A of shape [B, n, n], n <= 128.  Returns X, or (X, info[B]) if info."""
     torch = _torch()
@@ -132,6 +152,7 @@ def trinv_batched(A, uplo="L", *, unit=False, out=None, info=False, stream=None)
     return (X, inf) if info else X
 
 
+@_on_stream
 def trinv_batched_host(A_host, uplo="L", *, unit=False, out=None, chunk=0, info=False, device=None,
                        stream=None):
     """Invert a HOST batch [B, n, n] (contiguous, ideally pinned): chunked H2D / invert / D2H
@@ -157,6 +178,7 @@ def trinv_batched_host(A_host, uplo="L", *, unit=False, out=None, chunk=0, info=
     return (X, inf) if info else X
 
 
+@_on_stream
 def trinv_beta(A, uplo="L", beta=4, *, unit=False, out=None, check=False, stream=None):
     """Triangular inverse with a COMBRIT top level of block count beta (2 or 4; NEXT row f4)."""
     torch = _torch()
@@ -174,6 +196,7 @@ def trinv_beta(A, uplo="L", beta=4, *, unit=False, out=None, check=False, stream
     return X
 
 
+@_on_stream
 def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", stream=None):
     """C = alpha A B + beta C on the DMMA engine; A [.., M, K], B [.., K, N] (optionally batched
     with a leading batch dimension); struct_a / struct_b = 'L' / 'U' declare a triangular operand."""
@@ -198,6 +221,7 @@ def gemm(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", strea
     return C
 
 
+@_on_stream
 def gemm_oz(A, B, *, C=None, alpha=1.0, beta=0.0, struct_a="N", struct_b="N", digits=0, stream=None):
     """C = alpha A B + beta C, FP64-emulated (Ozaki-II) on the INT8 tensor cores: 16 moduli
     + CRT (trinv_gemm_oz; digits must be 0, the digit-splitting variant was retired)."""
@@ -245,6 +269,7 @@ def product_min_block():
     return _MIN_BLOCK
 
 
+@_on_stream
 def int8_scaling_ok(A, uplo="N", unit=False, stream=None):
     """The INT8 engine's scaling guard (trinv_int8_scaling_ok): True when A's row / column
     maxima span at most 8 binades and every entry is finite (only the `uplo` triangle read
@@ -261,6 +286,7 @@ def product_engine():
     return {0: "dmma", 2: "int8crt"}[lib().trinv_get_product_engine()]
 
 
+@_on_stream
 def gemm_strassen(A, B, *, C=None, stream=None):
     """C = A B (dense n x n) with one Strassen level over the DMMA GEMM (NEXT row f3, measurement)."""
     torch = _torch()
@@ -274,6 +300,7 @@ def gemm_strassen(A, B, *, C=None, stream=None):
     return C
 
 
+@_on_stream
 def lu_crout(A, *, check=False, stream=None):
     """In-place Crout factorisation without pivoting (SKUL): A <- L\\U packed,
     L lower with its diagonal, U unit upper (strict upper part stored)."""
@@ -288,6 +315,7 @@ def lu_crout(A, *, check=False, stream=None):
     return A
 
 
+@_on_stream
 def inv_general(A, *, out=None, check=False, stream=None):
     """X = A^{-1} for a general matrix with non-zero leading principal minors (Crout LU without
     pivoting, then U^{-1} L^{-1})."""
@@ -305,6 +333,7 @@ def inv_general(A, *, out=None, check=False, stream=None):
     return X
 
 
+@_on_stream
 def inv_from_lu(L, U, *, unit_l=True, unit_u=False, out=None, check=False, stream=None):
     """X = (L U)^{-1} = U^{-1} L^{-1} from a lower factor L and an upper factor U."""
     torch = _torch()

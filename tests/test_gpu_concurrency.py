@@ -33,3 +33,29 @@ def test_concurrent_strassen_products(n):
         for c, r in zip(Cs, ref):
             bad += not (((c - r).abs().max() / r.abs().max()).item() < 1e-12)
     assert bad == 0, f"{bad} of {25 * k} concurrent Strassen products wrong"
+
+
+def test_concurrent_trinv_bitwise_equal_serial():
+    """Two trinv calls that take the Strassen top merge (n = 16384, lower and upper) on two streams
+    at the same time give bit-for-bit the results of the same calls run one after another (the
+    DMMA path, Strassen included, is deterministic)."""
+    import synth
+    dev = torch.device("cuda:0")
+    n = 16384
+    TL = torch.empty((n, n), dtype=torch.float64, device=dev)
+    TU = torch.empty_like(TL)
+    synth.device_fill(TL, n, uplo="L", diag="signed")
+    synth.device_fill(TU, n, uplo="U", diag="pos")
+    refL = P.trinv_lower(TL)
+    refU = P.trinv_upper(TU)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        XL = torch.empty_like(TL)
+        XU = torch.empty_like(TU)
+        torch.cuda.synchronize()
+        P.trinv_lower(TL, out=XL, stream=s0)
+        P.trinv_upper(TU, out=XU, stream=s1)
+        torch.cuda.synchronize()
+        assert torch.equal(XL, refL)
+        assert torch.equal(XU, refU)

@@ -103,8 +103,10 @@ def test_inv_general_zero_pivot_and_layout():
     assert oracle.floored_rel_err(X, oracle.inv_general(A)) <= REL_TOL
 
 
-def test_inv_general_n8192_sampled():
-    n = 8192
+@pytest.mark.parametrize("n", [8192, 5000])
+def test_inv_general_n8192_sampled(n):
+    """BASELINE-scale general inverse (8192) and a ragged order (5000: uneven LU splits, ragged
+    merges in the inverse factors): 64 columns against the SKUL oracle, A X - I gate."""
     Lg = torch.empty((n, n), dtype=torch.float64, device=DEV)
     Ug = torch.empty_like(Lg)
     synth.device_fill(Lg, n, seed=5, tag="L", diag="pos")

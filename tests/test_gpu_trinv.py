@@ -144,6 +144,21 @@ def test_config2_n8192_lower():
     assert torch.all(torch.triu(X, 1) == 0)
 
 
+@pytest.mark.parametrize("n,uplo", [(3000, "L"), (5000, "U"), (6144, "L"), (12345, "U")])
+def test_sampled_ragged_large(n, uplo):
+    """Orders that are not powers of two above the full-parity range: ragged last merges on the
+    64x64 / 64x32 level tiles (and the 128-tile / quadrant decisions at their sizes), 64 oracle
+    columns including the boundary columns of the top split."""
+    Ad = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    synth.device_fill(Ad, n, uplo=uplo, diag="signed" if uplo == "L" else "pos", seed=n)
+    X = (P.trinv_lower if uplo == "L" else P.trinv_upper)(Ad)
+    T = Ad.cpu().numpy()
+    assert np.array_equal(T[:48, :48], synth.host(n, seed=n, uplo=uplo, diag="signed" if uplo == "L" else "pos")[:48, :48])
+    _sampled(T, X, uplo, 7)
+    opp = torch.triu(X, 1) if uplo == "L" else torch.tril(X, -1)
+    assert bool(torch.all(opp == 0))
+
+
 @pytest.mark.slow
 def test_config3_n32768_upper():
     n = 32768
@@ -155,6 +170,23 @@ def test_config3_n32768_upper():
     del Ad
     _sampled(T, X, "U", 3)
     assert bool(torch.all(torch.tril(X[:4096, :4096], -1) == 0))
+
+
+def test_inv_from_lu_ragged_sampled():
+    """inv_from_lu at a ragged order (6000): 64 columns against the oracle's y = L^-1 e_j,
+    x = U^-1 y, and the factored residual rho_LU (reading C21)."""
+    n = 6000
+    Ld = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    Ud = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    synth.device_fill(Ld, n, tag="L", diag="one")
+    synth.device_fill(Ud, n, tag="U", uplo="U", diag="pos")
+    X = P.inv_from_lu(Ld, Ud)
+    cols = sample_columns(n, 8)
+    Xs = X[:, torch.from_numpy(cols).to(DEV)].T.contiguous().cpu().numpy()
+    L = Ld.cpu().numpy(); U = Ud.cpu().numpy()
+    ref = oracle.lu_columns(L, U, cols, unit_l=True)
+    assert oracle.floored_rel_err(Xs, ref, axis_cols=0) <= REL_TOL
+    assert oracle.factored_column_residual_ratio(L, U, Xs, cols) <= RES_TOL
 
 
 def test_inv_from_lu_small():

@@ -757,6 +757,202 @@ __global__ void __launch_bounds__(256) leaf16_kernel(const LeafArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// n = 32, four matrices per warp (opt-in TRINV_LEAF32=quad, TRINV_LEAF32_QCFG = warps x slots
+// [x CTAs per SM]; measured 8-10% slower than the band kernel, profiles/r02_leaf_quad.txt:
+// it cuts the shared wavefronts to 143 per matrix and l1tex to 51%, but with ~255 registers per
+// thread and 17.5 KB per quad slot only 4-6 warps fit per SM and it is latency-bound).  Same recurrence as the
+// band kernel (proof of Thm 1, right-looking; CRIT P:568-581 for the upper case
+// through T' = J U J), but quarter-warp h (lanes 8h .. 8h+7) owns matrix 4g + h and lane
+// c of a quarter computes the four columns 2c, 2c+1, 2c+16, 2c+17 of its inverse.
+// Why (ncu of the band kernel, profiles/r02_ncu_leaf32_full.txt): one warp per matrix makes
+// every T_ik a warp-wide broadcast, and a 16-byte broadcast costs two shared-memory
+// wavefronts for 16 useful bytes: 546 wavefronts per matrix plus 64 for the row stores and
+// 48 for the TMA fills put l1tex at 96%, so the kernel is bound by the LSU exactly where
+// DRAM also saturates (compressing the output's zero triangle cut the DRAM writes by a third
+// and did not change the time: profiles/r02_leaf_quad.txt).  Here one 16-byte load serves
+// four matrices (the four quarters read the same offset of four regions whose bases differ
+// by 32 bytes mod 128: four disjoint bank groups) and each T_ik feeds four columns, so the
+// shared traffic per matrix drops ~4x; columns 2c+16, 2c+17 skip the 16 steps in which they
+// are structurally zero (31% fewer FP64 instructions than one warp per matrix).  Rows K, K+1
+// are stored as soon as step pair K has finalised them (their registers die early).
+// Staging: per-lane 16-byte cp.async of the referenced triangle, rows rounded to 16-byte
+// pairs (272 chunks, 4352 B per matrix, packed row after row: row i starts at chunk P(i) =
+// floor(i/2) floor(i/2 + 1) + (i odd) (floor(i/2) + 1)); the upper case stores T' rows
+// (U row 31 - i, pairs in reverse order, the two doubles of a pair swapped on read).
+// Stores: per row two 16-byte stores per lane (a quarter writes one 128-byte line).
+constexpr int QCH = 272;            // 16-byte chunks of a packed triangle
+constexpr int QMAT = 2 * QCH + 4;   // doubles per matrix region: 4384 B = 32 mod 128 (bank shift)
+constexpr int QSLOT = 4 * QMAT;     // doubles per quad slot
+constexpr int QRR = 36;             // doubles per reciprocal vector (288 B = 32 mod 128)
+__host__ __device__ constexpr int qP(int i) { return (i / 2) * (i / 2 + 1) + (i & 1) * (i / 2 + 1); }
+static_assert(qP(32) == QCH && (QMAT * 8) % 128 == 32 && (QRR * 8) % 128 == 32, "quad layout");
+
+template <bool UPPER>
+__device__ __forceinline__ double2 q_pair(const double* T, int i, int k) {  // (T'_ik, T'_i,k+1), k even
+  const double2 v = *reinterpret_cast<const double2*>(T + 2 * qP(i) + k);
+  return UPPER ? make_double2(v.y, v.x) : v;
+}
+template <bool UPPER>
+__device__ __forceinline__ double q_elem(const double* T, int i, int k) {  // T'_ik
+  return T[2 * qP(i) + (UPPER ? (k ^ 1) : k)];
+}
+
+// x0[i] = (X'_{i,2c}, X'_{i,2c+1}), rows 0..31; x1[i-16] = (X'_{i,2c+16}, X'_{i,2c+17}), rows 16..31
+// (double2: each pair lives in an aligned register quad, stored by one 16-byte store).
+template <int K, int OFF, int N>
+__device__ __forceinline__ void q_head(double2 (&x)[N], double2 r, double sub, double2& xk, double2& xk1) {
+  double2& u = x[K - OFF];
+  double2& v = x[K + 1 - OFF];
+  u.x *= r.x;
+  u.y *= r.x;
+  v.x = fma(-sub, u.x, v.x) * r.y;
+  v.y = fma(-sub, u.y, v.y) * r.y;
+  xk = u;
+  xk1 = v;
+}
+// Rows K and K+1 of X' are final once the head of step pair K has run: they are stored right
+// there (the opposite triangle masked to +0.0, row a7), so their registers die early.
+template <bool UPPER, int I>
+__device__ __forceinline__ void q_store_row(double* dst, int64_t ldx, int c, double2 (&x0)[32], double2 (&x1)[16]) {
+  double2 v = x0[I];
+  if (I < 2 * c) v.x = 0.0;
+  if (I < 2 * c + 1) v.y = 0.0;
+  double2 w = make_double2(0.0, 0.0);
+  if constexpr (I >= 16) {
+    w = x1[I - 16];
+    if (I < 2 * c + 16) w.x = 0.0;
+    if (I < 2 * c + 17) w.y = 0.0;
+  }
+  if (!UPPER) {
+    double* row = dst + (int64_t)I * ldx;
+    *reinterpret_cast<double2*>(row + 2 * c) = v;
+    *reinterpret_cast<double2*>(row + 2 * c + 16) = w;
+  } else {  // X = J X' J: T' (i, j) -> (31 - i, 31 - j); columns 30-2c, 31-2c as one pair
+    double* row = dst + (int64_t)(LEAF - 1 - I) * ldx;
+    *reinterpret_cast<double2*>(row + 30 - 2 * c) = make_double2(v.y, v.x);
+    *reinterpret_cast<double2*>(row + 14 - 2 * c) = make_double2(w.y, w.x);
+  }
+}
+template <bool UPPER, int K>
+__device__ __forceinline__ void q_step(const double* T, const double* rr, double2 (&x0)[32], double2 (&x1)[16],
+                                       double* dst, int64_t ldx, int c, bool live) {
+  const double2 r = *reinterpret_cast<const double2*>(rr + K);
+  const double sub = q_elem<UPPER>(T, K + 1, K);
+  double2 a0, b0, a1, b1;
+  q_head<K, 0>(x0, r, sub, a0, b0);
+  if constexpr (K >= 16) q_head<K, 16>(x1, r, sub, a1, b1);
+#pragma unroll
+  for (int i = K + 2; i < LEAF; ++i) {
+    const double2 t = q_pair<UPPER>(T, i, K);
+    x0[i].x = fma(-t.y, b0.x, fma(-t.x, a0.x, x0[i].x));
+    x0[i].y = fma(-t.y, b0.y, fma(-t.x, a0.y, x0[i].y));
+    if constexpr (K >= 16) {
+      x1[i - 16].x = fma(-t.y, b1.x, fma(-t.x, a1.x, x1[i - 16].x));
+      x1[i - 16].y = fma(-t.y, b1.y, fma(-t.x, a1.y, x1[i - 16].y));
+    }
+  }
+  if (live) {
+    q_store_row<UPPER, K>(dst, ldx, c, x0, x1);
+    q_store_row<UPPER, K + 1>(dst, ldx, c, x0, x1);
+  }
+}
+template <bool UPPER, int... P>
+__device__ __forceinline__ void q_steps(const double* T, const double* rr, double2 (&x0)[32], double2 (&x1)[16],
+                                        double* dst, int64_t ldx, int c, bool live, std::integer_sequence<int, P...>) {
+  (q_step<UPPER, 2 * P>(T, rr, x0, x1, dst, ldx, c, live), ...);
+}
+
+template <bool UPPER, int WARPS, int NS>
+__global__ void __launch_bounds__(WARPS * 32, 1) leaf32_quad_kernel(const LeafArgs a) {
+  extern __shared__ __align__(128) double qsmem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 3, c = lane & 7;
+  double* slots = qsmem + (size_t)warp * NS * QSLOT;
+  double* rr = qsmem + (size_t)WARPS * NS * QSLOT + (warp * 4 + h) * QRR;
+  const int64_t nquads = (a.batch + 3) / 4;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t TW = (int64_t)gridDim.x * WARPS;
+  if (gw >= nquads) return;
+  const int64_t count = (nquads - gw + TW - 1) / TW;
+
+  // quarter h copies matrix 4g + h: row i, pair c (every row) and pair c + 8 (rows >= 16)
+  auto issue = [&](int64_t t) {
+    if (t < count) {
+      const int64_t b = 4 * (gw + t * TW) + h;
+      if (b < a.batch) {
+        // source row pointer walked by +-lda (no per-row offsets held in registers)
+        const double* src = a.A + b * a.sA + (UPPER ? (LEAF - 1) * a.lda + 30 - 2 * c : 2 * c);
+        const int64_t step = UPPER ? -a.lda : a.lda;
+        double* dst = slots + (t % NS) * QSLOT + h * QMAT + 2 * c;
+#pragma unroll
+        for (int i = 0; i < LEAF; ++i) {
+          if (c <= i / 2) cpa16(dst + 2 * qP(i), src);                                         // pair c
+          if (i >= 16 && c + 8 <= i / 2) cpa16(dst + 2 * qP(i) + 16, src + (UPPER ? -16 : 16));  // pair c + 8
+          src += step;
+        }
+      }
+    }
+    cpa_commit();  // one group per slot, empty past the end (uniform wait counts)
+  };
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) issue(t);
+
+  for (int64_t t = 0; t < count; ++t) {
+    issue(t + NS - 1);
+    cpa_wait<NS - 1>();
+    __syncwarp();
+    const int64_t b = 4 * (gw + t * TW) + h;
+    const bool live = b < a.batch;
+    const double* T = slots + (t % NS) * QSLOT + h * QMAT;
+    // a1: reciprocals of T' rows c + 8m (IEEE division: X_jj == 1/T_jj bitwise, C4)
+    unsigned zq = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = c + 8 * m;
+      const double d = q_elem<UPPER>(T, j, j);
+      const unsigned bal = __ballot_sync(0xffffffffu, live && !a.unit && d == 0.0);
+      zq |= ((bal >> (8 * h)) & 0xffu) << (8 * m);
+      rr[j] = a.unit ? 1.0 : 1.0 / d;
+    }
+    __syncwarp();
+    double2 x0[32], x1[16];
+#pragma unroll
+    for (int i = 0; i < LEAF; ++i) x0[i] = make_double2(i == 2 * c ? 1.0 : 0.0, i == 2 * c + 1 ? 1.0 : 0.0);
+#pragma unroll
+    for (int i = 16; i < LEAF; ++i) x1[i - 16] = make_double2(i == 2 * c + 16 ? 1.0 : 0.0, i == 2 * c + 17 ? 1.0 : 0.0);
+    double* dst = a.X + (live ? b : 0) * a.sX;
+    q_steps<UPPER>(T, rr, x0, x1, dst, a.ldx, c, live, std::make_integer_sequence<int, LEAF / 2>{});
+    __syncwarp();  // every lane is done with the slot and rr: the next loads may overwrite them
+    if (live) {
+      if (c == 0) {
+        const unsigned zmask = UPPER ? __brev(zq) : zq;  // original row order
+        const int fz = zmask ? __ffs(zmask) - 1 : -1;
+        if (a.info_mode == 1) a.info[b] = zmask ? fz + 1 : 0;
+        else if (a.info_mode == 2 && zmask)
+          info_min_nonzero(a.info, static_cast<int32_t>(a.info_off + b * a.info_stride + fz + 1));
+      }
+    }
+  }
+  cpa_wait<0>();
+}
+
+template <int W, int NS, int CPS = 1>  // CPS: CTAs per SM
+static void launch_quad(char uplo, const LeafArgs& a, int sms, cudaStream_t s) {
+  constexpr size_t smem = ((size_t)W * NS * QSLOT + (size_t)W * 4 * QRR) * 8;
+  static_assert(smem * CPS <= 227 * 1024, "quad smem");
+  const int64_t ctas_needed = ((a.batch + 3) / 4 + W - 1) / W;
+  const int grid = (int)(ctas_needed < (int64_t)sms * CPS ? ctas_needed : (int64_t)sms * CPS);
+  if (uplo == 'L') {
+    constexpr auto k = leaf32_quad_kernel<false, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(a);
+  } else {
+    constexpr auto k = leaf32_quad_kernel<true, W, NS>;
+    set_smem_once<k>((int)smem);
+    k<<<grid, W * 32, smem, s>>>(a);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Plain-load kernel for any layout (odd n / ld, unaligned pointers): one warp
 // per matrix, rows loaded coalesced into a smem slot, result stored directly.
 template <bool UPPER>
@@ -868,6 +1064,24 @@ cudaError_t launch_leaf(char uplo, const LeafArgs& a, cudaStream_t s, int64_t* l
   static const int mcfg = [] { const char* e = std::getenv("TRINV_LEAF32_CFG"); return e ? std::atoi(e) : 1063; }();
   static const int pcfg = [] { const char* e = std::getenv("TRINV_LEAF32_PCFG"); return e ? std::atoi(e) : 82; }();
   bool launched = false;
+  static const bool quad = [] { const char* e = std::getenv("TRINV_LEAF32"); return e && !strcmp(e, "quad"); }();
+  static const int qcfg = [] { const char* e = std::getenv("TRINV_LEAF32_QCFG"); return e ? std::atoi(e) : 43; }();
+  if (quad && tma && full32 && a.batch < (int64_t)1 << 31) {
+    switch (qcfg) {
+      case 62: launch_quad<6, 2>(uplo, a, sms, s); break;
+      case 33: launch_quad<3, 3>(uplo, a, sms, s); break;
+      case 42: launch_quad<4, 2>(uplo, a, sms, s); break;
+      case 52: launch_quad<5, 2>(uplo, a, sms, s); break;
+      case 32: launch_quad<3, 2>(uplo, a, sms, s); break;
+      case 24: launch_quad<2, 4>(uplo, a, sms, s); break;
+      case 223: launch_quad<2, 2, 3>(uplo, a, sms, s); break;
+      case 126: launch_quad<1, 2, 6>(uplo, a, sms, s); break;
+      case 322: launch_quad<3, 2, 2>(uplo, a, sms, s); break;
+      case 134: launch_quad<1, 3, 4>(uplo, a, sms, s); break;
+      default: launch_quad<4, 3>(uplo, a, sms, s); break;
+    }
+    launched = true;
+  }
   // two matrices per warp (TRINV_LEAF32=pair; TRINV_LEAF32_PCFG = [100 full-row stores +] warps x
   // pair-slots): half the LSU wavefronts and 37% fewer FP64 instructions per matrix, yet 10%
   // slower than the band kernel in every shape (profiles/r02_leaf_pair.txt)

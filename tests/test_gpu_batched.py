@@ -245,7 +245,8 @@ print('BAD', bad)
 """
 
 
-@pytest.mark.parametrize("mode,cfg", [("mma", "1063"), ("mma", "83"), ("pair", "82"), ("pair", "182"), ("pair", "43")])
+@pytest.mark.parametrize("mode,cfg", [("mma", "1063"), ("mma", "83"), ("pair", "82"), ("pair", "182"), ("pair", "43"),
+                                      ("quad", "43"), ("quad", "62"), ("quad", "33")])
 def test_leaf32_variant_parity(mode, cfg):
     """The opt-in n = 32 kernels (read once per process, hence a subprocess): the DMMA-merge
     kernel (TRINV_LEAF32=mma, pipelined and plain) and the two-matrices-per-warp kernel
@@ -255,7 +256,7 @@ def test_leaf32_variant_parity(mode, cfg):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TRINV_LEAF32=mode, TRINV_LEAF32_CFG=cfg, TRINV_LEAF32_PCFG=cfg)
+    env = dict(os.environ, TRINV_LEAF32=mode, TRINV_LEAF32_CFG=cfg, TRINV_LEAF32_PCFG=cfg, TRINV_LEAF32_QCFG=cfg)
     r = subprocess.run([sys.executable, "-c", _MMA_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

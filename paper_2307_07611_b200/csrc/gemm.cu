@@ -344,7 +344,7 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   __shared__ int s_unit;
   // PDL: let the next kernel's CTAs be scheduled as this grid drains, and wait for the
   // previous kernel before touching global memory (no-ops without the launch attribute)
-  pdl_launch_dependents();
+  pdl_trigger_early();
   pdl_wait();
   int* sync = TR::sync(p);
   if (sync) {
@@ -1371,7 +1371,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
 // ---------------------------------------------------------------------------
 // rows over blockIdx.y (grid-strided), columns over blockIdx.x / threads: no division per entry
 __global__ void zero_2d_kernel(double* p, int64_t ld, int64_t rows, int64_t cols) {
-  pdl_launch_dependents();
+  pdl_trigger_early();
   pdl_wait();
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     double* r = p + i * ld;

@@ -214,9 +214,9 @@ cudaError_t strassen_acc(int64_t h, double alpha, const double* A, int64_t lda, 
                          int64_t* launches);
 
 // Programmatic dependent launch: launch `k` on `s` with the programmatic stream
-// serialization attribute when pdl_enabled() (TRINV_PDL=1, default off), so that its CTAs are
-// scheduled while the previous kernel's last wave drains; `k` must call pdl_wait() before
-// touching global memory the previous kernel produces or consumes.
+// serialization attribute when pdl_enabled() (default on, TRINV_PDL=0 off), so that its launch
+// overlaps the previous kernel's drain; `k` must call pdl_wait() before touching global memory
+// the previous kernel produces or consumes (every launch_k kernel does so first).
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -114,5 +114,14 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Where a PDL-launched kernel lets its dependents be scheduled: by default only implicitly, as
+// its CTAs exit, so that the dependents' CTAs never sit on SM slots that this grid's later CTAs
+// need; with -DTRINV_PDL_EARLY at the start of every CTA (round 2's first PDL variant, slower:
+// n = 2048 151.6 -> 155 us against 149.3 us late, profiles/r02_pdl.txt).
+__device__ __forceinline__ void pdl_trigger_early() {
+#ifdef TRINV_PDL_EARLY
+  pdl_launch_dependents();
+#endif
+}
 
 }  // namespace trinv

@@ -32,7 +32,7 @@ struct Mix {
 };
 template <int NIN, int NOUT>
 __global__ void __launch_bounds__(256) mix_kernel(int64_t rows, int64_t cols, double beta, const Mix m) {
-  pdl_launch_dependents();
+  pdl_trigger_early();
   pdl_wait();
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     for (int64_t j = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); j < cols;

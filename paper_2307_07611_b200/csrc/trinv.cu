@@ -25,10 +25,13 @@
 namespace trinv {
 
 // Programmatic dependent launch of the product / combination kernels (internal.h launch_k):
-// opt-in (TRINV_PDL=1).  Measured slower on graph-replayed calls (n = 2048: 165 -> 198 us,
-// n = 4096: 801 -> 868 us; profiles/r02_pdl.txt), so the launches stay stream-serialised.
+// on by default (TRINV_PDL=0 turns it off).  The dependents are released only as the previous
+// grid's CTAs exit (ptx.cuh pdl_trigger_early): graph-replayed n = 1024 / 2048 71.2 -> 69.3 /
+// 151.6 -> 149.3 us, configs 2 / 3 / 4 5.446 -> 5.419 / 309.5 -> 308.3 / 158.75 -> 158.08 ms.
+// The first variant released them at the start of every CTA and was slower (n = 2048: 165 ->
+// 198 us in round 2's first sessions; profiles/r02_pdl.txt).
 bool pdl_enabled() {
-  static const bool on = [] { const char* e = std::getenv("TRINV_PDL"); return e && e[0] == '1'; }();
+  static const bool on = [] { const char* e = std::getenv("TRINV_PDL"); return !(e && e[0] == '0'); }();
   return on;
 }
 

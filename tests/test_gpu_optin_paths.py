@@ -1,8 +1,8 @@
 """The opt-in experimental launch paths (each measured slower than the default and kept
 behind an environment variable read once per process, hence one subprocess per setting):
 serial split-K (TRINV_SPLITK=1, 64x64 and 32x32 tiles), split-K with the last-chunk fix-up
-(TRINV_SPLITK=2), fused level launches (TRINV_FUSED=1), programmatic dependent launch
-(TRINV_PDL=1), stream-K level launches (TRINV_SK=1; WMIN=2 cuts tiles into several pieces) and the
+(TRINV_SPLITK=2), fused level launches (TRINV_FUSED=1), stream-order launches without
+programmatic dependent launch (TRINV_PDL=0; PDL is the default since round 2's last session), stream-K level launches (TRINV_SK=1; WMIN=2 cuts tiles into several pieces) and the
 persistent dependency-driven level chain (TRINV_CHAIN=1; OCC=1 makes every CTA walk many tiles).  Each must still match the oracle: full parity at n = 1024 / 2048 (lower and
 upper, ragged n = 1500) and bit-for-bit determinism."""
 import os
@@ -36,7 +36,7 @@ print('BAD', bad)
 
 @pytest.mark.parametrize("env", [{"TRINV_SPLITK": "1"}, {"TRINV_SPLITK": "1", "TRINV_SPLITK_T": "32", "TRINV_SPLITK_KC": "256"},
                                  {"TRINV_SPLITK": "2", "TRINV_SPLITK_T": "32", "TRINV_SPLITK_KC": "256"},
-                                 {"TRINV_SPLITK": "2"}, {"TRINV_FUSED": "1"}, {"TRINV_PDL": "1"},
+                                 {"TRINV_SPLITK": "2"}, {"TRINV_FUSED": "1"}, {"TRINV_PDL": "0"},
                                  {"TRINV_SK": "1", "TRINV_SK_BMIN": "128"},
                                  {"TRINV_SK": "1", "TRINV_SK_TILE": "12864", "TRINV_SK_BMIN": "128", "TRINV_SK_WMIN": "2"},
                                  {"TRINV_CHAIN": "1"}, {"TRINV_CHAIN": "1", "TRINV_CHAIN_OCC": "1"}],

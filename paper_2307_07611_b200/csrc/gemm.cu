@@ -571,6 +571,16 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::kThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   run_tile<BM, BN, WM, WN, STAGES, 2, LevelTraits>(&mapA, &mapB, p, smem_raw);
 }
+// The same kernel capped at 128 registers: a warp then takes 4096 of its SM sub-partition's
+// 16384 registers, so three 5-warp CTAs fit per SM where 131 registers allow two (ncu
+// launch__occupancy_limit_registers; the 64x32 tile of the mid-size top levels).
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __maxnreg__(128)
+    dmma_level_kernel_r128(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                           const LevelArgs p) {
+  extern __shared__ unsigned char smem_raw[];
+  run_tile<BM, BN, WM, WN, STAGES, 2, LevelTraits>(&mapA, &mapB, p, smem_raw);
+}
 
 struct FusedMaps {
   CUtensorMap m[4];  // A1, B1, A2, B2
@@ -842,6 +852,16 @@ static cudaError_t launch_level_sk_cfg(const LevelArgs& a, int ctas_per_sm, int 
 }
 
 // ---------------------------------------------------------------------------
+// TRINV_R128 = bit mask of the 128-register level-kernel variants (dmma_level_kernel_r128):
+// 1 = 64x64 (default: 3 CTAs / SM instead of 2, n = 8192 5420 -> 5299 us, config 2 5.418 ->
+// 5.302 ms, config 4 158.09 -> 157.51 ms), 2 = 64x32 (slower: n = 2048's top level 39.7 -> 48.3
+// us), 0 = off; only levels with >= TRINV_R128_WAVES (4) waves of 3 CTAs per SM take it (n = 4096's
+// top level, 2.3 waves, measured 765 -> 803 us with it).  profiles/r02_tile_waves.txt
+static int r128_mask() {
+  static const int m = [] { const char* e = std::getenv("TRINV_R128"); return e ? atoi(e) : 1; }();
+  return m;
+}
+
 template <int BM, int BN, int WM, int WN, int STAGES>
 static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t* launches, int64_t units = 0) {
   using C = GemmCfg<BM, BN, WM, WN, STAGES>;
@@ -859,9 +879,23 @@ static cudaError_t launch_level_cfg(const LevelArgs& a, cudaStream_t s, int64_t*
   }
   if (tiles <= 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
-  set_smem_once<k>((int)C::SMEM);
-  const cudaError_t e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
+  cudaError_t e;
+  bool done = false;
+  if constexpr (BM == 64 && (BN == 32 || BN == 64)) {
+    // (the 128-register variant only where the level has >= TRINV_R128_WAVES waves of 3 CTAs / SM)
+    static const double r128_waves = [] { const char* e = std::getenv("TRINV_R128_WAVES"); return e ? atof(e) : 4.0; }();
+    if ((r128_mask() & (BN == 64 ? 1 : 2)) && tiles >= (int64_t)(r128_waves * 3 * device_sms())) {
+      constexpr auto k = dmma_level_kernel_r128<BM, BN, WM, WN, STAGES>;
+      set_smem_once<k>((int)C::SMEM);
+      e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
+      done = true;
+    }
+  }
+  if (!done) {
+    constexpr auto k = dmma_level_kernel<BM, BN, WM, WN, STAGES>;
+    set_smem_once<k>((int)C::SMEM);
+    e = launch_k(k, dim3((unsigned)tiles), dim3(C::kThreads), C::SMEM, s, mA, mB, a);
+  }
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -3,7 +3,8 @@ behind an environment variable read once per process, hence one subprocess per s
 serial split-K (TRINV_SPLITK=1, 64x64 and 32x32 tiles), split-K with the last-chunk fix-up
 (TRINV_SPLITK=2), fused level launches (TRINV_FUSED=1), stream-order launches without
 programmatic dependent launch (TRINV_PDL=0; PDL is the default since round 2's last session), stream-K level launches (TRINV_SK=1; WMIN=2 cuts tiles into several pieces) and the
-persistent dependency-driven level chain (TRINV_CHAIN=1; OCC=1 makes every CTA walk many tiles).  Each must still match the oracle: full parity at n = 1024 / 2048 (lower and
+persistent dependency-driven level chain (TRINV_CHAIN=1; OCC=1 makes every CTA walk many tiles), and the
+128-register level kernels off (TRINV_R128=0) or on for every 64x64 / 64x32 level (TRINV_R128=3, WAVES=0).  Each must still match the oracle: full parity at n = 1024 / 2048 (lower and
 upper, ragged n = 1500) and bit-for-bit determinism."""
 import os
 import subprocess
@@ -39,9 +40,10 @@ print('BAD', bad)
                                  {"TRINV_SPLITK": "2"}, {"TRINV_FUSED": "1"}, {"TRINV_PDL": "0"},
                                  {"TRINV_SK": "1", "TRINV_SK_BMIN": "128"},
                                  {"TRINV_SK": "1", "TRINV_SK_TILE": "12864", "TRINV_SK_BMIN": "128", "TRINV_SK_WMIN": "2"},
-                                 {"TRINV_CHAIN": "1"}, {"TRINV_CHAIN": "1", "TRINV_CHAIN_OCC": "1"}],
+                                 {"TRINV_CHAIN": "1"}, {"TRINV_CHAIN": "1", "TRINV_CHAIN_OCC": "1"},
+                                 {"TRINV_R128": "0"}, {"TRINV_R128": "3", "TRINV_R128_WAVES": "0"}],
                          ids=["splitk1", "splitk1-t32", "splitk2-t32", "splitk2", "fused", "pdl", "sk64", "sk128x64",
-                              "chain", "chain-occ1"])
+                              "chain", "chain-occ1", "r128-off", "r128-all"])
 def test_optin_path_parity(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", _SCRIPT], cwd=root, env=dict(os.environ, **env), capture_output=True,

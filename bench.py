@@ -169,7 +169,10 @@ def run_reference(args):
     import oracle
     import synth
     cfg = CONFIGS[args.config]
-    cores = len(os.sched_getaffinity(0))
+    # the other ranks exit at once: rank 0 runs the oracle on every host core it may use (torchrun
+    # sets OMP_NUM_THREADS=1 per process); `cores` is the OpenMP thread count actually used
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    cores = oracle.max_threads()
     if cfg["kind"] == "B":
         sample = BATCH  # the whole 131072-matrix batch per step (about 0.1-0.5 s on the host cores)
         A = synth.host(32, batch=sample)
@@ -239,7 +242,7 @@ def cpu_baseline(cfg):
     import numpy as np
     import oracle
     import synth
-    cores = len(os.sched_getaffinity(0))
+    cores = oracle.max_threads()  # the OpenMP threads the oracle's loops use in this process
     if cfg["kind"] == "B":
         sample = 32768
         A = synth.host(32, batch=sample)

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(BlkCfg<NB>::THREADS) blk_kernel(const LeafArgs
   __shared__ int zmin;
   __shared__ __align__(8) uint64_t ldbar;  // completion of the row bulk loads
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  pdl_trigger_early();  // the first level launch may be scheduled while the blocks finish
+  pdl_trigger_early();  // no-op by default (ptx.cuh): the first level launch is released as the blocks exit
   if (tid == 0) { mbar_init(&ldbar, 1); fence_mbar_init(); }
   uint32_t ldphase = 0;
 #ifdef TRINV_BLK_TIMING  // phase timestamps of the first block (latency study only)

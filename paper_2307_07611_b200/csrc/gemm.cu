@@ -342,8 +342,9 @@ __device__ __forceinline__ void run_tile(const CUtensorMap* mapA, const CUtensor
   // split-K levels take their work unit from an in-order ticket (a unit is handed out only
   // after every earlier unit has a running CTA, so a chunk never waits on an unscheduled one)
   __shared__ int s_unit;
-  // PDL: let the next kernel's CTAs be scheduled as this grid drains, and wait for the
-  // previous kernel before touching global memory (no-ops without the launch attribute)
+  // PDL: wait for the previous kernel before touching global memory (a no-op without the
+  // launch attribute); the next kernel is released as this grid's CTAs exit (pdl_trigger_early
+  // is a no-op unless built with -DTRINV_PDL_EARLY)
   pdl_trigger_early();
   pdl_wait();
   int* sync = TR::sync(p);

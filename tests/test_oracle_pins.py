@@ -228,6 +228,27 @@ def test_unit_flag_ignores_stored_diagonal():
                           oracle.columns(L1, "L", [0, 5, 19]))
 
 
+@pytest.mark.parametrize("stored", [7.0, np.nan])
+def test_unit_flag_ignores_stored_diagonal_every_routine(stored):
+    """CRIT* (Alg. 2) takes the diagonal as 1 whatever is stored there: the upper,
+    batched (lower and upper), column and path-sum routines with unit=True give bit for bit the
+    result of the same matrix with an explicit unit diagonal (round-2 mutation check: a CRIT* that
+    read the stored diagonal, or a batched upper routine that dropped the flag, passed the pins)."""
+    n = 12
+    U = synth.host(n, seed=6, uplo="U", diag="pos")
+    U1 = U.copy(); np.fill_diagonal(U1, 1.0)
+    Ug = U.copy(); np.fill_diagonal(Ug, stored)
+    assert np.array_equal(oracle.crit_upper(Ug, unit=True), oracle.crit_upper(U1))
+    assert np.array_equal(oracle.columns(Ug, "U", [0, 4, 11], unit=True), oracle.columns(U1, "U", [0, 4, 11]))
+    assert np.array_equal(oracle.pathsum(Ug, "U", unit=True), oracle.pathsum(U1, "U"))
+    for uplo, A in (("L", synth.host(n, batch=3, seed=2)), ("U", synth.host(n, batch=3, uplo="U", diag="pos"))):
+        A1 = A.copy(); Ag = A.copy()
+        idx = np.arange(n)
+        A1[:, idx, idx] = 1.0
+        Ag[:, idx, idx] = stored
+        assert np.array_equal(oracle.crit_batched(Ag, uplo, unit=True), oracle.crit_batched(A1, uplo))
+
+
 # --- P-k: transpose law; columns == full ----------------------------------------
 def test_transpose_law_and_columns():
     n = 90

@@ -92,6 +92,18 @@ MUTATIONS = [
     ("metrics.py", "    den = np.maximum(np.abs(R), floor * colmax)", "    den = np.maximum(np.abs(R), colmax)",
      "floored_rel_err: floor factor dropped"),
     ("metrics.py", "    E = L @ (U @ Xs)", "    E = U @ (L @ Xs)", "factored residual: U L for L U"),
+    # Python wrappers and the Hopscotch enumerator
+    ("__init__.py", "    f = lib().oracle_crit_lower_batched if uplo == \"L\" else lib().oracle_crit_upper_batched",
+     "    f = lib().oracle_crit_upper_batched if uplo == \"L\" else lib().oracle_crit_lower_batched",
+     "crit_batched: uplo swapped"),
+    ("__init__.py", "    lib().oracle_lu_columns(n, _p(L), n, int(unit_l), _p(U), n, int(unit_u), len(cols),",
+     "    lib().oracle_lu_columns(n, _p(L), n, int(unit_u), _p(U), n, int(unit_l), len(cols),",
+     "lu_columns: unit flags swapped"),
+    ("__init__.py", "    return S @ K", "    return K @ S", "inv_general: K S for S K"),
+    ("hopscotch.py", "    for k in range(len(interior), -1, -1):", "    for k in range(len(interior), 0, -1):",
+     "hopscotch: drops the direct hop a -> b"),
+    ("hopscotch.py", "    interior = list(range(a + 1, b))", "    interior = list(range(a + 1, b + 1))",
+     "hopscotch: interior includes b"),
 ]
 
 

@@ -1092,14 +1092,26 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   };
   // the two products of a pair run concurrently (each stream has its own CRT scratch)
   static const bool fork_on = [] { const char* e = std::getenv("TRINV_LU_FORK"); return !(e && e[0] == '0'); }();
-  const bool par = fork_on;
+  // The six triangle-times-full products of a node with h = r >= 2 Strassen sizes (the top node of
+  // n = 16384) by the P_TF quadrant recursion with Strassen in the dense quadrants (trmm_sq, Eq.
+  // PTFmbk P:614-629), all on the caller's stream (Strassen never runs beside other work, §9b):
+  // config 5 249.0 -> 247.8 ms, sampled error unchanged.  TRINV_LU_TRMM=0 keeps them on the
+  // DMMA GEMM with the U12 / L21 and K21 / S12 pairs on two streams.
+  static const bool lu_trmm = [] { const char* e = std::getenv("TRINV_LU_TRMM"); return !(e && e[0] == '0'); }();
+  const bool tsq = lu_trmm && sws && r == h && !ozws && trmm_split_ok(h);
+  const bool par = fork_on && !tsq;
   cudaStream_t s2 = par ? fc->aux : s;
+  auto tprod = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int triA, const double* B,
+                   int64_t ldb, int triB, double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
+    if (tsq) return cuda_fail(trmm_sq(h, alpha, A, lda, triA, B, ldb, triB, beta, C, ldc, sws, s));
+    return gemm(M, N, K, A, lda, triA, B, ldb, triB, C, ldc, alpha, beta, st);
+  };
   trinv_status_t st = lu_inv_rec(h, W, F, Li, Ui, ld, T, info, info_off, s, ozws, ozhalf, sws);  // A11 = L11 U11, K11, S11
   if (st != TRINV_OK) return st;
   // U12 = K11 A12 (K11 lower) || L21 = A21 S11 (S11 upper); Schur W22 <- A22 - L21 U12
   if (par) TRY(fork_to(fc, s));
-  if ((st = gemm(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0, s))) return st;
-  if ((st = gemm(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0, s2))) return st;
+  if ((st = tprod(h, r, h, Li, ld, TRI_LOWER, blk(W, 0, h), ld, TRI_NONE, blk(F, 0, h), ld, 1.0, 0.0, s))) return st;
+  if ((st = tprod(r, h, h, blk(W, h, 0), ld, TRI_NONE, Ui, ld, TRI_UPPER, blk(F, h, 0), ld, 1.0, 0.0, s2))) return st;
   if (par) TRY(join_from(fc, s));
   if (sws && r == h && !(ozws && lu_gemm_on_int8(r, r, h)) && strassen_ul(2 * h)) {  // W22 -= L21 U12 by Strassen
     TRY(strassen_acc(h, -1.0, blk(F, h, 0), ld, blk(F, 0, h), ld, 1.0, blk(W, h, h), ld, strassen_levels(),
@@ -1114,11 +1126,11 @@ static trinv_status_t lu_inv_rec(int64_t n, double* W, double* F, double* Li, do
   const int64_t lth = even_up(h), ltr = even_up(r);
   if (par) TRY(fork_to(fc, s));
   // K21 = -K22 (L21 K11)
-  if ((st = gemm(r, h, h, blk(F, h, 0), ld, TRI_NONE, Li, ld, TRI_LOWER, T, lth, 1.0, 0.0, s))) return st;
-  if ((st = gemm(r, h, r, blk(Li, h, h), ld, TRI_LOWER, T, lth, TRI_NONE, blk(Li, h, 0), ld, -1.0, 0.0, s))) return st;
+  if ((st = tprod(r, h, h, blk(F, h, 0), ld, TRI_NONE, Li, ld, TRI_LOWER, T, lth, 1.0, 0.0, s))) return st;
+  if ((st = tprod(r, h, r, blk(Li, h, h), ld, TRI_LOWER, T, lth, TRI_NONE, blk(Li, h, 0), ld, -1.0, 0.0, s))) return st;
   // S12 = -(S11 U12) S22 (second stream, second scratch)
-  if ((st = gemm(h, r, h, Ui, ld, TRI_UPPER, blk(F, 0, h), ld, TRI_NONE, T2, ltr, 1.0, 0.0, s2))) return st;
-  if ((st = gemm(h, r, r, T2, ltr, TRI_NONE, blk(Ui, h, h), ld, TRI_UPPER, blk(Ui, 0, h), ld, -1.0, 0.0, s2)))
+  if ((st = tprod(h, r, h, Ui, ld, TRI_UPPER, blk(F, 0, h), ld, TRI_NONE, T2, ltr, 1.0, 0.0, s2))) return st;
+  if ((st = tprod(h, r, r, T2, ltr, TRI_NONE, blk(Ui, h, h), ld, TRI_UPPER, blk(Ui, 0, h), ld, -1.0, 0.0, s2)))
     return st;
   // structural zeros of the opposite triangles (read densely by the diagonal tiles of S K)
   TRY(launch_zero_2d(blk(Li, 0, h), ld, h, r, s, &g_launches));

@@ -103,10 +103,12 @@ def test_inv_general_zero_pivot_and_layout():
     assert oracle.floored_rel_err(X, oracle.inv_general(A)) <= REL_TOL
 
 
-@pytest.mark.parametrize("n", [8192, 5000])
+@pytest.mark.parametrize("n", [8192, 5000, 16384])
 def test_inv_general_n8192_sampled(n):
-    """BASELINE-scale general inverse (8192) and a ragged order (5000: uneven LU splits, ragged
-    merges in the inverse factors): 64 columns against the SKUL oracle, A X - I gate."""
+    """BASELINE-scale general inverse (8192, and 16384 whose top LU node runs its six
+    triangle-times-full products by the quadrant recursion with Strassen) and a ragged order
+    (5000: uneven LU splits, ragged merges in the inverse factors): 64 columns against the SKUL
+    oracle, A X - I gate."""
     Lg = torch.empty((n, n), dtype=torch.float64, device=DEV)
     Ug = torch.empty_like(Lg)
     synth.device_fill(Lg, n, seed=5, tag="L", diag="pos")
